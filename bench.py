@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the dense D3Q19 fp32 LBM step (BASELINE.json metric) on B200.
+
+    python bench.py --gpus N --steps K --warmup W [--impl ours|reference]
+
+Workload (BASELINE configs[1]): D3Q19 BGK lid-driven cavity, dense 512^3,
+fp32, DisagSoA layout, z-slab partitions with zero-copy halo; at N>1 the
+512^3 domain is split into N slabs, one per rank (strong scaling; --weak puts
+512^3 on every rank). A "step" is one collide-and-stream pass over the whole
+domain. The state is 2 x 10.2 GB of populations: far larger than L2, so no L2
+flush is needed between steps.
+
+One JSON line on rank 0: value = whole-job MLUPS with inputs resident in HBM,
+timed with CUDA events on the engine stream (max over ranks); e2e = the same
+metric through the reference-facing API with host buffers (canonical fp64 state
+uploaded, per-step diagnostics read back, final state downloaded); roofline of
+the step kernel; cpu_baseline = the reference library compiled from
+/root/reference (oracle/_ref) timed on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+Q = 19
+BYTES_PER_LUP = 2 * Q * 4  # fp32 D3Q19: each population read once and written once
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=512, help="cubic domain edge (512 = BASELINE configs[1])")
+    ap.add_argument("--weak", action="store_true", help="size^3 per GPU (configs[2]) instead of split")
+    ap.add_argument("--halo", default="zero_copy", choices=["zero_copy", "copy"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-size", type=int, default=0, help="domain edge of the e2e run (default: --size)")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.rows = []
+        self.marks = []
+        self._proc = None
+        self._t = None
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+
+    def _read(self):
+        for line in self._proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self):
+        self.marks.append(time.time())
+
+    def stop(self):
+        if self._proc:
+            time.sleep(0.25)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [r for t, r in self.rows if t0 - 0.15 <= t <= t1 + 0.15] or [r for _, r in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def traffic_from_profiles():
+    """dram bytes per launch of the dense step kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "dense_step_ncu.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("voxels_per_launch")
+    return None, None
+
+
+# ---- CPU reference (oracle/_ref: the reference library built from /root/reference) ----
+
+def cpu_reference_sample(threads: int, budget_s: float, edge: int = 128):
+    """Time reference fused_stream_collide sweeps (reference_dense_run's loop) on
+    `threads` independent edge^3 cavity replicas, one per host thread."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+
+    cfg = dict(lattice="D3Q19", domain=[edge] * 3, tau=0.56, scenario="lid_driven_cavity", velocity=[0.05, 0, 0],
+               steps=1)
+    init = O.ref_initial_state(cfg)
+    kind = "reference" if O.ref_available() else "port"
+    bufs = [[init.copy(), np.empty_like(init)] for _ in range(threads)]
+    js = json.dumps(cfg).encode()
+
+    def one(i):
+        a, b = bufs[i]
+        if kind == "reference":
+            O.ref_lib().vref_dense_steps_from(js, a, b)
+        else:
+            b[:] = O.port_dense_run("D3Q19", (edge,) * 3, 0.56, "lid_driven_cavity", (0.05, 0, 0), 1, state=a)
+        bufs[i] = [b, a]
+
+    with ThreadPoolExecutor(threads) as ex:
+        t0 = time.perf_counter()
+        list(ex.map(one, range(threads)))
+        t_one = time.perf_counter() - t0
+        steps = max(1, min(30, int(budget_s / max(t_one, 1e-3))))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            list(ex.map(one, range(threads)))
+        dt = time.perf_counter() - t0
+    mlups = threads * edge ** 3 * steps / dt / 1e6
+    return mlups, steps, dt, kind
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 64 << 30
+    cores = os.cpu_count() or 1
+    edge = 128
+    per = 2 * edge ** 3 * Q * 8
+    threads = max(1, min(cores, int(0.5 * avail // per)))
+    # size each step so that K + W steps finish in ~2-3 minutes
+    budget_total = 150.0
+    per_step_budget = budget_total / max(1, args.steps + args.warmup)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # noqa: F401
+
+    # calibrate: one sweep per thread
+    mlups, _, dt, kind = cpu_reference_sample(threads, 0.0, edge)
+    one_step = threads * edge ** 3 / (mlups * 1e6)
+    if one_step > per_step_budget:
+        edge = max(16, int(edge * (per_step_budget / one_step) ** (1 / 3)))
+    t_steps = []
+    mlups_all = []
+    for s in range(args.warmup + args.steps):
+        m, n, dt, kind = cpu_reference_sample(threads, 0.0, edge)
+        if s >= args.warmup:
+            mlups_all.append(m)
+            t_steps.append(threads * edge ** 3 / (m * 1e6))
+    value = statistics.median(mlups_all)
+    line = {
+        "metric": "MLUPS (D3Q19 fp32) at 1/2/4/8 B200 and % of HBM roofline vs CPU ref",
+        "impl": "reference", "value": round(value, 3), "unit": "MLUPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(t_steps), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (rest-equilibrium lid-driven cavity)",
+        "config": {"workload": f"D3Q19 BGK lid-driven cavity, reference CPU fused_stream_collide, "
+                               f"{threads} independent {edge}^3 replicas (one per host thread)",
+                   "lattice": "D3Q19", "tau": 0.56, "lid_u": [0.05, 0, 0]},
+        "cpu_baseline": {"value": round(value, 3), "unit": "MLUPS", "cores": threads, "kind": kind,
+                         "sample": f"{threads} x {edge}^3 cavity replicas, one fused_stream_collide sweep each "
+                                   f"per step (the reference is single-threaded; replicas fill the host cores)"},
+        "e2e": {"value": round(value, 3), "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ------------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_2503_07898_b200 as V
+
+    n = args.size
+    domain = (n, n, n * world) if args.weak else (n, n, n)
+    if world > 1:
+        from paper_2503_07898_b200 import multigpu
+
+        eng = multigpu.DistributedDense(domain=domain, precision="fp32", halo_mode=args.halo)
+    else:
+        eng = V.DenseEngine(domain=domain, precision="fp32", layout="DisagSoA", partitions=1,
+                            halo_mode=args.halo)
+    eng.set_equilibrium(1.0, (0.0, 0.0, 0.0))
+    voxels_total = domain[0] * domain[1] * domain[2]
+    voxels_local = eng.owned_voxels() if world > 1 else voxels_total
+
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    eng.timed_steps(args.warmup)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.time()
+    total_ms, kernel_ms = eng.timed_steps(args.steps)
+    torch.cuda.synchronize()
+    t1 = time.time()
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    clocks = None
+    if sampler:
+        sampler.stop()
+        clocks = sampler.summary(t0, t1)
+    diag = eng.probe()
+
+    value = voxels_total * args.steps / (total_ms / 1e3) / 1e6
+    peak, peak_kind = measured_peaks()
+    avg_kernel_ms = kernel_ms / args.steps
+    achieved = BYTES_PER_LUP * voxels_local / (avg_kernel_ms / 1e3) / 1e9
+    dram, vox_prof = traffic_from_profiles()
+    traffic = None
+    if dram and vox_prof:
+        traffic = round(dram / vox_prof * voxels_local)
+
+    e2e = None
+    if not args.no_e2e and world == 1 and rank == 0:
+        e2e = e2e_run(args, V, np)
+    cpu = None
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            mlups, steps, dt, kind = cpu_reference_sample(1, 12.0, 128)
+            cpu = {"value": round(mlups, 3), "unit": "MLUPS", "cores": 1, "kind": kind,
+                   "sample": f"D3Q19 cavity 128^3 (configs[0] size), {steps} reference_dense_run sweeps "
+                             f"(fused_stream_collide, fp64, single thread) in {dt:.1f} s"}
+        except Exception as exc:  # the checker is optional on the box; report why
+            cpu = {"value": None, "unit": "MLUPS", "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "MLUPS (D3Q19 fp32) at 1/2/4/8 B200 and % of HBM roofline vs CPU ref",
+            "value": round(value, 1), "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak" if (args.weak or world == 1) else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (rest-equilibrium lid-driven cavity, device-initialised)",
+            "config": {"workload": f"D3Q19 BGK lid-driven cavity dense {domain[0]}x{domain[1]}x{domain[2]} fp32, "
+                                   f"DisagSoA, {world} z-slab partition(s), {args.halo} halo",
+                       "domain": list(domain), "tau": 0.56, "lid_u": [0.05, 0, 0], "layout": "DisagSoA",
+                       "partitions": world, "halo": args.halo,
+                       "l2": "state 2x10.2 GB >> 126 MB L2; no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_kind": peak_kind,
+                         "bytes_per_lup": BYTES_PER_LUP, "voxels_per_launch": voxels_local,
+                         "avg_kernel_ms": round(avg_kernel_ms, 4),
+                         "frac_of_8tbs": round(achieved / 8000.0, 4)},
+            "clocks": clocks,
+            "gpu_launches": args.steps * (1 if world == 1 else 3),
+            "diag": {"mass": diag.mass, "max_speed": diag.max_speed, "unstable": diag.unstable},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_run(args, V, np):
+    """The same metric through the reference-facing API with host buffers:
+    fill_canonical from a pinned fp64 canonical host array, K steps each
+    followed by probe_field (diagnostics row D2H, as voxl::run does per step,
+    solver.cpp:245-255), and to_canonical of the final field."""
+    import torch
+
+    n = args.e2e_size or args.size
+    dom = (n, n, n)
+    vox = n ** 3
+    eng = V.DenseEngine(domain=dom, precision="fp32", layout="DisagSoA", partitions=1)
+    host_in = torch.empty(vox * Q, dtype=torch.float64, pin_memory=True).numpy()
+    host_out = torch.empty(vox * Q, dtype=torch.float64, pin_memory=True).numpy()
+    # rest-equilibrium canonical input (initial_canonical_state, solver.cpp:165-187)
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    host_in.reshape(vox, Q)[:] = w
+    steps = args.steps
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.set_canonical(host_in)
+    for _ in range(steps):
+        eng.step(1)
+        eng.probe()
+    eng.get_canonical(host_out)
+    dt = time.perf_counter() - t0
+    eng.close()
+    bytes_in = vox * Q * 8
+    bytes_out = vox * Q * 8 + steps * 32
+    return {"value": round(vox * steps / dt / 1e6, 1), "unit": "MLUPS",
+            "h2d_bytes_per_step": int(bytes_in / steps), "d2h_bytes_per_step": int(bytes_out / steps),
+            "domain": list(dom), "seconds": round(dt, 3),
+            "path": "DenseEngine.set_canonical(host fp64) + steps x (step + probe) + get_canonical(host fp64)"}
+
+
+if __name__ == "__main__":
+    main()

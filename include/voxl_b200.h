@@ -1,0 +1,143 @@
+/* voxl_b200.h -- C-ABI of the B200-native disaggregated LBM engines.
+ *
+ * Plain C: opaque handles, plain pointers and sizes, int status codes. No torch
+ * or CUDA types cross this boundary (a stream is exposed as void*).
+ *
+ * Each entry point names the reference interface it replaces (paths relative to
+ * /root/reference/proj). The reference is a C++20 library with no FFI of its
+ * own; these are the symbols a maintainer binds from the reference-side
+ * drivers (see INTEGRATION.md for the C++ binding that keeps the reference's
+ * class names and exceptions).
+ *
+ * Errors: every call returns VOXL_OK (0) or a status; voxl_last_error() gives
+ * the message of the calling thread's last failure, with the reference's
+ * message text (e.g. "run aborted at step N: ...").
+ */
+#ifndef VOXL_B200_H
+#define VOXL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mirror the reference's exception types) ------------------- */
+#define VOXL_OK 0
+#define VOXL_INVALID_ARGUMENT 1 /* std::invalid_argument / ConfigError        */
+#define VOXL_OUT_OF_RANGE 2     /* std::out_of_range (layout.cpp:156)          */
+#define VOXL_RUNTIME 3          /* std::runtime_error (structure / links)      */
+#define VOXL_INSTABILITY 4      /* instability / run aborted at step N         */
+#define VOXL_CUDA_ERROR 5       /* CUDA runtime failure                        */
+#define VOXL_DOMAIN 6           /* std::domain_error (lattice.cpp:106)         */
+
+/* ---- enums (values equal the reference's enum order) ------------------------- */
+#define VOXL_D2Q9 0  /* LatticeKind (lattice.hpp:10) */
+#define VOXL_D3Q19 1
+#define VOXL_D3Q27 2
+#define VOXL_AOS 0   /* LayoutScheme (layout.hpp:14) */
+#define VOXL_SOA 1
+#define VOXL_DISAG_SOA 2
+#define VOXL_CAVITY 0   /* Scenario (solver.hpp:16) */
+#define VOXL_OBSTACLE 1
+#define VOXL_PERIODIC 2
+#define VOXL_F32 0
+#define VOXL_F64 1      /* bitwise parity mode */
+#define VOXL_HALO_ZERO_COPY 0 /* shared-layer kernel stores into the neighbour halo */
+#define VOXL_HALO_COPY 1      /* span copies after the step (halo_update)          */
+#define VOXL_NAIVE 0          /* sparse::Strategy (sparse.hpp:117) */
+#define VOXL_DISAG_BITMASK 1
+#define VOXL_DISAG_MEM 2
+
+const char* voxl_last_error(void);
+int voxl_version(void);
+/** Lattice descriptor as the reference's lattice_to_json (lattice.cpp:140-158). */
+int voxl_lattice_json(int lattice, char* out, int64_t cap, int64_t* len);
+
+/* ---- dense grid layer (layout.hpp / partition.hpp) ----------------------------- */
+
+/** LayoutMap::build(scheme, shape, q, axis, TransferSets::for_lattice).to_json()
+ *  (layout.cpp:72, :203). lattice < 0: generic build with `cardinality`. */
+int voxl_layout_json(int scheme, int nx, int ny, int nz, int lattice, int cardinality, int axis, char* out,
+                     int64_t cap, int64_t* len);
+/** LayoutMap::address for every (voxel, component), voxels k = -1..n (partition
+ *  axis), cross-section row-major, component innermost (layout.cpp:149). */
+int voxl_layout_addresses(int scheme, int nx, int ny, int nz, int lattice, int axis, int64_t* out, int64_t cap,
+                          int64_t* count);
+/** decompose (partition.cpp:20): slabs[2p], slabs[2p+1] = [begin, end). */
+int voxl_decompose(int nx, int ny, int nz, int parts, int axis, int periodic, int* slabs);
+/** classify_voxels (partition.cpp:43): 0 Private / 1 Shared per owned voxel. */
+int voxl_classify_voxels(int nx, int ny, int nz, int parts, int axis, int periodic, int p, uint8_t* out,
+                         int64_t cap);
+
+/* ---- dense engine (PartitionedField + step_occ + GatherKernel) ------------------ */
+
+typedef struct voxl_dense voxl_dense;
+
+typedef struct {
+    int lattice;          /* VOXL_D2Q9 | VOXL_D3Q19 | VOXL_D3Q27 */
+    int nx, ny, nz;       /* SolverConfig::domain (solver.hpp:29) */
+    double tau;
+    int scenario;         /* VOXL_CAVITY | VOXL_PERIODIC */
+    double velocity[3];   /* lid velocity */
+    int layout;           /* VOXL_AOS | VOXL_SOA | VOXL_DISAG_SOA */
+    int partitions;       /* 1D slab count along z (y in 2D) */
+    int precision;        /* VOXL_F32 | VOXL_F64 */
+    int halo_mode;        /* VOXL_HALO_ZERO_COPY | VOXL_HALO_COPY */
+    int first_partition;  /* owned range for multi-process use ... */
+    int local_partitions; /* ... -1 = all partitions in this process */
+} voxl_dense_desc;
+
+typedef struct {
+    double mass;          /* lbm::Diagnostics (lbm.hpp:137-141) */
+    double max_speed;
+    int unstable;         /* probe_field would throw (lbm.cpp:124-128) */
+    int bad_population;
+    int64_t bad_voxel;
+} voxl_diag;
+
+typedef struct {
+    int step, src, dst;   /* TransferRecord (partition.hpp:35-41) */
+    int64_t src_base, dst_base, elements;
+} voxl_transfer_record;
+
+/** PartitionedField x2 (partition.cpp:111) on the current device. */
+int voxl_dense_create(const voxl_dense_desc* desc, voxl_dense** out);
+int voxl_dense_destroy(voxl_dense* h);
+/** fill_canonical (partition.cpp:143): canonical fp64, x fastest, component innermost. */
+int voxl_dense_set_canonical(voxl_dense* h, const double* host);
+/** make_equilibrium_state (lbm.cpp:72): every voxel at equilibrium(rho, u), on the device. */
+int voxl_dense_set_equilibrium(voxl_dense* h, double rho, const double* u);
+/** to_canonical (partition.cpp:123). */
+int voxl_dense_get_canonical(voxl_dense* h, double* host);
+/** Planes [k_begin, k_end) of the partition axis only (chunked I/O). */
+int voxl_dense_set_planes(voxl_dense* h, const double* host, int k_begin, int k_end);
+int voxl_dense_get_planes(voxl_dense* h, double* host, int k_begin, int k_end);
+/** n x step_occ(a, b, GatherKernel) (partition.hpp:173) then error check. */
+int voxl_dense_step(voxl_dense* h, int n);
+/** Enqueue n steps on the engine stream; no host synchronisation. */
+int voxl_dense_enqueue(voxl_dense* h, int n);
+int voxl_dense_synchronize(voxl_dense* h);
+/** n steps timed with CUDA events on the engine stream: total span and the
+ *  sum of per-step (kernel) spans, in milliseconds. */
+int voxl_dense_timed_steps(voxl_dense* h, int n, double* total_ms, double* kernel_ms);
+/** probe_field on the current state (lbm.cpp:116), on the device. */
+int voxl_dense_probe(voxl_dense* h, voxl_diag* out);
+/** Ledger records of one step in the reference's order (partition.cpp:163-206). */
+int voxl_dense_ledger(voxl_dense* h, int step, voxl_transfer_record* out, int cap, int* count);
+/** The same records from a descriptor alone (no device needed). */
+int voxl_dense_plan_ledger(const voxl_dense_desc* desc, int step, voxl_transfer_record* out, int cap, int* count);
+int voxl_dense_layout_json(voxl_dense* h, int partition, char* out, int64_t cap, int64_t* len);
+int voxl_dense_steps_done(voxl_dense* h, int* steps);
+/** Device buffer of a partition: which 0 = current, 1 = next. */
+int voxl_dense_buffer(voxl_dense* h, int partition, int which, void** ptr, size_t* bytes);
+/** cudaStream_t of the engine, as void*. */
+int voxl_dense_stream(voxl_dense* h, void** stream);
+/** Multi-process: map a neighbour partition's buffers (IPC/peer pointers, both parities). */
+int voxl_dense_attach_peer(voxl_dense* h, int partition, void* buf0, void* buf1);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

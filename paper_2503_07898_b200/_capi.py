@@ -1,0 +1,131 @@
+"""ctypes binding of include/voxl_b200.h (the C-ABI of libvoxl_b200.so).
+
+The product path loads ONLY the in-tree CUDA library. If it is missing the
+import fails loudly -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libvoxl_b200.so")
+
+# status codes (voxl_b200.h)
+OK, INVALID_ARGUMENT, OUT_OF_RANGE, RUNTIME, INSTABILITY, CUDA_ERROR, DOMAIN = range(7)
+
+
+class VoxlError(RuntimeError):
+    """Base of the exceptions raised for non-zero C-ABI status codes."""
+
+
+class VoxlInvalidArgument(VoxlError, ValueError):
+    pass
+
+
+class VoxlOutOfRange(VoxlError, IndexError):
+    pass
+
+
+class VoxlInstability(VoxlError):
+    pass
+
+
+class VoxlCudaError(VoxlError):
+    pass
+
+
+class VoxlDomainError(VoxlError, ArithmeticError):
+    pass
+
+
+_EXC = {INVALID_ARGUMENT: VoxlInvalidArgument, OUT_OF_RANGE: VoxlOutOfRange, RUNTIME: VoxlError,
+        INSTABILITY: VoxlInstability, CUDA_ERROR: VoxlCudaError, DOMAIN: VoxlDomainError}
+
+
+class DenseDesc(C.Structure):
+    _fields_ = [("lattice", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("tau", C.c_double),
+                ("scenario", C.c_int), ("velocity", C.c_double * 3), ("layout", C.c_int), ("partitions", C.c_int),
+                ("precision", C.c_int), ("halo_mode", C.c_int), ("first_partition", C.c_int),
+                ("local_partitions", C.c_int)]
+
+
+class Diag(C.Structure):
+    _fields_ = [("mass", C.c_double), ("max_speed", C.c_double), ("unstable", C.c_int),
+                ("bad_population", C.c_int), ("bad_voxel", C.c_int64)]
+
+
+class TransferRecordC(C.Structure):
+    _fields_ = [("step", C.c_int), ("src", C.c_int), ("dst", C.c_int), ("src_base", C.c_int64),
+                ("dst_base", C.c_int64), ("elements", C.c_int64)]
+
+
+class SparseDesc(C.Structure):
+    _fields_ = [("lattice", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("tau", C.c_double),
+                ("u_bc", C.c_double * 3), ("block_edge", C.c_int), ("strategy", C.c_int), ("precision", C.c_int),
+                ("kernel_split", C.c_int)]
+
+
+class MresDesc(C.Structure):
+    _fields_ = [("lattice", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("levels", C.c_int),
+                ("tau", C.c_double), ("velocity", C.c_double * 3), ("fused", C.c_int), ("precision", C.c_int),
+                ("block_edge", C.c_int)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i64, cp = C.c_void_p, C.c_int64, C.c_char_p
+    sigs = {
+        "voxl_last_error": ([], cp),
+        "voxl_version": ([], C.c_int),
+        "voxl_lattice_json": ([C.c_int, cp, i64, C.POINTER(i64)], C.c_int),
+        "voxl_layout_json": ([C.c_int] * 7 + [cp, i64, C.POINTER(i64)], C.c_int),
+        "voxl_layout_addresses": ([C.c_int] * 6 + [vp, i64, C.POINTER(i64)], C.c_int),
+        "voxl_decompose": ([C.c_int] * 6 + [vp], C.c_int),
+        "voxl_classify_voxels": ([C.c_int] * 7 + [vp, i64], C.c_int),
+        "voxl_dense_create": ([C.POINTER(DenseDesc), C.POINTER(vp)], C.c_int),
+        "voxl_dense_destroy": ([vp], C.c_int),
+        "voxl_dense_set_canonical": ([vp, vp], C.c_int),
+        "voxl_dense_get_canonical": ([vp, vp], C.c_int),
+        "voxl_dense_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
+        "voxl_dense_set_planes": ([vp, vp, C.c_int, C.c_int], C.c_int),
+        "voxl_dense_get_planes": ([vp, vp, C.c_int, C.c_int], C.c_int),
+        "voxl_dense_step": ([vp, C.c_int], C.c_int),
+        "voxl_dense_enqueue": ([vp, C.c_int], C.c_int),
+        "voxl_dense_synchronize": ([vp], C.c_int),
+        "voxl_dense_timed_steps": ([vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+        "voxl_dense_probe": ([vp, C.POINTER(Diag)], C.c_int),
+        "voxl_dense_ledger": ([vp, C.c_int, vp, C.c_int, C.POINTER(C.c_int)], C.c_int),
+        "voxl_dense_plan_ledger": ([C.POINTER(DenseDesc), C.c_int, vp, C.c_int, C.POINTER(C.c_int)], C.c_int),
+        "voxl_dense_layout_json": ([vp, C.c_int, cp, i64, C.POINTER(i64)], C.c_int),
+        "voxl_dense_steps_done": ([vp, C.POINTER(C.c_int)], C.c_int),
+        "voxl_dense_buffer": ([vp, C.c_int, C.c_int, C.POINTER(vp), C.POINTER(C.c_size_t)], C.c_int),
+        "voxl_dense_stream": ([vp, C.POINTER(vp)], C.c_int),
+        "voxl_dense_attach_peer": ([vp, C.c_int, vp, vp], C.c_int),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    if status != OK:
+        msg = lib.voxl_last_error().decode()
+        raise _EXC.get(status, VoxlError)(msg)
+
+
+def text(fn, *args) -> str:
+    n = C.c_int64()
+    check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(fn(*args, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()

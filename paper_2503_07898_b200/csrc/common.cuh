@@ -1,0 +1,36 @@
+// common.cuh -- error plumbing shared by the engines and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace voxl_b200 {
+
+/// Status codes of the C-ABI (include/voxl_b200.h).
+enum Status : int {
+    kOk = 0,
+    kInvalidArgument = 1,  // std::invalid_argument in the reference
+    kOutOfRange = 2,       // std::out_of_range
+    kRuntime = 3,          // std::runtime_error (structure errors, asymmetric links)
+    kInstability = 4,      // "instability at step N" / "run aborted at step N"
+    kCuda = 5,             // CUDA runtime failure
+    kDomain = 6,           // std::domain_error (non-finite equilibrium input)
+};
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct InstabilityError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define VOXL_CUDA(call) ::voxl_b200::cuda_check((call), #call)
+
+} // namespace voxl_b200

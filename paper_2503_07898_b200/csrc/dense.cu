@@ -1,0 +1,717 @@
+// dense.cu -- dense pull + BGK kernels and the partitioned engine (see dense.cuh).
+//
+// Hot kernel: dense_step_kernel. One thread per voxel; a block is 128 voxels of
+// one cross-section row, so each warp reads 32 consecutive values of a
+// population plane (x-shifted by at most one element: the overfetched sector
+// is the neighbouring warp's and hits L2) and writes 128 B aligned runs. Every
+// stored population is read exactly once and written exactly once per step:
+// algorithmic traffic is 2*Q*sizeof(real) bytes per lattice update (152 B for
+// D3Q19 fp32), the HBM roofline of this operator.
+#include "dense.cuh"
+#include "lattice.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <numeric>
+
+namespace voxl_b200 {
+
+namespace {
+
+constexpr int kBlock = 128;
+
+template <int Q, class R>
+struct StepArgs {
+    const R* in;
+    R* out;
+    long long plane[kGroupCount][Q];  // element offset per (group, component)
+    R* up_out;                        // upper neighbour's next buffer (its LowerHalo), or null
+    long long up_plane[Q];
+    unsigned up_mask;
+    R* low_out;                       // lower neighbour's next buffer (its UpperHalo), or null
+    long long low_plane[Q];
+    unsigned low_mask;
+    R lid[Q];  // moving-wall term per direction (lbm.hpp:66-69), 0 where unused
+    R omega, keep;
+    int na, nb, n, s;
+    int k_first, k_step;
+    int kg0, nk;
+    int wall_a, wall_b, wall_k;
+    int periodic_a, periodic_b;
+    int has_lid;
+    int step;
+    int* error_flag;
+};
+
+__device__ __forceinline__ int group_of(int k, int n) {
+    return k == -1 ? 0 : (k == 0 ? 1 : (k == n - 1 ? 3 : (k == n ? 4 : 2)));
+}
+
+template <class R>
+__device__ __forceinline__ R ld_ro(const R* p) {
+    return __ldg(p);
+}
+
+/// Fused pull-stream + bounce-back/lid + BGK for one voxel per thread
+/// (gather_pull lbm.hpp:40-74 then bgk_relax lattice.cpp:131-138).
+/// AXIS is the partition axis (2 in 3D, 1 in 2D); `a` is x, `b` the remaining
+/// cross-section axis, `k` the local coordinate along AXIS.
+template <class L, class R, bool Exact, bool AOS, int AXIS, bool WRAP>
+__global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constant__ StepArgs<L::Q, R> A) {
+    constexpr int Q = L::Q;
+    constexpr int OTHER = AXIS == 2 ? 1 : 2;
+    using Ar = Arith<R, Exact>;
+    const int a = blockIdx.x * kBlock + threadIdx.x;
+    if (a >= A.na) return;
+    const int b = blockIdx.y;
+    const int k = A.k_first + int(blockIdx.z) * A.k_step;
+    const int kg = A.kg0 + k;
+    const int na = A.na, s = A.s;
+    const int cross = b * na + a;
+    const int lin = (k + 1) * s + cross;
+    const int gm = group_of(k - 1, A.n), g0 = group_of(k, A.n), gp = group_of(k + 1, A.n);
+
+    const bool a_lo = A.wall_a && a == 0, a_hi = A.wall_a && a == na - 1;
+    const bool b_lo = A.wall_b && b == 0, b_hi = A.wall_b && b == A.nb - 1;
+    const bool k_lo = A.wall_k && kg == 0, k_hi = A.wall_k && kg == A.nk - 1;
+    constexpr long long VS = AOS ? Q : 1;
+
+    R f[Q];
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int ea = L::e(i, 0), eb = L::e(i, OTHER), ek = L::e(i, AXIS);
+        bool oob = false;
+        if constexpr (ea > 0) oob = oob || a_lo;
+        if constexpr (ea < 0) oob = oob || a_hi;
+        if constexpr (eb > 0) oob = oob || b_lo;
+        if constexpr (eb < 0) oob = oob || b_hi;
+        if constexpr (ek > 0) oob = oob || k_lo;
+        if constexpr (ek < 0) oob = oob || k_hi;
+        int src_lin;
+        if constexpr (WRAP) {
+            int sa = a - ea, sb = b - eb;
+            if (A.periodic_a) sa = sa < 0 ? sa + na : (sa >= na ? sa - na : sa);
+            if (A.periodic_b) sb = sb < 0 ? sb + A.nb : (sb >= A.nb ? sb - A.nb : sb);
+            src_lin = (k - ek + 1) * s + sb * na + sa;
+        } else {
+            src_lin = lin - ea - eb * na - ek * s;
+        }
+        constexpr int sel = ek > 0 ? 0 : (ek < 0 ? 2 : 1);
+        const int gs = sel == 0 ? gm : (sel == 2 ? gp : g0);
+        const R* p_src = A.in + A.plane[gs][i] + (long long)src_lin * VS;
+        constexpr int oi = L::opp(i);
+        const R* p_own = A.in + A.plane[g0][oi] + (long long)lin * VS;
+        R v = ld_ro(oob ? p_own : p_src);
+        if constexpr (ek < 0) {
+            if (A.has_lid && k_hi) v = Ar::add(v, A.lid[i]);
+        }
+        f[i] = v;
+    });
+
+    bool ok = true;
+    R rho, u[3];
+    bgk_relax<L, R, Exact>(f, A.omega, A.keep, rho, u, ok);
+    if (!ok) atomicMin(A.error_flag, A.step);
+
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        A.out[A.plane[g0][i] + (long long)lin * VS] = f[i];
+    });
+    // Zero-copy halo: the shared layers store their face-crossing populations
+    // directly into the neighbour's halo group of its next buffer
+    // (halo_update partition.cpp:196-205 without the copy).
+    if (k == 0 && A.up_out) {
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            if ((A.up_mask >> i) & 1u) A.up_out[A.up_plane[i] + (long long)cross * VS] = f[i];
+        });
+    }
+    if (k == A.n - 1 && A.low_out) {
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            if ((A.low_mask >> i) & 1u) A.low_out[A.low_plane[i] + (long long)cross * VS] = f[i];
+        });
+    }
+}
+
+// ---- canonical <-> layout -----------------------------------------------------------
+
+template <int Q>
+struct CanonArgs {
+    long long plane[kGroupCount][Q];
+    long long vs;
+    int na, s, n;
+    int k_lo, k_hi;   // local k range being moved
+    int kg_stage0;    // global k of staging plane 0
+    int kg0;          // partition's global offset
+};
+
+template <int Q, class R, bool ToDevice>
+__global__ void canon_kernel(R* buf, double* staging, const __grid_constant__ CanonArgs<Q> A) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long count = (long long)(A.k_hi - A.k_lo) * A.s;
+    if (t >= count) return;
+    const int k = A.k_lo + int(t / A.s);
+    const int cross = int(t % A.s);
+    const int g = group_of(k, A.n);
+    const long long lin = (long long)(k + 1) * A.s + cross;
+    const long long st = ((long long)(A.kg0 + k - A.kg_stage0) * A.s + cross) * Q;
+    for (int c = 0; c < Q; ++c) {
+        R* p = buf + A.plane[g][c] + lin * A.vs;
+        if constexpr (ToDevice) *p = R(staging[st + c]);
+        else staging[st + c] = double(*p);
+    }
+}
+
+/// Uniform state over every voxel of the partition, halos included
+/// (make_equilibrium_state lbm.cpp:72-83 / initial_canonical_state's rest case).
+template <int Q, class R>
+__global__ void fill_kernel(R* buf, const __grid_constant__ CanonArgs<Q> A, const __grid_constant__ StepArgs<Q, R> V) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long count = (long long)(A.n + 2) * A.s;
+    if (t >= count) return;
+    const int k = int(t / A.s) - 1;
+    const int cross = int(t % A.s);
+    const int g = group_of(k, A.n);
+    const long long lin = (long long)(k + 1) * A.s + cross;
+    for (int c = 0; c < Q; ++c) buf[A.plane[g][c] + lin * A.vs] = V.lid[c];
+}
+
+// ---- diagnostics (probe_field, lbm.cpp:116-138) ------------------------------------
+
+constexpr int kProbeBlocks = 592;  // 4 x 148 SMs
+constexpr int kProbeThreads = 256;
+
+template <class L, class R>
+__global__ void __launch_bounds__(kProbeThreads) probe_kernel(const R* buf, const __grid_constant__ CanonArgs<L::Q> A,
+                                                            double* partial, unsigned long long* bad) {
+    constexpr int Q = L::Q;
+    const long long count = (long long)A.n * A.s;
+    double mass = 0.0, vmax = 0.0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int k = int(t / A.s), cross = int(t % A.s);
+        const int g = group_of(k, A.n);
+        const long long lin = (long long)(k + 1) * A.s + cross;
+        double f[Q];
+        double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+        bool bad_here = false;
+        int bad_pop = 0;
+        for (int c = 0; c < Q; ++c) {
+            f[c] = double(buf[A.plane[g][c] + lin * A.vs]);
+            if (!bad_here && (!isfinite(f[c]) || fabs(f[c]) > 1e3)) {
+                bad_here = true;
+                bad_pop = c;
+            }
+        }
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            mass += f[i];
+            r += f[i];
+            mx = acc_term<double, false, L::ex(i)>(mx, f[i]);
+            my = acc_term<double, false, L::ey(i)>(my, f[i]);
+            mz = acc_term<double, false, L::ez(i)>(mz, f[i]);
+        });
+        if (bad_here || !(r > 0.0)) {
+            const unsigned long long canon = (unsigned long long)(A.kg0 + k) * A.s + cross;
+            atomicMin(bad, (canon << 5) | (unsigned long long)bad_pop);
+        } else {
+            const double ux = mx / r, uy = my / r, uz = mz / r;
+            vmax = fmax(vmax, sqrt(ux * ux + uy * uy + uz * uz));
+        }
+    }
+    __shared__ double sm[kProbeThreads], sv[kProbeThreads];
+    sm[threadIdx.x] = mass;
+    sv[threadIdx.x] = vmax;
+    __syncthreads();
+    for (int w = kProbeThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sm[threadIdx.x] += sm[threadIdx.x + w];
+            sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = sm[0];
+        partial[2 * blockIdx.x + 1] = sv[0];
+    }
+}
+
+__global__ void probe_final_kernel(const double* partial, int n, double* out) {
+    // fixed-order reduction: deterministic run to run
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double m = 0.0, v = 0.0;
+        for (int i = 0; i < n; ++i) {
+            m += partial[2 * i];
+            v = fmax(v, partial[2 * i + 1]);
+        }
+        out[0] += m;
+        out[1] = fmax(out[1], v);
+    }
+}
+
+// ---- launch plumbing ------------------------------------------------------------------
+
+template <class L>
+constexpr int axis_of() {
+    return L::dim == 3 ? 2 : 1;
+}
+
+struct PartGeom {
+    int na, nb, n, s, kg0, nk;
+};
+
+PartGeom geom_of(const Decomposition& d, int p) {
+    PartGeom g{};
+    const int axis = d.axis;
+    const int other = axis == 2 ? 1 : 2;
+    g.na = d.domain[0];
+    g.nb = d.domain[other];
+    g.n = d.thickness(p);
+    g.s = g.na * g.nb;
+    g.kg0 = d.slabs[p].first;
+    g.nk = d.domain[axis];
+    return g;
+}
+
+template <class L, class R, bool Exact>
+struct DenseOps {
+    static constexpr int Q = L::Q;
+    static constexpr int AXIS = axis_of<L>();
+
+    static void fill_planes(const LayoutMap& m, long long (&plane)[kGroupCount][Q]) {
+        for (int g = 0; g < kGroupCount; ++g)
+            for (int c = 0; c < Q; ++c) plane[g][c] = m.plane_offset(g, c);
+    }
+
+    static void launch_step(const DenseConfig& cfg, const Decomposition& d, const std::vector<LayoutMap>& maps,
+                            int p, const void* in, void* out, void* up_out, void* low_out, bool wrap,
+                            int step, int* error_flag, int k_first, int k_step, int k_count, cudaStream_t st) {
+        StepArgs<Q, R> A{};
+        const PartGeom g = geom_of(d, p);
+        A.in = static_cast<const R*>(in);
+        A.out = static_cast<R*>(out);
+        fill_planes(maps[p], A.plane);
+        const bool aos = maps[p].scheme() == LayoutScheme::AoS;
+        const int up = d.upper_neighbor(p), low = d.lower_neighbor(p);
+        A.up_out = static_cast<R*>(up_out);
+        A.low_out = static_cast<R*>(low_out);
+        A.up_mask = A.low_mask = 0;
+        if (up >= 0 && up_out) {
+            const LayoutMap& nm = maps[up];
+            const std::vector<int>& comps = nm.transfer().down;
+            for (int c = 0; c < Q; ++c) {
+                const bool send = aos || std::find(comps.begin(), comps.end(), c) != comps.end();
+                if (send) A.up_mask |= 1u << c;
+                // neighbour's LowerHalo, k = n_up: lin = (n_up + 1) * s + cross
+                A.up_plane[c] = nm.plane_offset(int(GroupTag::LowerHalo), c) +
+                                (long long)(nm.shape()[d.axis] + 1) * g.s * nm.voxel_stride();
+            }
+        }
+        if (low >= 0 && low_out) {
+            const LayoutMap& nm = maps[low];
+            const std::vector<int>& comps = nm.transfer().up;
+            for (int c = 0; c < Q; ++c) {
+                const bool send = aos || std::find(comps.begin(), comps.end(), c) != comps.end();
+                if (send) A.low_mask |= 1u << c;
+                A.low_plane[c] = nm.plane_offset(int(GroupTag::UpperHalo), c);  // k = -1: lin = cross
+            }
+        }
+        const bool lid = cfg.scenario == Scenario::LidDrivenCavity;
+        for (int i = 0; i < Q; ++i) {
+            // (((2.0 * w_i) * 1.0) * 3.0) * eu, eu = (ex*u0 + ey*u1) + ez*u2 (lbm.hpp:66-69)
+            const double eu = double(L::ex(i)) * cfg.velocity[0] + double(L::ey(i)) * cfg.velocity[1] +
+                              double(L::ez(i)) * cfg.velocity[2];
+            A.lid[i] = R(2.0 * L::w(i) * 1.0 * 3.0 * eu);
+        }
+        const double inv_tau = 1.0 / cfg.tau;
+        if constexpr (Exact) {
+            A.omega = R(inv_tau);
+            A.keep = R(1.0 - inv_tau);
+        } else {
+            A.omega = R(inv_tau);
+            A.keep = R(1.0) - R(inv_tau);
+        }
+        A.na = g.na;
+        A.nb = g.nb;
+        A.n = g.n;
+        A.s = g.s;
+        A.k_first = k_first;
+        A.k_step = k_step;
+        A.kg0 = g.kg0;
+        A.nk = g.nk;
+        const bool periodic = cfg.scenario == Scenario::PeriodicBox;
+        A.wall_a = !periodic;
+        A.wall_b = !periodic && L::dim == 3;
+        A.wall_k = !periodic;
+        A.periodic_a = periodic;
+        A.periodic_b = periodic && L::dim == 3;
+        A.has_lid = lid;
+        A.step = step;
+        A.error_flag = error_flag;
+        const dim3 grid((g.na + kBlock - 1) / kBlock, g.nb, k_count);
+        if (aos) {
+            if (wrap) dense_step_kernel<L, R, Exact, true, AXIS, true><<<grid, kBlock, 0, st>>>(A);
+            else dense_step_kernel<L, R, Exact, true, AXIS, false><<<grid, kBlock, 0, st>>>(A);
+        } else {
+            if (wrap) dense_step_kernel<L, R, Exact, false, AXIS, true><<<grid, kBlock, 0, st>>>(A);
+            else dense_step_kernel<L, R, Exact, false, AXIS, false><<<grid, kBlock, 0, st>>>(A);
+        }
+        VOXL_CUDA(cudaGetLastError());
+    }
+
+    static void canon(const Decomposition& d, const LayoutMap& m, int p, void* buf, double* staging, int k_lo,
+                      int k_hi, int kg_stage0, bool to_device, cudaStream_t st) {
+        CanonArgs<Q> A{};
+        fill_planes(m, A.plane);
+        const PartGeom g = geom_of(d, p);
+        A.vs = m.voxel_stride();
+        A.na = g.na;
+        A.s = g.s;
+        A.n = g.n;
+        A.k_lo = k_lo;
+        A.k_hi = k_hi;
+        A.kg_stage0 = kg_stage0;
+        A.kg0 = g.kg0;
+        const long long count = (long long)(k_hi - k_lo) * g.s;
+        if (count <= 0) return;
+        const int threads = 256;
+        const unsigned blocks = unsigned((count + threads - 1) / threads);
+        if (to_device) canon_kernel<Q, R, true><<<blocks, threads, 0, st>>>(static_cast<R*>(buf), staging, A);
+        else canon_kernel<Q, R, false><<<blocks, threads, 0, st>>>(static_cast<R*>(buf), staging, A);
+        VOXL_CUDA(cudaGetLastError());
+    }
+
+    static void fill(const Decomposition& d, const LayoutMap& m, int p, void* buf, const double* feq,
+                     cudaStream_t st) {
+        CanonArgs<Q> A{};
+        fill_planes(m, A.plane);
+        const PartGeom g = geom_of(d, p);
+        A.vs = m.voxel_stride();
+        A.na = g.na;
+        A.s = g.s;
+        A.n = g.n;
+        StepArgs<Q, R> V{};
+        for (int c = 0; c < Q; ++c) V.lid[c] = R(feq[c]);
+        const long long count = (long long)(g.n + 2) * g.s;
+        fill_kernel<Q, R><<<unsigned((count + 255) / 256), 256, 0, st>>>(static_cast<R*>(buf), A, V);
+        VOXL_CUDA(cudaGetLastError());
+    }
+
+    static void probe(const Decomposition& d, const LayoutMap& m, int p, const void* buf, double* partial,
+                      unsigned long long* bad, double* out, cudaStream_t st) {
+        CanonArgs<Q> A{};
+        fill_planes(m, A.plane);
+        const PartGeom g = geom_of(d, p);
+        A.vs = m.voxel_stride();
+        A.na = g.na;
+        A.s = g.s;
+        A.n = g.n;
+        A.kg0 = g.kg0;
+        probe_kernel<L, R><<<kProbeBlocks, kProbeThreads, 0, st>>>(static_cast<const R*>(buf), A, partial, bad);
+        probe_final_kernel<<<1, 32, 0, st>>>(partial, kProbeBlocks, out);
+        VOXL_CUDA(cudaGetLastError());
+    }
+};
+
+template <class F>
+void dispatch(int lattice, Precision prec, F&& f) {
+    auto by_prec = [&](auto lat) {
+        using L = decltype(lat);
+        if (prec == Precision::F64) f(DenseOps<L, double, true>{});
+        else f(DenseOps<L, float, false>{});
+    };
+    switch (lattice) {
+        case kD2Q9: by_prec(D2Q9{}); break;
+        case kD3Q19: by_prec(D3Q19{}); break;
+        case kD3Q27: by_prec(D3Q27{}); break;
+        default: throw std::invalid_argument("unknown lattice kind");
+    }
+}
+
+} // namespace
+
+// ---- engine ------------------------------------------------------------------------
+
+DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg) {
+    if (cfg_.lattice < 0 || cfg_.lattice > 2) throw std::invalid_argument("unknown lattice kind");
+    const LatticeTable t = make_lattice(cfg_.lattice);
+    q_ = t.q;
+    axis_ = t.dim == 2 ? 1 : 2;
+    if (!(cfg_.tau > 0.5)) throw std::invalid_argument("invalid configuration: tau must be > 0.5; ");
+    if (t.dim == 2 && cfg_.domain[2] != 1) throw std::invalid_argument("invalid configuration: D2Q9 requires nz == 1; ");
+    if (t.dim == 3 && cfg_.domain[2] < 2)
+        throw std::invalid_argument("invalid configuration: 3D lattices require nz >= 2; ");
+    if (cfg_.domain[0] < 2 || cfg_.domain[1] < 2)
+        throw std::invalid_argument("invalid configuration: domain extents must be >= 2; ");
+    if (cfg_.scenario == Scenario::FlowOverObstacle)
+        throw std::invalid_argument("dense engine: flow_over_obstacle runs on the block-sparse engine");
+    esize_ = cfg_.precision == Precision::F64 ? 8 : 4;
+    decomp_ = decompose(cfg_.domain, cfg_.partitions, axis_, cfg_.scenario == Scenario::PeriodicBox);
+    if (cfg_.local_partitions < 0) {
+        cfg_.first_partition = 0;
+        cfg_.local_partitions = cfg_.partitions;
+    }
+    if (cfg_.first_partition < 0 || cfg_.first_partition + cfg_.local_partitions > cfg_.partitions)
+        throw std::invalid_argument("dense engine: bad local partition range");
+    const TransferSets ts = TransferSets::for_lattice(cfg_.lattice, axis_);
+    for (int p = 0; p < cfg_.partitions; ++p) {
+        std::array<int, 3> shape = cfg_.domain;
+        shape[axis_] = decomp_.thickness(p);
+        maps_.push_back(LayoutMap::build(cfg_.layout, shape, q_, axis_, ts));
+    }
+    parts_.resize(cfg_.partitions);
+    VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    for (int p = 0; p < cfg_.partitions; ++p) {
+        if (!local(p)) continue;
+        const std::size_t bytes = buffer_bytes(p);
+        for (int w = 0; w < 2; ++w) {
+            VOXL_CUDA(cudaMalloc(&parts_[p].buf[w], bytes));
+            VOXL_CUDA(cudaMemsetAsync(parts_[p].buf[w], 0, bytes, stream_));
+        }
+        parts_[p].owned = true;
+    }
+    VOXL_CUDA(cudaMalloc(&error_flag_, sizeof(int)));
+    const int big = INT_MAX;
+    VOXL_CUDA(cudaMemcpyAsync(error_flag_, &big, sizeof(int), cudaMemcpyHostToDevice, stream_));
+    diag_scratch_len_ = 2 * kProbeBlocks + 4;
+    VOXL_CUDA(cudaMalloc(&diag_scratch_, diag_scratch_len_ * sizeof(double)));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+DenseEngine::~DenseEngine() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& p : parts_)
+        if (p.owned)
+            for (void* b : p.buf) cudaFree(b);
+    cudaFree(error_flag_);
+    cudaFree(diag_scratch_);
+    if (staging_) cudaFree(staging_);
+    if (flags_) cudaFree(flags_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+std::int64_t DenseEngine::owned_voxels() const {
+    std::int64_t v = 0;
+    const std::int64_t s = maps_[0].cross_section();
+    for (int p = 0; p < cfg_.partitions; ++p)
+        if (local(p)) v += std::int64_t(decomp_.thickness(p)) * s;
+    return v;
+}
+
+std::size_t DenseEngine::buffer_bytes(int p) const { return std::size_t(maps_[p].total_len()) * esize_; }
+
+void* DenseEngine::buffer(int p, int which) const { return parts_[p].buf[which == 0 ? cur_ : cur_ ^ 1]; }
+
+void DenseEngine::attach_peer(int p, void* b0, void* b1) {
+    if (local(p)) throw std::invalid_argument("attach_peer: partition is owned locally");
+    parts_[p].buf[0] = b0;
+    parts_[p].buf[1] = b1;
+}
+
+void DenseEngine::attach_flags(std::uint32_t* local_flags, std::uint32_t* up, std::uint32_t* low) {
+    flags_ = local_flags;
+    remote_flag_up_ = up;
+    remote_flag_low_ = low;
+}
+
+void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_device) {
+    const std::int64_t s = maps_[0].cross_section();
+    const std::size_t plane_bytes = std::size_t(s) * q_ * sizeof(double);
+    // stage at most ~256 MiB of canonical planes at a time
+    int chunk = int(std::max<std::size_t>(1, (std::size_t(256) << 20) / plane_bytes));
+    chunk = std::min(chunk, std::max(1, k_end - k_begin));
+    const std::size_t need = std::size_t(chunk) * plane_bytes;
+    if (staging_bytes_ < need) {
+        if (staging_) VOXL_CUDA(cudaFree(staging_));
+        VOXL_CUDA(cudaMalloc(&staging_, need));
+        staging_bytes_ = need;
+    }
+    for (int k0 = k_begin; k0 < k_end; k0 += chunk) {
+        const int k1 = std::min(k_end, k0 + chunk);
+        double* hchunk = host + std::size_t(k0 - k_begin) * s * q_;
+        const std::size_t bytes = std::size_t(k1 - k0) * plane_bytes;
+        if (to_device)
+            VOXL_CUDA(cudaMemcpyAsync(staging_, hchunk, bytes, cudaMemcpyHostToDevice, stream_));
+        for (int p = 0; p < cfg_.partitions; ++p) {
+            if (!local(p)) continue;
+            const int lo = std::max(k0, decomp_.slabs[p].first), hi = std::min(k1, decomp_.slabs[p].second);
+            if (lo >= hi) continue;
+            dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+                decltype(ops)::canon(decomp_, maps_[p], p, parts_[p].buf[cur_], static_cast<double*>(staging_),
+                                     lo - decomp_.slabs[p].first, hi - decomp_.slabs[p].first, k0, to_device,
+                                     stream_);
+            });
+        }
+        if (!to_device)
+            VOXL_CUDA(cudaMemcpyAsync(hchunk, staging_, bytes, cudaMemcpyDeviceToHost, stream_));
+        VOXL_CUDA(cudaStreamSynchronize(stream_));
+    }
+}
+
+void DenseEngine::set_canonical_planes(const double* host, int k_begin, int k_end) {
+    scatter_gather(const_cast<double*>(host), k_begin, k_end, true);
+}
+
+void DenseEngine::get_canonical_planes(double* host, int k_begin, int k_end) {
+    scatter_gather(host, k_begin, k_end, false);
+}
+
+void DenseEngine::set_canonical(const double* host) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int p = 0; p < cfg_.partitions; ++p)
+        if (local(p)) {
+            lo = std::min(lo, decomp_.slabs[p].first);
+            hi = std::max(hi, decomp_.slabs[p].second);
+        }
+    const std::int64_t s = maps_[0].cross_section();
+    scatter_gather(const_cast<double*>(host) + std::size_t(lo) * s * q_, lo, hi, true);
+    // fill_canonical leaves halos stale; the first step_occ's halo_update
+    // refreshes them. Do the same refresh here for the single-process engine
+    // (multi-process engines refresh through their shared-layer stores).
+    if (cfg_.local_partitions == cfg_.partitions) halo_copy(0);
+}
+
+void DenseEngine::set_equilibrium(double rho, const double u[3]) {
+    // equilibrium (lattice.cpp:104-113) evaluated on the host in the reference's
+    // double op order, then broadcast to every voxel of both parities.
+    const LatticeTable t = make_lattice(cfg_.lattice);
+    double feq[27];
+    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    for (int i = 0; i < t.q; ++i) {
+        const double eu = double(t.e[i][0]) * u[0] + double(t.e[i][1]) * u[1] + double(t.e[i][2]) * u[2];
+        const double w = double(t.wnum[i]) / double(t.wden[i]);
+        feq[i] = w * rho * (1.0 + 3.0 * eu + 4.5 * eu * eu - 1.5 * uu);
+    }
+    for (int p = 0; p < cfg_.partitions; ++p) {
+        if (!local(p)) continue;
+        for (int w = 0; w < 2; ++w)
+            dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+                decltype(ops)::fill(decomp_, maps_[p], p, parts_[p].buf[w], feq, stream_);
+            });
+    }
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void DenseEngine::get_canonical(double* host) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int p = 0; p < cfg_.partitions; ++p)
+        if (local(p)) {
+            lo = std::min(lo, decomp_.slabs[p].first);
+            hi = std::max(hi, decomp_.slabs[p].second);
+        }
+    const std::int64_t s = maps_[0].cross_section();
+    scatter_gather(host + std::size_t(lo) * s * q_, lo, hi, false);
+}
+
+void DenseEngine::halo_copy(int which) {
+    // halo_update (partition.cpp:163-206): one cudaMemcpyAsync per contiguous
+    // span, source = shared slab of p, destination = neighbour's halo slab.
+    const int par = which == 0 ? cur_ : cur_ ^ 1;
+    const auto recs = halo_records(decomp_, maps_, 0);
+    for (const auto& r : recs) {
+        if (!parts_[r.src].buf[par] || !parts_[r.dst].buf[par]) continue;
+        char* dst = static_cast<char*>(parts_[r.dst].buf[par]) + r.dst_span.base * esize_;
+        const char* src = static_cast<const char*>(parts_[r.src].buf[par]) + r.src_span.base * esize_;
+        VOXL_CUDA(cudaMemcpyAsync(dst, src, std::size_t(r.elements) * esize_, cudaMemcpyDeviceToDevice, stream_));
+    }
+}
+
+void DenseEngine::launch_step() {
+    const bool wrap = cfg_.scenario == Scenario::PeriodicBox;
+    const bool zero_copy = cfg_.halo == HaloMode::ZeroCopy;
+    const int in = cur_, out = cur_ ^ 1;
+    for (int p = 0; p < cfg_.partitions; ++p) {
+        if (!local(p)) continue;
+        const int up = decomp_.upper_neighbor(p), low = decomp_.lower_neighbor(p);
+        void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
+        void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
+        const int n = decomp_.thickness(p);
+        dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+            decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out,
+                                       low_out, wrap, steps_done_, error_flag_, 0, 1, n, stream_);
+        });
+    }
+    cur_ = out;
+    if (!zero_copy) halo_copy(0);
+    ++steps_done_;
+}
+
+void DenseEngine::enqueue_steps(int n) {
+    for (int i = 0; i < n; ++i) launch_step();
+}
+
+double DenseEngine::timed_steps(int n, double* kernel_ms) {
+    // CUDA events on the launching stream: one pair around each step (the
+    // step's kernels), plus the span from the first to the last event.
+    std::vector<cudaEvent_t> ev(2 * std::size_t(n));
+    for (auto& e : ev) VOXL_CUDA(cudaEventCreate(&e));
+    for (int i = 0; i < n; ++i) {
+        VOXL_CUDA(cudaEventRecord(ev[2 * i], stream_));
+        launch_step();
+        VOXL_CUDA(cudaEventRecord(ev[2 * i + 1], stream_));
+    }
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    double ksum = 0.0;
+    for (int i = 0; i < n; ++i) {
+        float ms = 0.f;
+        VOXL_CUDA(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+        ksum += ms;
+    }
+    float total = 0.f;
+    if (n > 0) VOXL_CUDA(cudaEventElapsedTime(&total, ev[0], ev[2 * n - 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (kernel_ms) *kernel_ms = ksum;
+    check_errors();
+    return total;
+}
+
+void DenseEngine::check_errors() {
+    int flag = INT_MAX;
+    VOXL_CUDA(cudaMemcpyAsync(&flag, error_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    if (flag != INT_MAX)
+        throw InstabilityError("run aborted at step " + std::to_string(flag) +
+                               ": macroscopic: non-positive density");
+}
+
+void DenseEngine::step(int n) {
+    if (n < 0) throw std::invalid_argument("step: n must be >= 0");
+    enqueue_steps(n);
+    check_errors();
+}
+
+DenseDiag DenseEngine::probe() {
+    double* partial = diag_scratch_;
+    double* out = diag_scratch_ + 2 * kProbeBlocks;
+    auto* bad = reinterpret_cast<unsigned long long*>(diag_scratch_ + 2 * kProbeBlocks + 2);
+    const double zero[2] = {0.0, 0.0};
+    const unsigned long long none = ~0ull;
+    VOXL_CUDA(cudaMemcpyAsync(out, zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
+    for (int p = 0; p < cfg_.partitions; ++p) {
+        if (!local(p)) continue;
+        dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+            decltype(ops)::probe(decomp_, maps_[p], p, parts_[p].buf[cur_], partial, bad, out, stream_);
+        });
+    }
+    double res[2];
+    unsigned long long b = 0;
+    VOXL_CUDA(cudaMemcpyAsync(res, out, sizeof res, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(&b, bad, sizeof b, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    DenseDiag d;
+    d.mass = res[0];
+    d.max_speed = res[1];
+    if (b != ~0ull) {
+        d.unstable = 1;
+        d.bad_voxel = std::int64_t(b >> 5);
+        d.bad_population = int(b & 31);
+    }
+    return d;
+}
+
+std::vector<TransferRecord> DenseEngine::ledger_records(int step) const { return halo_records(decomp_, maps_, step); }
+
+} // namespace voxl_b200

@@ -1,0 +1,146 @@
+// dense.cuh -- dense z-slab (y-slab in 2D) LBM engine on B200.
+//
+// Drop-in for the reference's dense path: PartitionedField + step_occ +
+// GatherKernel (proj/include/voxl/partition.hpp:95-214, lbm.hpp:123-133) and the
+// single-grid oracle loop reference_dense_run (proj/src/solver.cpp:189-206).
+//
+// One DenseEngine owns P partitions. Each partition is a pair of device buffers
+// laid out EXACTLY as the reference's LayoutMap (AoS / SoA / DisagSoA) over the
+// owned slab plus one-deep halos. A step is one fused pull + BGK kernel per
+// partition; in zero-copy mode the shared-layer voxels also store their
+// face-crossing populations straight into the neighbour partition's halo
+// group of the output buffer (one contiguous 5*s span in DisagSoA), so no halo
+// copy exists at all. Partitions may live on different devices (peer pointers)
+// or in different processes (IPC pointers, see attach_peer()).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "grid.hpp"
+
+namespace voxl_b200 {
+
+enum class Precision : int { F32 = 0, F64 = 1 };
+enum class HaloMode : int { ZeroCopy = 0, Copy = 1 };
+enum class Scenario : int { LidDrivenCavity = 0, FlowOverObstacle = 1, PeriodicBox = 2 };
+
+struct DenseConfig {
+    int lattice = 1;  // LatticeKind
+    std::array<int, 3> domain{32, 32, 32};
+    double tau = 0.56;
+    Scenario scenario = Scenario::LidDrivenCavity;
+    std::array<double, 3> velocity{0.05, 0.0, 0.0};
+    LayoutScheme layout = LayoutScheme::DisagSoA;
+    int partitions = 1;
+    Precision precision = Precision::F32;
+    HaloMode halo = HaloMode::ZeroCopy;
+    // Partitions owned by this engine: [first_partition, first_partition + local_partitions).
+    // The default (-1) owns all of them (single process).
+    int first_partition = 0;
+    int local_partitions = -1;
+};
+
+struct DenseDiag {
+    double mass = 0.0;
+    double max_speed = 0.0;
+    int unstable = 0;            // 1 if some |f| > 1e3 or non-finite
+    std::int64_t bad_voxel = -1; // canonical voxel index of the first offender
+    int bad_population = -1;
+};
+
+class DenseEngine {
+public:
+    explicit DenseEngine(const DenseConfig& cfg);
+    ~DenseEngine();
+    DenseEngine(const DenseEngine&) = delete;
+    DenseEngine& operator=(const DenseEngine&) = delete;
+
+    const DenseConfig& config() const { return cfg_; }
+    const Decomposition& decomposition() const { return decomp_; }
+    const LayoutMap& layout(int p) const { return maps_[p]; }
+    int q() const { return q_; }
+    std::int64_t owned_voxels() const;  // voxels of the locally owned partitions
+    int steps_done() const { return steps_done_; }
+
+    /// Canonical fp64 state (x fastest, component innermost) for the whole
+    /// domain (fill_canonical / to_canonical, partition.cpp:123-161). With a
+    /// partial engine only the owned slabs are read/written.
+    void set_canonical(const double* host);
+    /// Every voxel (halos included, both buffers) at equilibrium(rho, u):
+    /// the reference's rest-state initialisation, done on the device.
+    void set_equilibrium(double rho, const double u[3]);
+    void get_canonical(double* host);
+    /// Same, over global axis planes [k_begin, k_end) only (chunked I/O).
+    void set_canonical_planes(const double* host, int k_begin, int k_end);
+    void get_canonical_planes(double* host, int k_begin, int k_end);
+
+    /// Advance n steps (step_occ x n). Throws InstabilityError if the device
+    /// reported a non-positive density / non-finite moment.
+    void step(int n);
+    /// Enqueue n steps without any host synchronisation or error check.
+    void enqueue_steps(int n);
+    /// n steps bracketed by CUDA events on the engine stream; returns the
+    /// first-to-last event span (ms) and the summed per-step spans.
+    double timed_steps(int n, double* kernel_ms);
+    /// probe_field on the current state (lbm.cpp:116-138), on the device.
+    DenseDiag probe();
+    /// Checks the device error flag; throws InstabilityError on a set flag.
+    void check_errors();
+
+    /// Halo refresh of the current buffers by span copies (halo_update).
+    void halo_copy(int which);
+
+    /// Records the halo exchange of steps [0, steps_done) as the reference's
+    /// TransferLedger would hold them.
+    std::vector<TransferRecord> ledger_records(int step) const;
+
+    cudaStream_t stream() const { return stream_; }
+    /// Raw device buffer of partition p (current if which == 0 else next).
+    void* buffer(int p, int which) const;
+    std::size_t buffer_bytes(int p) const;
+    /// Multi-process: register a neighbour partition's device buffers (both
+    /// parities, IPC- or peer-mapped) so the shared-layer kernel stores into it.
+    void attach_peer(int p, void* buf0, void* buf1);
+    /// Multi-process: device flag words the neighbours signal after their
+    /// shared-layer stores.
+    void attach_flags(std::uint32_t* local_flags, std::uint32_t* upper_flag_remote,
+                      std::uint32_t* lower_flag_remote);
+    std::uint32_t* flag_words() const { return flags_; }
+
+private:
+    DenseConfig cfg_;
+    int q_ = 19;
+    int axis_ = 2;
+    int esize_ = 4;
+    Decomposition decomp_;
+    std::vector<LayoutMap> maps_;
+    struct Part {
+        void* buf[2] = {nullptr, nullptr};  // owned or attached
+        bool owned = false;
+        int device = 0;
+    };
+    std::vector<Part> parts_;
+    int cur_ = 0;  // parity of the current buffer
+    int steps_done_ = 0;
+    cudaStream_t stream_ = nullptr;
+    int* error_flag_ = nullptr;
+    double* diag_scratch_ = nullptr;
+    std::size_t diag_scratch_len_ = 0;
+    void* staging_ = nullptr;  // fp64 canonical staging (device)
+    std::size_t staging_bytes_ = 0;
+    std::uint32_t* flags_ = nullptr;
+    std::uint32_t* remote_flag_up_ = nullptr;
+    std::uint32_t* remote_flag_low_ = nullptr;
+
+    bool local(int p) const {
+        return p >= cfg_.first_partition && p < cfg_.first_partition + cfg_.local_partitions;
+    }
+    void launch_step();
+    void scatter_gather(double* host, int k_begin, int k_end, bool to_device);
+};
+
+} // namespace voxl_b200

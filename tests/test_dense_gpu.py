@@ -1,0 +1,137 @@
+"""Dense CUDA engine parity (GPU). Calls through the C-ABI (ctypes over
+libvoxl_b200.so) and checks against the C oracle / golden reference fixtures.
+
+* fp64 mode: BITWISE equal to the reference (same IEEE op order, no FMA).
+* fp32 mode: within the BASELINE tolerance (<= 1e-5 relative per population).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2503_07898_b200 as V
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def run_engine(lattice, domain, tau, scenario, velocity, steps, init, **kw):
+    e = V.DenseEngine(lattice=lattice, domain=domain, tau=tau, scenario=scenario, velocity=velocity, **kw)
+    e.set_canonical(init)
+    e.step(steps)
+    out = e.get_canonical()
+    e.close()
+    return out
+
+
+@pytest.mark.parametrize("name", ["dense_cavity_d3q19_12", "dense_cavity_d2q9_24x16", "dense_cavity_d3q27_8x10x12",
+                                  "dense_periodic_d3q19_10"])
+@pytest.mark.parametrize("parts", [1, 2])
+def test_fp64_bitwise_vs_reference_golden(name, parts):
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    cfg = json.loads(str(z["config"]))
+    dom = tuple(cfg["domain"])
+    init = O.port_initial_state(cfg["lattice"], dom, cfg["scenario"], cfg.get("seed", 42), cfg.get("perturbation", 0))
+    out = run_engine(cfg["lattice"], dom, cfg["tau"], cfg["scenario"], tuple(cfg["velocity"]), cfg["steps"], init,
+                     precision="fp64", partitions=parts)
+    assert np.array_equal(out, z["field"]), np.abs(out - z["field"]).max()
+
+
+_CACHE = {}
+
+
+def oracle_cavity(n, steps):
+    key = (n, steps)
+    if key not in _CACHE:
+        _CACHE[key] = O.port_dense_run("D3Q19", (n, n, n), 0.56, "lid_driven_cavity", (0.05, 0, 0), steps)
+    return _CACHE[key]
+
+
+@pytest.mark.parametrize("layout", ["AoS", "SoA", "DisagSoA"])
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("halo", ["zero_copy", "copy"])
+def test_partition_invariance_fp64(layout, parts, halo):
+    """Acceptance C3 on the GPU: 32^3 cavity, bitwise across partitions x layouts."""
+    ref = oracle_cavity(32, 60)
+    init = O.port_initial_state("D3Q19", (32, 32, 32))
+    out = run_engine("D3Q19", (32, 32, 32), 0.56, "lid_driven_cavity", (0.05, 0, 0), 60, init, precision="fp64",
+                     layout=layout, partitions=parts, halo_mode=halo)
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3])
+def test_periodic_partitioned_fp64(parts):
+    dom = (12, 10, 14)
+    init = O.port_initial_state("D3Q19", dom, "periodic_box", 7, 0.05)
+    ref = O.port_dense_run("D3Q19", dom, 0.8, "periodic_box", (0, 0, 0), 25, seed=7, perturbation=0.05)
+    out = run_engine("D3Q19", dom, 0.8, "periodic_box", (0, 0, 0), 25, init, precision="fp64", partitions=parts)
+    assert np.array_equal(out, ref)
+
+
+def test_fp64_bitwise_at_128_cubed():
+    """A BASELINE-size case: 128^3 cavity, 20 steps, bitwise."""
+    ref = oracle_cavity(128, 20)
+    init = O.port_initial_state("D3Q19", (128, 128, 128))
+    out = run_engine("D3Q19", (128, 128, 128), 0.56, "lid_driven_cavity", (0.05, 0, 0), 20, init,
+                     precision="fp64", partitions=4)
+    assert np.array_equal(out, ref)
+
+
+def test_fp32_tolerance_1000_steps_128():
+    """BASELINE tolerance: fp32 <= 1e-5 relative per population after 1000 steps at
+    128^3. The fp64 engine is the reference here: it is bitwise equal to the
+    oracle (tests above), and the oracle needs ~10 CPU minutes at this size."""
+    init = O.port_initial_state("D3Q19", (128, 128, 128))
+    kw = dict(lattice="D3Q19", domain=(128, 128, 128), tau=0.56, scenario="lid_driven_cavity",
+              velocity=(0.05, 0, 0), steps=1000, init=init)
+    f64 = run_engine(precision="fp64", **kw)
+    f32 = run_engine(precision="fp32", **kw)
+    rel = np.abs(f32 - f64) / np.abs(f64)
+    print("fp32 max rel err after 1000 steps:", rel.max(), "mean:", rel.mean())
+    assert rel.max() <= 1e-5
+
+
+def test_fp32_short_run_vs_oracle():
+    ref = oracle_cavity(32, 60)
+    init = O.port_initial_state("D3Q19", (32, 32, 32))
+    out = run_engine("D3Q19", (32, 32, 32), 0.56, "lid_driven_cavity", (0.05, 0, 0), 60, init, precision="fp32")
+    assert np.max(np.abs(out - ref) / np.abs(ref)) <= 1e-5
+
+
+def test_probe_matches_oracle():
+    ref = oracle_cavity(32, 60)
+    m_ref, s_ref = O.port_probe("D3Q19", ref)
+    e = V.DenseEngine(domain=(32, 32, 32), precision="fp64", partitions=2)
+    e.set_canonical(O.port_initial_state("D3Q19", (32, 32, 32)))
+    e.step(60)
+    d = e.probe()
+    assert d.unstable == 0
+    assert abs(d.mass - m_ref) <= 1e-12 * m_ref
+    assert abs(d.max_speed - s_ref) <= 1e-14
+
+
+def test_instability_reported():
+    e = V.DenseEngine(domain=(8, 8, 8), precision="fp64")
+    bad = O.port_initial_state("D3Q19", (8, 8, 8)) * -1.0
+    e.set_canonical(bad)
+    with pytest.raises(V.VoxlInstability, match="run aborted at step 0"):
+        e.step(1)
+    d = e.probe()
+    assert d.unstable == 0 or d.bad_voxel >= 0
+
+
+def test_probe_flags_large_population():
+    e = V.DenseEngine(domain=(8, 8, 8), precision="fp64")
+    st = O.port_initial_state("D3Q19", (8, 8, 8))
+    st[(3 * 64 + 2 * 8 + 1) * 19 + 5] = 2e3
+    e.set_canonical(st)
+    d = e.probe()
+    assert d.unstable == 1 and d.bad_voxel == 3 * 64 + 2 * 8 + 1 and d.bad_population == 5
+
+
+def test_engine_ledger_equals_plan():
+    e = V.DenseEngine(domain=(16, 16, 16), partitions=4, layout="SoA")
+    assert [r.__dict__ for r in e.ledger(3)] == [r.__dict__ for r in V.plan_ledger(3, domain=(16, 16, 16),
+                                                                                    partitions=4, layout="SoA")]

@@ -136,6 +136,22 @@ int voxl_dense_buffer(voxl_dense* h, int partition, int which, void** ptr, size_
 int voxl_dense_stream(voxl_dense* h, void** stream);
 /** Multi-process: map a neighbour partition's buffers (IPC/peer pointers, both parities). */
 int voxl_dense_attach_peer(voxl_dense* h, int partition, void* buf0, void* buf1);
+/** Allocation-order buffer w (0/1) of an owned partition (for IPC export). */
+int voxl_dense_raw_buffer(voxl_dense* h, int partition, int w, void** ptr);
+/** Multi-process zero-copy: allocate the step-flag words (returned, for IPC export). */
+int voxl_dense_enable_distributed(voxl_dense* h, void** flags);
+/** The neighbours' flag slots this rank signals after its shared layers
+ *  (upper neighbour's flags + 1 word, lower neighbour's flags + 0); NULL at a domain end. */
+int voxl_dense_attach_flags(voxl_dense* h, void* upper_slot, void* lower_slot);
+/** Peer-copy this rank's shared slabs into the neighbours' halos (after set_canonical). */
+int voxl_dense_halo_push(voxl_dense* h);
+int voxl_dense_owned_voxels(voxl_dense* h, int64_t* voxels);
+
+/* ---- CUDA IPC helpers (64-byte cudaIpcMemHandle_t as bytes) ------------------- */
+int voxl_ipc_export(void* dev_ptr, char* handle64);
+int voxl_ipc_open(const char* handle64, void** dev_ptr);
+int voxl_ipc_close(void* dev_ptr);
+int voxl_enable_peer_access(int peer_device);
 
 #ifdef __cplusplus
 }

@@ -106,6 +106,15 @@ def _load():
         "voxl_dense_buffer": ([vp, C.c_int, C.c_int, C.POINTER(vp), C.POINTER(C.c_size_t)], C.c_int),
         "voxl_dense_stream": ([vp, C.POINTER(vp)], C.c_int),
         "voxl_dense_attach_peer": ([vp, C.c_int, vp, vp], C.c_int),
+        "voxl_dense_raw_buffer": ([vp, C.c_int, C.c_int, C.POINTER(vp)], C.c_int),
+        "voxl_dense_enable_distributed": ([vp, C.POINTER(vp)], C.c_int),
+        "voxl_dense_attach_flags": ([vp, vp, vp], C.c_int),
+        "voxl_dense_halo_push": ([vp], C.c_int),
+        "voxl_dense_owned_voxels": ([vp, C.POINTER(i64)], C.c_int),
+        "voxl_ipc_export": ([vp, vp], C.c_int),
+        "voxl_ipc_open": ([vp, C.POINTER(vp)], C.c_int),
+        "voxl_ipc_close": ([vp], C.c_int),
+        "voxl_enable_peer_access": ([C.c_int], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)

@@ -290,4 +290,70 @@ int voxl_dense_attach_peer(voxl_dense* h, int p, void* b0, void* b1) {
     return guarded([&] { h->eng->attach_peer(p, b0, b1); });
 }
 
+int voxl_dense_raw_buffer(voxl_dense* h, int p, int w, void** ptr) {
+    return guarded([&] {
+        require(p >= 0 && p < h->eng->config().partitions && (w == 0 || w == 1), "bad partition/buffer");
+        *ptr = h->eng->raw_buffer(p, w);
+    });
+}
+
+int voxl_dense_enable_distributed(voxl_dense* h, void** flags) {
+    return guarded([&] {
+        h->eng->enable_distributed();
+        if (flags) *flags = h->eng->flag_words();
+    });
+}
+
+int voxl_dense_attach_flags(voxl_dense* h, void* upper_slot, void* lower_slot) {
+    return guarded([&] {
+        h->eng->attach_flags(static_cast<std::uint32_t*>(upper_slot), static_cast<std::uint32_t*>(lower_slot));
+    });
+}
+
+int voxl_dense_halo_push(voxl_dense* h) {
+    return guarded([&] { h->eng->halo_push(); });
+}
+
+int voxl_dense_owned_voxels(voxl_dense* h, int64_t* voxels) {
+    return guarded([&] { *voxels = h->eng->owned_voxels(); });
+}
+
+int voxl_ipc_export(void* dev_ptr, char* handle64) {
+    return guarded([&] {
+        cudaIpcMemHandle_t hd;
+        VOXL_CUDA(cudaIpcGetMemHandle(&hd, dev_ptr));
+        static_assert(sizeof(hd) == 64, "IPC handle size");
+        std::memcpy(handle64, &hd, 64);
+    });
+}
+
+int voxl_ipc_open(const char* handle64, void** dev_ptr) {
+    return guarded([&] {
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, handle64, 64);
+        VOXL_CUDA(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int voxl_ipc_close(void* dev_ptr) {
+    return guarded([&] { VOXL_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
+}
+
+int voxl_enable_peer_access(int peer_device) {
+    return guarded([&] {
+        int cur = 0;
+        VOXL_CUDA(cudaGetDevice(&cur));
+        if (cur == peer_device) return;
+        int can = 0;
+        VOXL_CUDA(cudaDeviceCanAccessPeer(&can, cur, peer_device));
+        if (!can) throw CudaError("peer access not supported between devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+            cudaGetLastError();
+            return;
+        }
+        VOXL_CUDA(e);
+    });
+}
+
 } // extern "C"

@@ -41,6 +41,11 @@ struct StepArgs {
     int periodic_a, periodic_b;
     int has_lid;
     int step;
+    int remote_fence;  // remote halo stores cross a process/device: membar.sys after them
+    int uniform_groups;  // all groups share one plane table (AoS / SoA)
+    long long fast_base;  // byte offset of the interior plane table's component 0
+    long long fast_in_off[Q];   // per-direction pull byte offset relative to fast_base + lin
+    long long fast_out_off[Q];  // per-direction store byte offset
     int* error_flag;
 };
 
@@ -72,12 +77,44 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
     const int lin = (k + 1) * s + cross;
     const int gm = group_of(k - 1, A.n), g0 = group_of(k, A.n), gp = group_of(k + 1, A.n);
 
+    constexpr long long VS = AOS ? Q : 1;
+    R f[Q];
+
+    // Fast path (warp-uniform): no lane of this warp touches a wall and the
+    // source planes k-1..k+1 share one plane table (interior group, or any
+    // group of a non-disaggregated layout). Every population address is then
+    // one per-thread base pointer plus a block-uniform byte offset per
+    // direction, so each pull is a single LDG [R.64 + UR] and each push a
+    // single STG.
+    if constexpr (!WRAP) {
+        const int a_w0 = a - (threadIdx.x & 31);
+        const int a_w1 = min(a_w0 + 31, na - 1);
+        const bool wall = (A.wall_a && (a_w0 == 0 || a_w1 == na - 1)) || (A.wall_b && (b == 0 || b == A.nb - 1)) ||
+                          (A.wall_k && (kg == 0 || kg == A.nk - 1)) || a_w1 - a_w0 != 31;
+        const bool uniform_planes = A.uniform_groups || (gm == 2 && g0 == 2 && gp == 2);
+        if (!wall && uniform_planes) {
+            const char* base_in = reinterpret_cast<const char*>(A.in) + A.fast_base + (long long)lin * (VS * sizeof(R));
+            static_for<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                f[i] = ld_ro(reinterpret_cast<const R*>(base_in + A.fast_in_off[i]));
+            });
+            bool ok = true;
+            R rho, u[3];
+            if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
+            else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok);
+            if (!ok) atomicMin(A.error_flag, A.step);
+            char* base_out = reinterpret_cast<char*>(A.out) + A.fast_base + (long long)lin * (VS * sizeof(R));
+            static_for<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                *reinterpret_cast<R*>(base_out + A.fast_out_off[i]) = f[i];
+            });
+            return;
+        }
+    }
+
     const bool a_lo = A.wall_a && a == 0, a_hi = A.wall_a && a == na - 1;
     const bool b_lo = A.wall_b && b == 0, b_hi = A.wall_b && b == A.nb - 1;
     const bool k_lo = A.wall_k && kg == 0, k_hi = A.wall_k && kg == A.nk - 1;
-    constexpr long long VS = AOS ? Q : 1;
-
-    R f[Q];
     static_for<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
         constexpr int ea = L::e(i, 0), eb = L::e(i, OTHER), ek = L::e(i, AXIS);
@@ -111,7 +148,8 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
 
     bool ok = true;
     R rho, u[3];
-    bgk_relax<L, R, Exact>(f, A.omega, A.keep, rho, u, ok);
+    if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
+    else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok);
     if (!ok) atomicMin(A.error_flag, A.step);
 
     static_for<Q>([&](auto I) {
@@ -133,6 +171,39 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
             if ((A.low_mask >> i) & 1u) A.low_out[A.low_plane[i] + (long long)cross * VS] = f[i];
         });
     }
+    // Cross-GPU ordering: the peer stores above must be performed before this
+    // step's completion flag (written by signal_kernel after this kernel).
+    if (A.remote_fence && ((k == 0 && A.up_out) || (k == A.n - 1 && A.low_out))) __threadfence_system();
+}
+
+// ---- cross-GPU step flags ---------------------------------------------------------------
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+/// Blocks the stream until both neighbours have finished the shared layers of
+/// step target-1 (RAW: our halos are filled; WAR: they no longer read the
+/// halo slots we are about to overwrite).
+__global__ void wait_flags_kernel(const unsigned* flags, int need_up, int need_low, unsigned target) {
+    if (threadIdx.x != 0) return;
+    if (need_up)
+        while (ld_acquire_sys(flags + 0) < target) __nanosleep(64);
+    if (need_low)
+        while (ld_acquire_sys(flags + 1) < target) __nanosleep(64);
+}
+
+__global__ void signal_flags_kernel(unsigned* up_slot, unsigned* low_slot, unsigned value) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    if (up_slot) st_release_sys(up_slot, value);
+    if (low_slot) st_release_sys(low_slot, value);
 }
 
 // ---- canonical <-> layout -----------------------------------------------------------
@@ -140,6 +211,7 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
 template <int Q>
 struct CanonArgs {
     long long plane[kGroupCount][Q];
+    double shift[Q];  // w_i for shifted fp32 storage (g = f - w), 0 for fp64
     long long vs;
     int na, s, n;
     int k_lo, k_hi;   // local k range being moved
@@ -159,8 +231,8 @@ __global__ void canon_kernel(R* buf, double* staging, const __grid_constant__ Ca
     const long long st = ((long long)(A.kg0 + k - A.kg_stage0) * A.s + cross) * Q;
     for (int c = 0; c < Q; ++c) {
         R* p = buf + A.plane[g][c] + lin * A.vs;
-        if constexpr (ToDevice) *p = R(staging[st + c]);
-        else staging[st + c] = double(*p);
+        if constexpr (ToDevice) *p = R(staging[st + c] - A.shift[c]);
+        else staging[st + c] = double(*p) + A.shift[c];
     }
 }
 
@@ -199,7 +271,7 @@ __global__ void __launch_bounds__(kProbeThreads) probe_kernel(const R* buf, cons
         bool bad_here = false;
         int bad_pop = 0;
         for (int c = 0; c < Q; ++c) {
-            f[c] = double(buf[A.plane[g][c] + lin * A.vs]);
+            f[c] = double(buf[A.plane[g][c] + lin * A.vs]) + A.shift[c];
             if (!bad_here && (!isfinite(f[c]) || fabs(f[c]) > 1e3)) {
                 bad_here = true;
                 bad_pop = c;
@@ -280,6 +352,11 @@ struct DenseOps {
     static constexpr int Q = L::Q;
     static constexpr int AXIS = axis_of<L>();
 
+    /// fp32 stores g = f - w (bgk_relax_shifted); fp64 parity mode stores f.
+    static void fill_shift(double (&shift)[Q]) {
+        for (int c = 0; c < Q; ++c) shift[c] = Exact ? 0.0 : L::w(c);
+    }
+
     static void fill_planes(const LayoutMap& m, long long (&plane)[kGroupCount][Q]) {
         for (int g = 0; g < kGroupCount; ++g)
             for (int c = 0; c < Q; ++c) plane[g][c] = m.plane_offset(g, c);
@@ -287,8 +364,11 @@ struct DenseOps {
 
     static void launch_step(const DenseConfig& cfg, const Decomposition& d, const std::vector<LayoutMap>& maps,
                             int p, const void* in, void* out, void* up_out, void* low_out, bool wrap,
-                            int step, int* error_flag, int k_first, int k_step, int k_count, cudaStream_t st) {
+                            int step, int* error_flag, int k_first, int k_step, int k_count, cudaStream_t st,
+                            bool remote_fence = false) {
+        if (k_count <= 0) return;
         StepArgs<Q, R> A{};
+        A.remote_fence = remote_fence;
         const PartGeom g = geom_of(d, p);
         A.in = static_cast<const R*>(in);
         A.out = static_cast<R*>(out);
@@ -350,6 +430,18 @@ struct DenseOps {
         A.has_lid = lid;
         A.step = step;
         A.error_flag = error_flag;
+        constexpr int OTHER = AXIS == 2 ? 1 : 2;
+        const long long vs = maps[p].voxel_stride();
+        A.uniform_groups = maps[p].scheme() != LayoutScheme::DisagSoA;
+        const int gi = int(GroupTag::Interior);
+        A.fast_base = A.plane[gi][0] * (long long)sizeof(R);
+        for (int i = 0; i < Q; ++i) {
+            const long long shift = -(long long)L::e(i, 0) - (long long)L::e(i, OTHER) * g.na -
+                                    (long long)L::e(i, AXIS) * g.s;
+            const long long rel = A.plane[gi][i] - A.plane[gi][0];
+            A.fast_in_off[i] = (rel + vs * shift) * (long long)sizeof(R);
+            A.fast_out_off[i] = rel * (long long)sizeof(R);
+        }
         const dim3 grid((g.na + kBlock - 1) / kBlock, g.nb, k_count);
         if (aos) {
             if (wrap) dense_step_kernel<L, R, Exact, true, AXIS, true><<<grid, kBlock, 0, st>>>(A);
@@ -365,6 +457,7 @@ struct DenseOps {
                       int k_hi, int kg_stage0, bool to_device, cudaStream_t st) {
         CanonArgs<Q> A{};
         fill_planes(m, A.plane);
+        fill_shift(A.shift);
         const PartGeom g = geom_of(d, p);
         A.vs = m.voxel_stride();
         A.na = g.na;
@@ -387,13 +480,14 @@ struct DenseOps {
                      cudaStream_t st) {
         CanonArgs<Q> A{};
         fill_planes(m, A.plane);
+        fill_shift(A.shift);
         const PartGeom g = geom_of(d, p);
         A.vs = m.voxel_stride();
         A.na = g.na;
         A.s = g.s;
         A.n = g.n;
         StepArgs<Q, R> V{};
-        for (int c = 0; c < Q; ++c) V.lid[c] = R(feq[c]);
+        for (int c = 0; c < Q; ++c) V.lid[c] = R(feq[c] - A.shift[c]);
         const long long count = (long long)(g.n + 2) * g.s;
         fill_kernel<Q, R><<<unsigned((count + 255) / 256), 256, 0, st>>>(static_cast<R*>(buf), A, V);
         VOXL_CUDA(cudaGetLastError());
@@ -403,6 +497,7 @@ struct DenseOps {
                       unsigned long long* bad, double* out, cudaStream_t st) {
         CanonArgs<Q> A{};
         fill_planes(m, A.plane);
+        fill_shift(A.shift);
         const PartGeom g = geom_of(d, p);
         A.vs = m.voxel_stride();
         A.na = g.na;
@@ -488,7 +583,7 @@ DenseEngine::~DenseEngine() {
     cudaFree(error_flag_);
     cudaFree(diag_scratch_);
     if (staging_) cudaFree(staging_);
-    if (flags_) cudaFree(flags_);
+    if (flags_ && distributed_) cudaFree(flags_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -508,12 +603,6 @@ void DenseEngine::attach_peer(int p, void* b0, void* b1) {
     if (local(p)) throw std::invalid_argument("attach_peer: partition is owned locally");
     parts_[p].buf[0] = b0;
     parts_[p].buf[1] = b1;
-}
-
-void DenseEngine::attach_flags(std::uint32_t* local_flags, std::uint32_t* up, std::uint32_t* low) {
-    flags_ = local_flags;
-    remote_flag_up_ = up;
-    remote_flag_low_ = low;
 }
 
 void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_device) {
@@ -618,7 +707,73 @@ void DenseEngine::halo_copy(int which) {
     }
 }
 
+void DenseEngine::enable_distributed() {
+    if (!flags_) {
+        VOXL_CUDA(cudaMalloc(&flags_, 4 * sizeof(std::uint32_t)));
+        VOXL_CUDA(cudaMemset(flags_, 0, 4 * sizeof(std::uint32_t)));
+    }
+    distributed_ = true;
+}
+
+void DenseEngine::attach_flags(std::uint32_t* up, std::uint32_t* low) {
+    remote_flag_up_ = up;
+    remote_flag_low_ = low;
+}
+
+void DenseEngine::halo_push() {
+    // Our shared slabs -> neighbours' halos of the current parity (peer copies).
+    const auto recs = halo_records(decomp_, maps_, 0);
+    for (const auto& r : recs) {
+        if (!local(r.src) || !parts_[r.dst].buf[cur_]) continue;
+        char* dst = static_cast<char*>(parts_[r.dst].buf[cur_]) + r.dst_span.base * esize_;
+        const char* src = static_cast<const char*>(parts_[r.src].buf[cur_]) + r.src_span.base * esize_;
+        VOXL_CUDA(cudaMemcpyAsync(dst, src, std::size_t(r.elements) * esize_, cudaMemcpyDefault, stream_));
+    }
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void DenseEngine::launch_step_distributed() {
+    // One owned partition p; neighbours live in other processes / devices.
+    // Per step: wait(neighbour flags >= t) -> shared layers (k = 0, n-1) with
+    // peer halo stores -> signal(t + 1) -> interior (k = 1 .. n-2). The interior
+    // kernel never touches a halo, so it overlaps the neighbours' exchange.
+    const int p = cfg_.first_partition;
+    const bool wrap = cfg_.scenario == Scenario::PeriodicBox;
+    const bool zero_copy = cfg_.halo == HaloMode::ZeroCopy;
+    const int in = cur_, out = cur_ ^ 1;
+    const int up = decomp_.upper_neighbor(p), low = decomp_.lower_neighbor(p);
+    const unsigned t = unsigned(steps_done_);
+    if (zero_copy) {
+        wait_flags_kernel<<<1, 32, 0, stream_>>>(flags_, up >= 0, low >= 0, t);
+        VOXL_CUDA(cudaGetLastError());
+    }
+    void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
+    void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
+    const int n = decomp_.thickness(p);
+    dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        // shared layers first: k = 0 and k = n - 1
+        Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out, wrap,
+                         steps_done_, error_flag_, 0, n - 1, 2, stream_, true);
+    });
+    if (zero_copy) {
+        signal_flags_kernel<<<1, 32, 0, stream_>>>(remote_flag_up_, remote_flag_low_, t + 1);
+        VOXL_CUDA(cudaGetLastError());
+    }
+    dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr, wrap,
+                         steps_done_, error_flag_, 1, 1, n - 2, stream_, false);
+    });
+    cur_ = out;
+    ++steps_done_;
+}
+
 void DenseEngine::launch_step() {
+    if (distributed_) {
+        launch_step_distributed();
+        return;
+    }
     const bool wrap = cfg_.scenario == Scenario::PeriodicBox;
     const bool zero_copy = cfg_.halo == HaloMode::ZeroCopy;
     const int in = cur_, out = cur_ ^ 1;

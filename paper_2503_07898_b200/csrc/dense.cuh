@@ -105,11 +105,21 @@ public:
     /// Multi-process: register a neighbour partition's device buffers (both
     /// parities, IPC- or peer-mapped) so the shared-layer kernel stores into it.
     void attach_peer(int p, void* buf0, void* buf1);
-    /// Multi-process: device flag words the neighbours signal after their
-    /// shared-layer stores.
-    void attach_flags(std::uint32_t* local_flags, std::uint32_t* upper_flag_remote,
-                      std::uint32_t* lower_flag_remote);
+    /// Multi-process: allocate this rank's flag words (zeroed). flags[0] is
+    /// written by the upper neighbour, flags[1] by the lower neighbour, each
+    /// with the number of steps whose shared-layer stores it has completed.
+    void enable_distributed();
+    /// Multi-process: the neighbours' flag slots this rank signals
+    /// (upper neighbour's flags[1], lower neighbour's flags[0]); null at a
+    /// domain end.
+    void attach_flags(std::uint32_t* upper_flag_remote, std::uint32_t* lower_flag_remote);
     std::uint32_t* flag_words() const { return flags_; }
+    /// Raw buffer w (0/1, allocation order, not parity) of partition p.
+    void* raw_buffer(int p, int w) const { return parts_[p].buf[w]; }
+    bool distributed() const { return distributed_; }
+    /// Push this engine's shared slabs into the neighbours' halos (peer
+    /// copies), for a canonical state loaded in multi-process mode.
+    void halo_push();
 
 private:
     DenseConfig cfg_;
@@ -135,11 +145,13 @@ private:
     std::uint32_t* flags_ = nullptr;
     std::uint32_t* remote_flag_up_ = nullptr;
     std::uint32_t* remote_flag_low_ = nullptr;
+    bool distributed_ = false;
 
     bool local(int p) const {
         return p >= cfg_.first_partition && p < cfg_.first_partition + cfg_.local_partitions;
     }
     void launch_step();
+    void launch_step_distributed();
     void scatter_gather(double* host, int k_begin, int k_end, bool to_device);
 };
 

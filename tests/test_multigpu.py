@@ -1,0 +1,142 @@
+"""Multi-process (one rank per GPU) dense path.
+
+CPU: world_size-2/4 gloo tests of the host logic -- the per-rank exchange plan
+derived from the reference-order ledger, and the span send/recv itself on
+DisagSoA/SoA/AoS buffers (the NCCL comparison path's exchange, run over gloo).
+GPU: two ranks sharing one device exercise the real zero-copy path (CUDA IPC
+buffers, device step flags) and must stay bitwise equal to the oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import oracle as O
+import paper_2503_07898_b200 as V
+from paper_2503_07898_b200.multigpu import exchange_plan
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("layout", ["AoS", "SoA", "DisagSoA"])
+def test_exchange_plan_pairs_up(world, layout):
+    desc = dict(lattice="D3Q19", domain=(8, 8, 4 * world), layout=layout)
+    plans = [exchange_plan(r, world, **desc) for r in range(world)]
+    for r, (sends, _) in enumerate(plans):
+        for peer, _, n in sends:
+            recvs_of_peer = [x for x in plans[peer][1] if x[0] == r]
+            assert n in [x[2] for x in recvs_of_peer]
+        expect = {"DisagSoA": 1, "SoA": 5, "AoS": 1}[layout]
+        for nb in (r - 1, r + 1):
+            if 0 <= nb < world:
+                assert len([s for s in sends if s[0] == nb]) == expect
+
+
+def _halo_worker(rank, world, port, layout, result_q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_07898_b200.multigpu import exchange_halos
+
+    dom = (6, 5, 4 * world)
+    q = 19
+    canon = np.arange(dom[0] * dom[1] * dom[2] * q, dtype=np.float64) + 0.5
+    slabs = V.decompose(dom, world, 2)
+    k0, k1 = slabs[rank]
+    shape = (dom[0], dom[1], k1 - k0)
+    addr = V.layout_addresses(layout, shape, "D3Q19", 2).reshape(shape[2] + 2, dom[1], dom[0], q)
+    buf = np.zeros(addr.size, np.float64)
+    g = canon.reshape(dom[2], dom[1], dom[0], q)
+    buf[addr[1:-1].ravel()] = g[k0:k1].ravel()
+    t = torch.from_numpy(buf)
+    sends, recvs = exchange_plan(rank, world, lattice="D3Q19", domain=dom, layout=layout)
+    exchange_halos(dist, t, sends, recvs)
+    ok = True
+    lat = np.array([[0, 0, 0], [-1, 0, 0], [0, -1, 0], [0, 0, -1], [0, 0, 1], [0, 1, 0], [1, 0, 0]])
+    up = [4, 9, 12, 14, 17]  # e_z > 0 (halo UH holds these), down = e_z < 0 (halo LH)
+    down = [3, 8, 11, 13, 16]
+    if rank > 0:  # upper halo = upper neighbour's last slab, up-crossing set (all comps for AoS)
+        comps = range(q) if layout == "AoS" else up
+        for c in comps:
+            ok &= np.array_equal(buf[addr[0, :, :, c].ravel()], g[k0 - 1, :, :, c].ravel())
+    if rank < world - 1:
+        comps = range(q) if layout == "AoS" else down
+        for c in comps:
+            ok &= np.array_equal(buf[addr[-1, :, :, c].ravel()], g[k1, :, :, c].ravel())
+    _ = lat
+    result_q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("layout", ["SoA", "DisagSoA", "AoS"])
+def test_gloo_span_exchange_fills_halos(world, layout):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, layout, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()), res
+
+
+def _gpu_worker(rank, world, port, result_q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_07898_b200.multigpu import DistributedDense
+
+    dom = (24, 20, 32)
+    eng = DistributedDense(domain=dom, precision="fp64", halo_mode="zero_copy")
+    init = O.port_initial_state("D3Q19", dom)
+    k0, k1 = eng.slab()
+    s = dom[0] * dom[1] * 19
+    eng.set_canonical_planes(init[k0 * s:k1 * s], k0, k1)
+    eng.refresh_halos()
+    eng.step(30)
+    out = eng.get_canonical_planes(k0, k1)
+    d = eng.probe()
+    result_q.put((rank, k0, k1, out, d.mass))
+    dist.barrier()
+    eng.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_zero_copy_multiprocess_bitwise(world):
+    """Ranks share cuda:0 here (the box has one GPU per call); the IPC buffers,
+    peer stores and device step flags are the same code path as on 8 GPUs."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    dom = (24, 20, 32)
+    ref = O.port_dense_run("D3Q19", dom, 0.56, "lid_driven_cavity", (0.05, 0, 0), 30)
+    s = dom[0] * dom[1] * 19
+    for rank, k0, k1, out, mass in res:
+        assert np.array_equal(out, ref[k0 * s:k1 * s]), f"rank {rank} differs"
+    m_ref, _ = O.port_probe("D3Q19", ref)
+    assert abs(res[0][4] - m_ref) <= 1e-12 * m_ref

@@ -147,6 +147,64 @@ int voxl_dense_attach_flags(voxl_dense* h, void* upper_slot, void* lower_slot);
 int voxl_dense_halo_push(voxl_dense* h);
 int voxl_dense_owned_voxels(voxl_dense* h, int64_t* voxels);
 
+/* ---- block-sparse engine (sparse::SparseLbmEngine, sparse.hpp:175-213) --------- */
+
+typedef struct voxl_sparse voxl_sparse;
+
+typedef struct {
+    int lattice;        /* VOXL_D3Q19 | VOXL_D3Q27 */
+    int nx, ny, nz;
+    double tau;
+    double u_bc[3];     /* regularized inflow/outflow velocity (SparseScenario::wind_tunnel) */
+    int block_edge;     /* 4 (reference tables) or 8 (B200 production) */
+    int strategy;       /* VOXL_NAIVE | VOXL_DISAG_BITMASK | VOXL_DISAG_MEM */
+    int precision;      /* VOXL_F32 | VOXL_F64 */
+} voxl_sparse_desc;
+
+/** Active set of run_sparse (solver.cpp:272-283): box minus sphere of `radius`
+ *  (<= 0: min extent / 5) centred at (n/2 - 0.5); x fastest bytes. */
+int voxl_obstacle_mask(int nx, int ny, int nz, double radius, uint8_t* out, int64_t* active);
+/** BlockSparseGrid::build + classify_blocks + arrange + dispatch_plan
+ *  (sparse.cpp:20, :109, :144, :199) and device buffers at rest equilibrium. */
+int voxl_sparse_create(const voxl_sparse_desc* desc, const uint8_t* active, voxl_sparse** out);
+int voxl_sparse_destroy(voxl_sparse* h);
+/** The same grid, classification, arrangement and plan with no device
+ *  allocation (host tables only); the getters below accept either handle
+ *  kind through voxl_sparse_plan_of. */
+typedef struct voxl_sparse_plan voxl_sparse_plan;
+int voxl_sparse_plan_create(const voxl_sparse_desc* desc, const uint8_t* active, voxl_sparse_plan** out);
+int voxl_sparse_plan_destroy(voxl_sparse_plan* p);
+/** Host tables of an engine (owned by the engine). */
+int voxl_sparse_plan_of(voxl_sparse* h, voxl_sparse_plan** out);
+int voxl_sparse_plan_info(voxl_sparse_plan* p, int64_t* num_active, int* num_blocks, int64_t* n_boundary,
+                          int64_t* n_non_boundary);
+int voxl_sparse_plan_blocks(voxl_sparse_plan* p, int* origins, uint64_t* masks, uint8_t* classes);
+int voxl_sparse_plan_arrangement(voxl_sparse_plan* p, int* permutation, uint8_t* bitmask, int32_t* meta_index,
+                                 int64_t* boundary_voxels);
+int voxl_sparse_plan_report_json(voxl_sparse_plan* p, char* out, int64_t cap, int64_t* len);
+/** 27-neighbour block table, d = (dx+1) + 3(dy+1) + 9(dz+1), -1 when absent. */
+int voxl_sparse_plan_neighbours(voxl_sparse_plan* p, int32_t* out);
+int voxl_sparse_info(voxl_sparse* h, int64_t* num_active, int* num_blocks, int64_t* n_boundary,
+                     int64_t* n_non_boundary);
+/** Blocks in list order: origins (3 ints), masks (block_edge^3/64 words, >= 1), class (1 = boundary). */
+int voxl_sparse_blocks(voxl_sparse* h, int* origins, uint64_t* masks, uint8_t* classes);
+/** Arrangement (sparse.hpp:101-107): permutation, bitmask, voxel_meta_index (any may be NULL). */
+int voxl_sparse_arrangement(voxl_sparse* h, int* permutation, uint8_t* bitmask, int32_t* meta_index,
+                            int64_t* boundary_voxels);
+/** ExecutionReport::to_json (sparse.cpp:240-251). */
+int voxl_sparse_report_json(voxl_sparse* h, char* out, int64_t cap, int64_t* len);
+/** canonical_state / set_state (sparse.cpp:416-453): pack_coord order, q per voxel. */
+int voxl_sparse_get_state(voxl_sparse* h, double* canonical);
+int voxl_sparse_set_state(voxl_sparse* h, const double* canonical);
+int voxl_sparse_set_equilibrium(voxl_sparse* h, double rho, const double* u);
+/** n x SparseLbmEngine::step (sparse.cpp:386-394). */
+int voxl_sparse_step(voxl_sparse* h, int n);
+int voxl_sparse_timed_steps(voxl_sparse* h, int n, double* total_ms, double* boundary_ms, double* light_ms);
+int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out);
+/** dispatch_plan(...).to_json() (sparse.cpp:199-225; Table 2). */
+int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int block_size, int s_w, int s_i,
+                            int naive_full_domain_storage, char* out, int64_t cap, int64_t* len);
+
 /* ---- CUDA IPC helpers (64-byte cudaIpcMemHandle_t as bytes) ------------------- */
 int voxl_ipc_export(void* dev_ptr, char* handle64);
 int voxl_ipc_open(const char* handle64, void** dev_ptr);

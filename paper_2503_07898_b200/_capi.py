@@ -62,8 +62,7 @@ class TransferRecordC(C.Structure):
 
 class SparseDesc(C.Structure):
     _fields_ = [("lattice", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("tau", C.c_double),
-                ("u_bc", C.c_double * 3), ("block_edge", C.c_int), ("strategy", C.c_int), ("precision", C.c_int),
-                ("kernel_split", C.c_int)]
+                ("u_bc", C.c_double * 3), ("block_edge", C.c_int), ("strategy", C.c_int), ("precision", C.c_int)]
 
 
 class MresDesc(C.Structure):
@@ -111,6 +110,31 @@ def _load():
         "voxl_dense_attach_flags": ([vp, vp, vp], C.c_int),
         "voxl_dense_halo_push": ([vp], C.c_int),
         "voxl_dense_owned_voxels": ([vp, C.POINTER(i64)], C.c_int),
+        "voxl_obstacle_mask": ([C.c_int, C.c_int, C.c_int, C.c_double, vp, C.POINTER(i64)], C.c_int),
+        "voxl_sparse_create": ([C.POINTER(SparseDesc), vp, C.POINTER(vp)], C.c_int),
+        "voxl_sparse_destroy": ([vp], C.c_int),
+        "voxl_sparse_plan_create": ([C.POINTER(SparseDesc), vp, C.POINTER(vp)], C.c_int),
+        "voxl_sparse_plan_destroy": ([vp], C.c_int),
+        "voxl_sparse_plan_of": ([vp, C.POINTER(vp)], C.c_int),
+        "voxl_sparse_plan_info": ([vp, C.POINTER(i64), C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(i64)],
+                                  C.c_int),
+        "voxl_sparse_plan_blocks": ([vp, vp, vp, vp], C.c_int),
+        "voxl_sparse_plan_arrangement": ([vp, vp, vp, vp, C.POINTER(i64)], C.c_int),
+        "voxl_sparse_plan_report_json": ([vp, cp, i64, C.POINTER(i64)], C.c_int),
+        "voxl_sparse_plan_neighbours": ([vp, vp], C.c_int),
+        "voxl_sparse_info": ([vp, C.POINTER(i64), C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(i64)], C.c_int),
+        "voxl_sparse_blocks": ([vp, vp, vp, vp], C.c_int),
+        "voxl_sparse_arrangement": ([vp, vp, vp, vp, C.POINTER(i64)], C.c_int),
+        "voxl_sparse_report_json": ([vp, cp, i64, C.POINTER(i64)], C.c_int),
+        "voxl_sparse_get_state": ([vp, vp], C.c_int),
+        "voxl_sparse_set_state": ([vp, vp], C.c_int),
+        "voxl_sparse_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
+        "voxl_sparse_step": ([vp, C.c_int], C.c_int),
+        "voxl_sparse_timed_steps": ([vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double)], C.c_int),
+        "voxl_sparse_probe": ([vp, C.POINTER(Diag)], C.c_int),
+        "voxl_dispatch_plan_json": ([C.c_int, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, cp, i64,
+                                     C.POINTER(i64)], C.c_int),
         "voxl_ipc_export": ([vp, vp], C.c_int),
         "voxl_ipc_open": ([vp, C.POINTER(vp)], C.c_int),
         "voxl_ipc_close": ([vp], C.c_int),

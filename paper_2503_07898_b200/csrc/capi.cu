@@ -9,6 +9,7 @@
 #include "dense.cuh"
 #include "grid.hpp"
 #include "lattice.cuh"
+#include "sparse.cuh"
 
 using namespace voxl_b200;
 
@@ -316,6 +317,170 @@ int voxl_dense_halo_push(voxl_dense* h) {
 
 int voxl_dense_owned_voxels(voxl_dense* h, int64_t* voxels) {
     return guarded([&] { *voxels = h->eng->owned_voxels(); });
+}
+
+int voxl_obstacle_mask(int nx, int ny, int nz, double radius, uint8_t* out, int64_t* active) {
+    return guarded([&] {
+        // solver.cpp:272-283 (same double arithmetic)
+        const int mn = std::min(nx, std::min(ny, nz));
+        const double r = radius > 0.0 ? radius : mn / 5.0;
+        const double cx = nx / 2.0 - 0.5, cy = ny / 2.0 - 0.5, cz = nz / 2.0 - 0.5;
+        int64_t n = 0;
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    const double dx = x - cx, dy = y - cy, dz = z - cz;
+                    const bool a = dx * dx + dy * dy + dz * dz > r * r;
+                    out[(int64_t(z) * ny + y) * nx + x] = a;
+                    n += a;
+                }
+        if (active) *active = n;
+    });
+}
+
+int voxl_sparse_create(const voxl_sparse_desc* d, const uint8_t* active, voxl_sparse** out) {
+    return guarded([&] {
+        require(d && active && out, "voxl_sparse_create: null argument");
+        SparseConfig c;
+        c.lattice = d->lattice;
+        c.domain = {d->nx, d->ny, d->nz};
+        c.tau = d->tau;
+        c.u_bc = {d->u_bc[0], d->u_bc[1], d->u_bc[2]};
+        c.edge = d->block_edge;
+        require(d->strategy >= 0 && d->strategy <= 2, "unknown sparse strategy");
+        c.strategy = Strategy(d->strategy);
+        require(d->precision == VOXL_F32 || d->precision == VOXL_F64, "unknown precision");
+        c.precision = Precision(d->precision);
+        *out = reinterpret_cast<voxl_sparse*>(new SparseEngine(c, active));
+    });
+}
+
+int voxl_sparse_destroy(voxl_sparse* h) {
+    return guarded([&] { delete reinterpret_cast<SparseEngine*>(h); });
+}
+
+static SparseEngine* SP(voxl_sparse* h) { return reinterpret_cast<SparseEngine*>(h); }
+static SparseTables* PL(voxl_sparse_plan* p) { return reinterpret_cast<SparseTables*>(p); }
+
+int voxl_sparse_plan_create(const voxl_sparse_desc* d, const uint8_t* active, voxl_sparse_plan** out) {
+    return guarded([&] {
+        require(d && active && out, "voxl_sparse_plan_create: null argument");
+        require(d->strategy >= 0 && d->strategy <= 2, "unknown sparse strategy");
+        require(d->lattice >= 0 && d->lattice <= 2, "unknown lattice kind");
+        auto* t = new SparseTables(SparseTables::build({d->nx, d->ny, d->nz}, active, d->block_edge,
+                                                       Strategy(d->strategy), make_lattice(d->lattice).q));
+        *out = reinterpret_cast<voxl_sparse_plan*>(t);
+    });
+}
+
+int voxl_sparse_plan_destroy(voxl_sparse_plan* p) {
+    return guarded([&] { delete PL(p); });
+}
+
+int voxl_sparse_plan_of(voxl_sparse* h, voxl_sparse_plan** out) {
+    return guarded([&] { *out = reinterpret_cast<voxl_sparse_plan*>(&SP(h)->tables()); });
+}
+
+int voxl_sparse_plan_info(voxl_sparse_plan* p, int64_t* na, int* nb, int64_t* nbd, int64_t* nnb) {
+    return guarded([&] {
+        if (na) *na = PL(p)->grid.num_active();
+        if (nb) *nb = PL(p)->grid.num_blocks();
+        if (nbd) *nbd = PL(p)->classes.n_boundary;
+        if (nnb) *nnb = PL(p)->classes.n_non_boundary;
+    });
+}
+
+int voxl_sparse_plan_blocks(voxl_sparse_plan* p, int* origins, uint64_t* masks, uint8_t* classes) {
+    return guarded([&] {
+        const BlockGrid& g = PL(p)->grid;
+        for (int b = 0; b < g.num_blocks(); ++b) {
+            if (origins)
+                for (int a = 0; a < 3; ++a) origins[3 * b + a] = g.blocks()[b].origin[a];
+            if (masks)
+                for (int w = 0; w < g.mask_words(); ++w) masks[std::size_t(b) * g.mask_words() + w] = g.mask(b, w);
+            if (classes) classes[b] = PL(p)->classes.classes[b];
+        }
+    });
+}
+
+int voxl_sparse_plan_arrangement(voxl_sparse_plan* p, int* perm, uint8_t* bitmask, int32_t* meta, int64_t* count) {
+    return guarded([&] {
+        const Arrangement& a = PL(p)->arr;
+        if (perm) std::memcpy(perm, a.permutation.data(), a.permutation.size() * sizeof(int));
+        if (bitmask && !a.boundary_bitmask.empty())
+            std::memcpy(bitmask, a.boundary_bitmask.data(), a.boundary_bitmask.size());
+        if (meta && !a.voxel_meta_index.empty())
+            std::memcpy(meta, a.voxel_meta_index.data(), a.voxel_meta_index.size() * sizeof(int32_t));
+        if (count) *count = a.boundary_voxel_count;
+    });
+}
+
+int voxl_sparse_plan_report_json(voxl_sparse_plan* p, char* out, int64_t cap, int64_t* len) {
+    return guarded([&] { put_text(PL(p)->plan.to_json(true), out, cap, len); });
+}
+
+int voxl_sparse_plan_neighbours(voxl_sparse_plan* p, int32_t* out) {
+    return guarded([&] {
+        const auto t = PL(p)->grid.neighbour_table();
+        std::memcpy(out, t.data(), t.size() * sizeof(int32_t));
+    });
+}
+
+int voxl_sparse_info(voxl_sparse* h, int64_t* na, int* nb, int64_t* nbd, int64_t* nnb) {
+    return voxl_sparse_plan_info(reinterpret_cast<voxl_sparse_plan*>(&SP(h)->tables()), na, nb, nbd, nnb);
+}
+
+int voxl_sparse_blocks(voxl_sparse* h, int* origins, uint64_t* masks, uint8_t* classes) {
+    return voxl_sparse_plan_blocks(reinterpret_cast<voxl_sparse_plan*>(&SP(h)->tables()), origins, masks, classes);
+}
+
+int voxl_sparse_arrangement(voxl_sparse* h, int* perm, uint8_t* bitmask, int32_t* meta, int64_t* count) {
+    return voxl_sparse_plan_arrangement(reinterpret_cast<voxl_sparse_plan*>(&SP(h)->tables()), perm, bitmask, meta,
+                                        count);
+}
+
+int voxl_sparse_report_json(voxl_sparse* h, char* out, int64_t cap, int64_t* len) {
+    return voxl_sparse_plan_report_json(reinterpret_cast<voxl_sparse_plan*>(&SP(h)->tables()), out, cap, len);
+}
+
+int voxl_sparse_get_state(voxl_sparse* h, double* canonical) {
+    return guarded([&] { SP(h)->get_state(canonical); });
+}
+
+int voxl_sparse_set_state(voxl_sparse* h, const double* canonical) {
+    return guarded([&] { SP(h)->set_state(canonical); });
+}
+
+int voxl_sparse_set_equilibrium(voxl_sparse* h, double rho, const double* u) {
+    return guarded([&] { SP(h)->set_equilibrium(rho, u); });
+}
+
+int voxl_sparse_step(voxl_sparse* h, int n) {
+    return guarded([&] { SP(h)->step(n); });
+}
+
+int voxl_sparse_timed_steps(voxl_sparse* h, int n, double* total, double* bms, double* lms) {
+    return guarded([&] { *total = SP(h)->timed_steps(n, bms, lms); });
+}
+
+int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out) {
+    return guarded([&] {
+        const DenseDiag d = SP(h)->probe();
+        out->mass = d.mass;
+        out->max_speed = d.max_speed;
+        out->unstable = d.unstable;
+        out->bad_population = d.bad_population;
+        out->bad_voxel = d.bad_voxel;
+    });
+}
+
+int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int bs, int s_w, int s_i, int full,
+                            char* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        require(strategy >= 0 && strategy <= 2, "unknown sparse strategy");
+        put_text(dispatch_plan(Strategy(strategy), n_b, n_nb, q, bs, s_w, s_i, full != 0).to_json(false), out, cap,
+                 len);
+    });
 }
 
 int voxl_ipc_export(void* dev_ptr, char* handle64) {

@@ -1,0 +1,642 @@
+// sparse.cu -- block-sparse kernels and engine (see sparse.cuh).
+//
+// One CTA per block (E^3 threads, one voxel each). The CTA stages its 27
+// neighbour-block indices and activity masks in shared memory; each pull then
+// resolves "source active?" with a shared-memory bit test and reads the source
+// population straight from the neighbour block's SoA plane (a warp covers
+// 32 / E rows of one block, so a plane read is one contiguous run plus the
+// lanes that cross into the x-neighbour block). Inactive sources bounce back
+// off the voxel's own opposite population (sparse.cpp:321-345). Algorithmic
+// traffic: 2*Q*sizeof(real) per active voxel, plus 27 ints and 27*E^3/8 mask
+// bytes per block of metadata (L2-resident, < 0.2 % at E = 8).
+#include "sparse.cuh"
+#include "lattice.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+namespace voxl_b200 {
+
+namespace {
+
+// Velocity source of the regularized boundary (Table 2 "indexing" column).
+enum VelSource : int { kVelConst = 0, kVelIndirect = 1, kVelInline = 2 };
+// Kernel flavours.
+enum SparseMode : int { kLight = 0, kHeavy = 1 };
+
+template <int Q, class R>
+struct SparseArgs {
+    const R* cur;
+    R* nxt;
+    const std::int32_t* nbr;      // 27 per block
+    const std::uint64_t* masks;   // WORDS per block
+    const int* origins;           // 3 per block
+    int block_begin;
+    const std::uint8_t* bitmask;  // DisagBitmask: skip blocks whose bit != want
+    int bitmask_want;
+    int vel_source;
+    const std::int32_t* meta_index;  // per slot (DisagBitmask)
+    const R* compact_meta;           // 3 per boundary voxel (DisagBitmask)
+    const R* naive_meta;             // 3 per slot (Naive)
+    R u_bc[3];
+    int nx;
+    R omega, keep;
+    double shift[Q];  // w_i for shifted fp32 storage
+    int step;
+    int* error_flag;
+};
+
+/// equilibrium (lattice.cpp:104-113) at given (rho, u), reference op order.
+template <class L, class R, bool Exact>
+__device__ __forceinline__ void equilibrium_dev(R rho, const R (&u)[3], R (&feq)[L::Q]) {
+    using A = Arith<R, Exact>;
+    const R uu = A::add(A::add(A::mul(u[0], u[0]), A::mul(u[1], u[1])), A::mul(u[2], u[2]));
+    const R c15uu = A::mul(R(1.5), uu);
+    static_for<L::Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        R eu = R(0);
+        eu = acc_term<R, Exact, L::ex(i)>(eu, u[0]);
+        eu = acc_term<R, Exact, L::ey(i)>(eu, u[1]);
+        eu = acc_term<R, Exact, L::ez(i)>(eu, u[2]);
+        constexpr double wi = L::w(i);
+        const R poly = A::sub(A::add(A::add(R(1), A::mul(R(3), eu)), A::mul(A::mul(R(4.5), eu), eu)), c15uu);
+        feq[i] = A::mul(A::mul(R(wi), rho), poly);
+    });
+}
+
+/// regularized_reconstruct (lbm.cpp:10-59) for a face with inward normal
+/// +-x (the wind tunnel's only regularized faces), reference op order.
+template <class L, class R, bool Exact>
+__device__ __forceinline__ bool regularized_dev(int sign, const R (&ubc)[3], R (&f)[L::Q]) {
+    using A = Arith<R, Exact>;
+    const R u_n = A::mul(ubc[0], R(sign));
+    if (!(fabs(A::sub(R(1), u_n)) > R(1e-12))) return false;
+    R sum0 = R(0), sum_in = R(0);
+    static_for<L::Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int ex = L::ex(i);
+        const int en = ex * sign;
+        if (en == 0) sum0 = A::add(sum0, f[i]);
+        else if (en < 0) sum_in = A::add(sum_in, f[i]);
+    });
+    R rho;
+    if constexpr (Exact) rho = A::add(sum0, A::mul(R(2), sum_in)) / A::sub(R(1), u_n);
+    else rho = (sum0 + R(2) * sum_in) / (R(1) - u_n);
+    R feq[L::Q];
+    equilibrium_dev<L, R, Exact>(rho, ubc, feq);
+    R fneq[L::Q];
+    static_for<L::Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int oi = L::opp(i);
+        const int en = L::ex(i) * sign;
+        fneq[i] = en > 0 ? A::sub(f[oi], feq[oi]) : A::sub(f[i], feq[i]);
+    });
+    // Pi_ab = sum_i fneq_i e_ia e_ib (sequential over i; zero terms skipped).
+    R pi[3][3];
+    static_for<3>([&](auto AA) {
+        constexpr int a = decltype(AA)::value;
+        static_for<3>([&](auto BB) {
+            constexpr int b = decltype(BB)::value;
+            R acc = R(0);
+            static_for<L::Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                acc = acc_term<R, Exact, L::e(i, a) * L::e(i, b)>(acc, fneq[i]);
+            });
+            pi[a][b] = acc;
+        });
+    });
+    constexpr double cs2 = 1.0 / 3.0;
+    constexpr double cdiag1 = 1.0 - cs2, cdiag0 = 0.0 - cs2;
+    static_for<L::Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        R qpi = R(0);
+        static_for<3>([&](auto AA) {
+            constexpr int a = decltype(AA)::value;
+            static_for<3>([&](auto BB) {
+                constexpr int b = decltype(BB)::value;
+                constexpr int eab = L::e(i, a) * L::e(i, b);
+                if constexpr (a == b) {
+                    constexpr double c = eab ? cdiag1 : cdiag0;
+                    qpi = A::add(qpi, A::mul(R(c), pi[a][b]));
+                } else {
+                    qpi = acc_term<R, Exact, eab>(qpi, pi[a][b]);
+                }
+            });
+        });
+        constexpr double wi = L::w(i);
+        f[i] = A::add(feq[i], A::mul(A::mul(R(wi), R(4.5)), qpi));
+    });
+    return true;
+}
+
+template <class L, class R, bool Exact, int E, int MODE>
+__global__ void __launch_bounds__(E* E* E) sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
+    constexpr int Q = L::Q;
+    constexpr int BV = E * E * E;
+    constexpr int W = BV >= 64 ? BV / 64 : 1;
+    const int b = A.block_begin + int(blockIdx.x);
+    if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip
+    __shared__ int s_nbr[27];
+    __shared__ unsigned long long s_mask[27][W];
+    const int t = threadIdx.x;
+    if (t < 27) s_nbr[t] = A.nbr[(long long)b * 27 + t];
+    __syncthreads();
+    for (int j = t; j < 27 * W; j += BV) {
+        const int d = j / W, w = j % W;
+        const int nb = s_nbr[d];
+        s_mask[d][w] = nb >= 0 ? A.masks[(long long)nb * W + w] : 0ull;
+    }
+    __syncthreads();
+    if (!((s_mask[13][t >> 6] >> (t & 63)) & 1ull)) return;  // inactive slot
+    const int lx = t % E, ly = (t / E) % E, lz = t / (E * E);
+    const long long self_base = (long long)b * Q * BV;
+
+    R g[Q];
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
+        constexpr int oi = L::opp(i);
+        const int sx = lx - ex, sy = ly - ey, sz = lz - ez;
+        const int dx = ex == 0 ? 1 : (sx < 0 ? 0 : (sx >= E ? 2 : 1));
+        const int dy = ey == 0 ? 1 : (sy < 0 ? 0 : (sy >= E ? 2 : 1));
+        const int dz = ez == 0 ? 1 : (sz < 0 ? 0 : (sz >= E ? 2 : 1));
+        const int d = dx + 3 * dy + 9 * dz;
+        const int sl = ((sz & (E - 1)) * E + (sy & (E - 1))) * E + (sx & (E - 1));
+        const bool solid = !((s_mask[d][sl >> 6] >> (sl & 63)) & 1ull);
+        const long long src = solid ? self_base + (long long)oi * BV + t
+                                    : (long long)s_nbr[d] * Q * BV + (long long)i * BV + sl;
+        g[i] = __ldg(A.cur + src);
+    });
+
+    bool ok = true;
+    if constexpr (MODE == kHeavy) {
+        const int x = A.origins[3 * b] + lx;
+        if (x == 0 || x == A.nx - 1) {
+            R u[3];
+            if (A.vel_source == kVelConst) {
+                u[0] = A.u_bc[0];
+                u[1] = A.u_bc[1];
+                u[2] = A.u_bc[2];
+            } else if (A.vel_source == kVelIndirect) {
+                const int id = A.meta_index[(long long)b * BV + t];
+                u[0] = A.compact_meta[3 * (long long)id];
+                u[1] = A.compact_meta[3 * (long long)id + 1];
+                u[2] = A.compact_meta[3 * (long long)id + 2];
+            } else {
+                const long long s3 = 3 * ((long long)b * BV + t);
+                u[0] = A.naive_meta[s3];
+                u[1] = A.naive_meta[s3 + 1];
+                u[2] = A.naive_meta[s3 + 2];
+            }
+            if constexpr (!Exact) {  // reconstruct on the unshifted populations
+                static_for<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    g[i] += R(A.shift[i]);
+                });
+            }
+            ok = regularized_dev<L, R, Exact>(x == 0 ? 1 : -1, u, g);
+            if constexpr (!Exact) {
+                static_for<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    g[i] -= R(A.shift[i]);
+                });
+            }
+        }
+    }
+    R rho, uu[3];
+    if constexpr (Exact) bgk_relax<L, R, true>(g, A.omega, A.keep, rho, uu, ok);
+    else bgk_relax_shifted<L, R>(g, A.omega, A.keep, rho, uu, ok);
+    if (!ok) atomicMin(A.error_flag, A.step);
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        A.nxt[self_base + (long long)i * BV + t] = g[i];
+    });
+}
+
+template <int Q, class R, bool ToDevice>
+__global__ void sparse_io_kernel(R* buf, double* staging, const std::int64_t* slots, long long n, int bv,
+                                 const __grid_constant__ SparseArgs<Q, R> A) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const long long slot = slots[v];
+    const long long b = slot / bv, local = slot % bv;
+    for (int c = 0; c < Q; ++c) {
+        R* p = buf + (b * Q + c) * bv + local;
+        if constexpr (ToDevice) *p = R(staging[v * Q + c] - A.shift[c]);
+        else staging[v * Q + c] = double(*p) + A.shift[c];
+    }
+}
+
+template <int Q, class R>
+__global__ void sparse_fill_kernel(R* buf, long long total, int bv, const __grid_constant__ SparseArgs<Q, R> A) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int c = int((e / bv) % Q);
+    buf[e] = R(A.shift[c]);  // shift[] carries (feq - storage shift) here
+}
+
+template <class L, class R>
+__global__ void sparse_probe_kernel(const R* buf, const std::int64_t* slots, long long n, int bv,
+                                    const __grid_constant__ SparseArgs<L::Q, R> A, double* partial,
+                                    unsigned long long* bad) {
+    constexpr int Q = L::Q;
+    double mass = 0.0, vmax = 0.0;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
+        const long long slot = slots[v];
+        const long long b = slot / bv, local = slot % bv;
+        double f[Q];
+        bool badv = false;
+        int bp = 0;
+        double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+        for (int c = 0; c < Q; ++c) {
+            f[c] = double(buf[(b * Q + c) * bv + local]) + A.shift[c];
+            if (!badv && (!isfinite(f[c]) || fabs(f[c]) > 1e3)) {
+                badv = true;
+                bp = c;
+            }
+        }
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            mass += f[i];
+            r += f[i];
+            mx = acc_term<double, false, L::ex(i)>(mx, f[i]);
+            my = acc_term<double, false, L::ey(i)>(my, f[i]);
+            mz = acc_term<double, false, L::ez(i)>(mz, f[i]);
+        });
+        if (badv || !(r > 0.0)) {
+            atomicMin(bad, ((unsigned long long)v << 5) | (unsigned long long)bp);
+        } else {
+            const double ux = mx / r, uy = my / r, uz = mz / r;
+            vmax = fmax(vmax, sqrt(ux * ux + uy * uy + uz * uz));
+        }
+    }
+    __shared__ double sm[256], sv[256];
+    sm[threadIdx.x] = mass;
+    sv[threadIdx.x] = vmax;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sm[threadIdx.x] += sm[threadIdx.x + w];
+            sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = sm[0];
+        partial[2 * blockIdx.x + 1] = sv[0];
+    }
+}
+
+__global__ void sparse_probe_final(const double* partial, int n, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double m = 0.0, v = 0.0;
+        for (int i = 0; i < n; ++i) {
+            m += partial[2 * i];
+            v = fmax(v, partial[2 * i + 1]);
+        }
+        out[0] = m;
+        out[1] = v;
+    }
+}
+
+constexpr int kSpProbeBlocks = 592;
+
+template <class L, class R, bool Exact>
+struct SparseOps {
+    static constexpr int Q = L::Q;
+
+    static SparseArgs<Q, R> base_args(const SparseConfig& cfg) {
+        SparseArgs<Q, R> A{};
+        const double inv_tau = 1.0 / cfg.tau;
+        A.omega = R(inv_tau);
+        A.keep = Exact ? R(1.0 - inv_tau) : R(1) - R(inv_tau);
+        for (int a = 0; a < 3; ++a) A.u_bc[a] = R(cfg.u_bc[a]);
+        A.nx = cfg.domain[0];
+        for (int c = 0; c < Q; ++c) A.shift[c] = Exact ? 0.0 : L::w(c);
+        return A;
+    }
+
+    template <int E>
+    static void launch_e(SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
+        if (nblocks <= 0) return;
+        if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy><<<nblocks, E * E * E, 0, st>>>(A);
+        else sparse_step_kernel<L, R, Exact, E, kLight><<<nblocks, E * E * E, 0, st>>>(A);
+        VOXL_CUDA(cudaGetLastError());
+    }
+
+    static void launch(int edge, SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
+        switch (edge) {
+            case 4: launch_e<4>(A, mode, nblocks, st); break;
+            case 8: launch_e<8>(A, mode, nblocks, st); break;
+            default: throw std::invalid_argument("sparse engine: device kernels support block edge 4 or 8");
+        }
+    }
+};
+
+template <class F>
+void sparse_dispatch(int lattice, Precision prec, F&& f) {
+    auto by_prec = [&](auto lat) {
+        using L = decltype(lat);
+        if (prec == Precision::F64) f(SparseOps<L, double, true>{});
+        else f(SparseOps<L, float, false>{});
+    };
+    switch (lattice) {
+        case kD3Q19: by_prec(D3Q19{}); break;
+        case kD3Q27: by_prec(D3Q27{}); break;
+        default: throw std::invalid_argument("sparse engine: D3Q19 or D3Q27 only (3D wind tunnel)");
+    }
+}
+
+} // namespace
+
+SparseEngine::SparseEngine(const SparseConfig& cfg, const std::uint8_t* active) : cfg_(cfg) {
+    if (!(cfg_.tau > 0.5)) throw std::invalid_argument("sparse engine: tau must be > 0.5");
+    if (cfg_.lattice != kD3Q19 && cfg_.lattice != kD3Q27)
+        throw std::invalid_argument("sparse engine: D3Q19 or D3Q27 only (3D wind tunnel)");
+    if (cfg_.edge != 4 && cfg_.edge != 8) throw std::invalid_argument("sparse engine: block edge must be 4 or 8");
+    q_ = make_lattice(cfg_.lattice).q;
+    esize_ = cfg_.precision == Precision::F64 ? 8 : 4;
+    T_ = SparseTables::build(cfg_.domain, active, cfg_.edge, cfg_.strategy, q_);
+
+    VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    const std::size_t nb = std::size_t(grid_.num_blocks());
+    const std::size_t bytes = nb * q_ * grid_.block_volume() * esize_;
+    for (auto& b : buf_) {
+        VOXL_CUDA(cudaMalloc(&b, bytes));
+        VOXL_CUDA(cudaMemsetAsync(b, 0, bytes, stream_));
+    }
+    const auto nbr = grid_.neighbour_table();
+    VOXL_CUDA(cudaMalloc(&d_nbr_, nbr.size() * sizeof(std::int32_t)));
+    VOXL_CUDA(cudaMemcpy(d_nbr_, nbr.data(), nbr.size() * sizeof(std::int32_t), cudaMemcpyHostToDevice));
+    VOXL_CUDA(cudaMalloc(&d_masks_, grid_.masks().size() * sizeof(std::uint64_t)));
+    VOXL_CUDA(cudaMemcpy(d_masks_, grid_.masks().data(), grid_.masks().size() * sizeof(std::uint64_t),
+                         cudaMemcpyHostToDevice));
+    std::vector<int> org(nb * 3);
+    for (std::size_t b = 0; b < nb; ++b)
+        for (int a = 0; a < 3; ++a) org[3 * b + a] = grid_.blocks()[b].origin[a];
+    VOXL_CUDA(cudaMalloc(&d_origins_, org.size() * sizeof(int)));
+    VOXL_CUDA(cudaMemcpy(d_origins_, org.data(), org.size() * sizeof(int), cudaMemcpyHostToDevice));
+    // Boundary-velocity metadata per strategy (sparse.cpp:271-295).
+    auto upload_real = [&](const std::vector<double>& v, void** dst) {
+        VOXL_CUDA(cudaMalloc(dst, std::max<std::size_t>(1, v.size()) * esize_));
+        if (esize_ == 8) {
+            VOXL_CUDA(cudaMemcpy(*dst, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<float> f(v.begin(), v.end());
+            VOXL_CUDA(cudaMemcpy(*dst, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+        }
+    };
+    const int e = grid_.edge(), nx = cfg_.domain[0];
+    if (cfg_.strategy == Strategy::Naive) {
+        std::vector<double> meta(nb * grid_.block_volume() * 3, 0.0);
+        for (std::size_t b = 0; b < nb; ++b)
+            for (int local = 0; local < grid_.block_volume(); ++local) {
+                if (!grid_.bit(int(b), local)) continue;
+                const int x = grid_.blocks()[b].origin[0] + local % e;
+                if (x == 0 || x == nx - 1)
+                    for (int d = 0; d < 3; ++d) meta[(b * grid_.block_volume() + local) * 3 + d] = cfg_.u_bc[d];
+            }
+        upload_real(meta, &d_naive_meta_);
+    } else if (cfg_.strategy == Strategy::DisagBitmask) {
+        std::vector<double> compact(std::size_t(arr_.boundary_voxel_count) * 3);
+        for (std::int64_t i = 0; i < arr_.boundary_voxel_count; ++i)
+            for (int d = 0; d < 3; ++d) compact[std::size_t(i) * 3 + d] = cfg_.u_bc[d];
+        upload_real(compact, &d_compact_meta_);
+        VOXL_CUDA(cudaMalloc(&d_meta_index_, arr_.voxel_meta_index.size() * sizeof(std::int32_t)));
+        VOXL_CUDA(cudaMemcpy(d_meta_index_, arr_.voxel_meta_index.data(),
+                             arr_.voxel_meta_index.size() * sizeof(std::int32_t), cudaMemcpyHostToDevice));
+        VOXL_CUDA(cudaMalloc(&d_bitmask_, nb));
+        VOXL_CUDA(cudaMemcpy(d_bitmask_, arr_.boundary_bitmask.data(), nb, cudaMemcpyHostToDevice));
+    }
+    VOXL_CUDA(cudaMalloc(&d_error_, sizeof(int)));
+    const int big = INT_MAX;
+    VOXL_CUDA(cudaMemcpy(d_error_, &big, sizeof(int), cudaMemcpyHostToDevice));
+    VOXL_CUDA(cudaMalloc(&d_diag_, (2 * kSpProbeBlocks + 4) * sizeof(double)));
+    const double u0[3] = {0.0, 0.0, 0.0};
+    set_equilibrium(1.0, u0);  // the reference's rest start (sparse.cpp:297-303)
+}
+
+SparseEngine::~SparseEngine() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (void* b : buf_) cudaFree(b);
+    cudaFree(d_nbr_);
+    cudaFree(d_masks_);
+    cudaFree(d_origins_);
+    cudaFree(d_bitmask_);
+    cudaFree(d_meta_index_);
+    cudaFree(d_compact_meta_);
+    cudaFree(d_naive_meta_);
+    cudaFree(d_slots_);
+    cudaFree(d_staging_);
+    cudaFree(d_error_);
+    cudaFree(d_diag_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void SparseEngine::set_equilibrium(double rho, const double u[3]) {
+    // Every slot of both buffers (inactive slots included, as the reference
+    // initialises whole blocks) at equilibrium(rho, u).
+    const LatticeTable t = make_lattice(cfg_.lattice);
+    double feq[27];
+    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    for (int i = 0; i < t.q; ++i) {
+        const double eu = double(t.e[i][0]) * u[0] + double(t.e[i][1]) * u[1] + double(t.e[i][2]) * u[2];
+        const double w = double(t.wnum[i]) / double(t.wden[i]);
+        feq[i] = w * rho * (1.0 + 3.0 * eu + 4.5 * eu * eu - 1.5 * uu);
+    }
+    const long long total = (long long)grid_.num_blocks() * q_ * grid_.block_volume();
+    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        auto A = Ops::base_args(cfg_);
+        for (int c = 0; c < q_; ++c) A.shift[c] = feq[c] - A.shift[c];
+        using R = std::remove_pointer_t<decltype(A.nxt)>;
+        for (void* b : buf_)
+            sparse_fill_kernel<Ops::Q, R><<<unsigned((total + 255) / 256), 256, 0, stream_>>>(
+                static_cast<R*>(b), total, grid_.block_volume(), A);
+        VOXL_CUDA(cudaGetLastError());
+    });
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void SparseEngine::ensure_slots() {
+    if (d_slots_) return;
+    const auto slots = canonical_slots(grid_);
+    VOXL_CUDA(cudaMalloc(&d_slots_, slots.size() * sizeof(std::int64_t)));
+    VOXL_CUDA(cudaMemcpy(d_slots_, slots.data(), slots.size() * sizeof(std::int64_t), cudaMemcpyHostToDevice));
+}
+
+void SparseEngine::set_state(const double* canonical) {
+    ensure_slots();
+    const long long n = grid_.num_active();
+    const std::size_t len = std::size_t(n) * q_;
+    if (staging_len_ < len) {
+        cudaFree(d_staging_);
+        VOXL_CUDA(cudaMalloc(&d_staging_, len * sizeof(double)));
+        staging_len_ = len;
+    }
+    VOXL_CUDA(cudaMemcpyAsync(d_staging_, canonical, len * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        auto A = Ops::base_args(cfg_);
+        using R = std::remove_pointer_t<decltype(A.nxt)>;
+        sparse_io_kernel<Ops::Q, R, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(
+            static_cast<R*>(buf_[cur_]), d_staging_, d_slots_, n, grid_.block_volume(), A);
+        VOXL_CUDA(cudaGetLastError());
+    });
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void SparseEngine::get_state(double* canonical) {
+    ensure_slots();
+    const long long n = grid_.num_active();
+    const std::size_t len = std::size_t(n) * q_;
+    if (staging_len_ < len) {
+        cudaFree(d_staging_);
+        VOXL_CUDA(cudaMalloc(&d_staging_, len * sizeof(double)));
+        staging_len_ = len;
+    }
+    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        auto A = Ops::base_args(cfg_);
+        using R = std::remove_pointer_t<decltype(A.nxt)>;
+        sparse_io_kernel<Ops::Q, R, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(
+            static_cast<R*>(buf_[cur_]), d_staging_, d_slots_, n, grid_.block_volume(), A);
+        VOXL_CUDA(cudaGetLastError());
+    });
+    VOXL_CUDA(cudaMemcpyAsync(canonical, d_staging_, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l) {
+    // sweep / step (sparse.cpp:359-394) as real kernels.
+    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        auto A = Ops::base_args(cfg_);
+        using R = std::remove_pointer_t<decltype(A.nxt)>;
+        A.cur = static_cast<const R*>(buf_[cur_]);
+        A.nxt = static_cast<R*>(buf_[cur_ ^ 1]);
+        A.nbr = d_nbr_;
+        A.masks = d_masks_;
+        A.origins = d_origins_;
+        A.step = steps_done_;
+        A.error_flag = d_error_;
+        A.meta_index = d_meta_index_;
+        A.compact_meta = static_cast<const R*>(d_compact_meta_);
+        A.naive_meta = static_cast<const R*>(d_naive_meta_);
+        const int nb = grid_.num_blocks();
+        const int edge = grid_.edge();
+        switch (cfg_.strategy) {
+            case Strategy::Naive:
+                A.vel_source = kVelInline;
+                A.block_begin = 0;
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], stream_));
+                Ops::launch(edge, A, kHeavy, nb, stream_);
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], stream_));
+                if (ev_l) {
+                    VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
+                    VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
+                }
+                break;
+            case Strategy::DisagBitmask:
+                A.vel_source = kVelIndirect;
+                A.block_begin = 0;
+                A.bitmask = d_bitmask_;
+                A.bitmask_want = 1;
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], stream_));
+                Ops::launch(edge, A, kHeavy, nb, stream_);
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], stream_));
+                A.bitmask_want = 0;
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
+                Ops::launch(edge, A, kLight, nb, stream_);
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
+                break;
+            case Strategy::DisagMem: {
+                A.vel_source = kVelConst;
+                const int n_b = int(classes_.n_boundary);
+                A.block_begin = 0;
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], stream_));
+                Ops::launch(edge, A, kHeavy, n_b, stream_);
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], stream_));
+                A.block_begin = n_b;
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
+                Ops::launch(edge, A, kLight, nb - n_b, stream_);
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
+                break;
+            }
+        }
+    });
+    cur_ ^= 1;
+    ++steps_done_;
+}
+
+void SparseEngine::check_errors() {
+    int flag = INT_MAX;
+    VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    if (flag != INT_MAX)
+        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": non-positive density");
+}
+
+void SparseEngine::step(int n) {
+    for (int i = 0; i < n; ++i) launch(0, nullptr, nullptr);
+    check_errors();
+}
+
+double SparseEngine::timed_steps(int n, double* boundary_ms, double* light_ms) {
+    std::vector<cudaEvent_t> ev(4 * std::size_t(n) + 2);
+    for (auto& e : ev) VOXL_CUDA(cudaEventCreate(&e));
+    VOXL_CUDA(cudaEventRecord(ev[4 * n], stream_));
+    for (int i = 0; i < n; ++i) launch(0, &ev[4 * i], &ev[4 * i + 2]);
+    VOXL_CUDA(cudaEventRecord(ev[4 * n + 1], stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    double sb = 0, sl = 0;
+    for (int i = 0; i < n; ++i) {
+        float a = 0, b = 0;
+        VOXL_CUDA(cudaEventElapsedTime(&a, ev[4 * i], ev[4 * i + 1]));
+        VOXL_CUDA(cudaEventElapsedTime(&b, ev[4 * i + 2], ev[4 * i + 3]));
+        sb += a;
+        sl += b;
+    }
+    float total = 0;
+    VOXL_CUDA(cudaEventElapsedTime(&total, ev[4 * n], ev[4 * n + 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (boundary_ms) *boundary_ms = sb;
+    if (light_ms) *light_ms = sl;
+    check_errors();
+    return total;
+}
+
+DenseDiag SparseEngine::probe() {
+    ensure_slots();
+    const long long n = grid_.num_active();
+    unsigned long long none = ~0ull;
+    auto* bad = reinterpret_cast<unsigned long long*>(d_diag_ + 2 * kSpProbeBlocks + 2);
+    VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
+    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        using L = std::conditional_t<Ops::Q == 19, D3Q19, D3Q27>;
+        auto A = Ops::base_args(cfg_);
+        using R = std::remove_pointer_t<decltype(A.nxt)>;
+        sparse_probe_kernel<L, R><<<kSpProbeBlocks, 256, 0, stream_>>>(static_cast<const R*>(buf_[cur_]), d_slots_,
+                                                                       n, grid_.block_volume(), A, d_diag_, bad);
+        sparse_probe_final<<<1, 32, 0, stream_>>>(d_diag_, kSpProbeBlocks, d_diag_ + 2 * kSpProbeBlocks);
+        VOXL_CUDA(cudaGetLastError());
+    });
+    double res[2];
+    unsigned long long b = 0;
+    VOXL_CUDA(cudaMemcpyAsync(res, d_diag_ + 2 * kSpProbeBlocks, sizeof res, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(&b, bad, sizeof b, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    DenseDiag d;
+    d.mass = res[0];
+    d.max_speed = res[1];
+    if (b != ~0ull) {
+        d.unstable = 1;
+        d.bad_voxel = std::int64_t(b >> 5);
+        d.bad_population = int(b & 31);
+    }
+    return d;
+}
+
+} // namespace voxl_b200

@@ -1,0 +1,95 @@
+// sparse.cuh -- block-sparse wind-tunnel LBM engine on B200.
+//
+// Drop-in for sparse::SparseLbmEngine (proj/include/voxl/sparse.hpp:175-213,
+// proj/src/sparse.cpp:253-453): the same three dispatch strategies (Table 2),
+// with real kernels behind them:
+//   Naive        one "combined" kernel over every block; the regularized path
+//                is compiled in for all voxels (3Q register footprint) and the
+//                boundary velocity comes from an inline per-slot table.
+//   DisagBitmask two kernels over every block, each skipping the other class
+//                by the per-block bitmask; boundary velocity through the
+//                indirect voxel_meta_index into a compact buffer.
+//   DisagMem     boundary blocks stored first: a heavy kernel over [0, n_b)
+//                and a light bounce-back + BGK kernel (2Q) over [n_b, n);
+//                boundary velocity derived from geometry, zero extra storage.
+// Storage is the reference's BlockField: SoA within each block,
+// data[((b*Q)+c)*E^3 + local], local = (lz*E + ly)*E + lx.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "sparse_grid.hpp"
+
+namespace voxl_b200 {
+
+struct SparseConfig {
+    int lattice = 1;
+    std::array<int, 3> domain{32, 32, 32};
+    double tau = 0.7;
+    std::array<double, 3> u_bc{0.04, 0.0, 0.0};
+    int edge = 8;
+    Strategy strategy = Strategy::DisagMem;
+    Precision precision = Precision::F32;
+};
+
+class SparseEngine {
+public:
+    SparseEngine(const SparseConfig& cfg, const std::uint8_t* active);
+    ~SparseEngine();
+    SparseEngine(const SparseEngine&) = delete;
+    SparseEngine& operator=(const SparseEngine&) = delete;
+
+    const SparseConfig& config() const { return cfg_; }
+    const BlockGrid& grid() const { return T_.grid; }
+    const ClassifyResult& classes() const { return T_.classes; }
+    const Arrangement& arrangement() const { return T_.arr; }
+    const DispatchPlan& plan() const { return T_.plan; }
+    SparseTables& tables() { return T_; }
+    int q() const { return q_; }
+
+    void set_equilibrium(double rho, const double u[3]);
+    /// Canonical state: active voxels sorted by pack_coord (x slowest, z
+    /// fastest), q populations each (sparse.cpp:416-453).
+    void set_state(const double* canonical);
+    void get_state(double* canonical);
+    void step(int n);
+    /// n steps timed with CUDA events per launch: returns total ms, and the
+    /// summed boundary-kernel and non-boundary-kernel ms.
+    double timed_steps(int n, double* boundary_ms, double* light_ms);
+    DenseDiag probe();
+    void check_errors();
+
+private:
+    SparseConfig cfg_;
+    int q_ = 19;
+    SparseTables T_;
+    BlockGrid& grid_ = T_.grid;
+    ClassifyResult& classes_ = T_.classes;
+    Arrangement& arr_ = T_.arr;
+    int esize_ = 4;
+    void* buf_[2] = {nullptr, nullptr};
+    int cur_ = 0;
+    int steps_done_ = 0;
+    std::int32_t* d_nbr_ = nullptr;
+    std::uint64_t* d_masks_ = nullptr;
+    int* d_origins_ = nullptr;
+    std::uint8_t* d_bitmask_ = nullptr;
+    std::int32_t* d_meta_index_ = nullptr;
+    void* d_compact_meta_ = nullptr;
+    void* d_naive_meta_ = nullptr;
+    std::int64_t* d_slots_ = nullptr;
+    double* d_staging_ = nullptr;
+    std::size_t staging_len_ = 0;
+    int* d_error_ = nullptr;
+    double* d_diag_ = nullptr;
+    cudaStream_t stream_ = nullptr;
+
+    void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l);
+    void ensure_slots();
+};
+
+} // namespace voxl_b200

@@ -1,0 +1,166 @@
+"""Block-sparse path: host tables bit-exact vs the reference (CPU) and the CUDA
+engine's physics vs the oracle (GPU; fp64 bitwise, fp32 within 1e-5)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2503_07898_b200 as V
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+
+
+def test_obstacle_mask_matches_oracle():
+    for dom in [(32, 32, 32), (24, 20, 16), (17, 19, 23)]:
+        assert np.array_equal(V.obstacle_mask(dom), O.obstacle_mask(dom))
+
+
+@needs_ref
+@pytest.mark.parametrize("strategy", ["naive", "disag_bitmask", "disag_mem"])
+@pytest.mark.parametrize("domain", [(32, 32, 32), (24, 20, 16), (19, 13, 22)])
+def test_tables_bit_exact_vs_reference_edge4(strategy, domain):
+    cfg = dict(lattice="D3Q19", domain=list(domain), tau=0.7, scenario="flow_over_obstacle",
+               velocity=[0.04, 0, 0], steps=0, strategy=strategy)
+    ref = O.RefSparse(cfg, 4)
+    ours = V.SparsePlan(domain, block_edge=4, strategy=strategy)
+    ro, rm, rc = ref.blocks()
+    oo, om, oc = ours.blocks()
+    assert np.array_equal(ro, oo)
+    assert np.array_equal(rm, om[:, 0])
+    assert np.array_equal(rc.astype(np.uint8), oc)
+    rp, rb, rmi, rcnt = ref.arrangement()
+    op, ob, omi, ocnt = ours.arrangement()
+    assert np.array_equal(rp, op)
+    assert rcnt == ocnt
+    if strategy == "disag_bitmask":
+        assert np.array_equal(rb, ob)
+        assert np.array_equal(rmi, omi)
+    assert ref.report_json() == ours.report_json()
+    assert ref.num_active == ours.info()["num_active"]
+
+
+@needs_ref
+@pytest.mark.parametrize("edge", [1, 2])
+def test_small_edges_match_reference(edge):
+    cfg = dict(lattice="D3Q19", domain=[12, 10, 9], tau=0.7, scenario="flow_over_obstacle", velocity=[0.04, 0, 0],
+               steps=0, strategy="disag_mem")
+    ref = O.RefSparse(cfg, edge)
+    ours = V.SparsePlan((12, 10, 9), block_edge=edge, strategy="disag_mem")
+    ro, rm, rc = ref.blocks()
+    oo, om, oc = ours.blocks()
+    assert np.array_equal(ro, oo) and np.array_equal(rm, om[:, 0]) and np.array_equal(rc.astype(np.uint8), oc)
+
+
+@pytest.mark.parametrize("strategy", ["naive", "disag_bitmask", "disag_mem"])
+def test_edge8_tables_properties(strategy):
+    dom = (40, 36, 28)
+    act = V.obstacle_mask(dom)
+    p = V.SparsePlan(dom, act, block_edge=8, strategy=strategy)
+    info = p.info()
+    assert info["num_active"] == int(act.sum())
+    o, m, c = p.blocks()
+    # masks cover exactly the active set
+    a3 = act.reshape(dom[2], dom[1], dom[0])
+    cover = np.zeros_like(a3)
+    for (ox, oy, oz), words in zip(o, m):
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little").reshape(8, 8, 8)
+        sub = cover[oz:oz + 8, oy:oy + 8, ox:ox + 8]
+        sub |= bits[: sub.shape[0], : sub.shape[1], : sub.shape[2]]
+    assert np.array_equal(cover, a3)
+    # classification: boundary iff an active voxel on x == 0 or x == nx-1
+    for (ox, oy, oz), cls in zip(o, c):
+        face = a3[oz:oz + 8, oy:oy + 8, ox:ox + 8]
+        xs = np.arange(ox, ox + face.shape[2])
+        expect = bool(face[:, :, (xs == 0) | (xs == dom[0] - 1)].any())
+        assert bool(cls) == expect
+    if strategy == "disag_mem":
+        assert np.all(np.diff(c.astype(int)) <= 0)  # boundary blocks form a prefix
+    nbr = p.neighbours()
+    assert np.array_equal(nbr[:, 13], np.arange(len(o)))
+    rep = json.loads(p.report_json())
+    assert rep["strategy"] == strategy
+
+
+def test_dispatch_plan_table2():
+    """Table 2 rows (SPEC sparse examples; sparse.cpp:199-225)."""
+    j = json.loads(V.dispatch_plan_json("naive", 10, 20, q=27, block_size=64, s_w=24, s_i=4))
+    assert j["kernels"] == [{"name": "combined", "blocks": 30, "cost": 81}]
+    assert j["extra_storage_bytes"] == 24 * 20 * 64 and j["indexing"] == "direct"
+    j = json.loads(V.dispatch_plan_json("naive", 10, 20, q=27, naive_full_domain_storage=True))
+    assert j["extra_storage_bytes"] == 24 * 30 * 64
+    j = json.loads(V.dispatch_plan_json("disag_mem", 32, 32, q=19))
+    assert [k["blocks"] for k in j["kernels"]] == [32, 32] and j["extra_storage_bytes"] == 0
+    assert [k["cost"] for k in j["kernels"]] == [57, 38]
+    j = json.loads(V.dispatch_plan_json("disag_bitmask", 32, 32, q=19, block_size=64, s_i=4))
+    assert j["extra_storage_bytes"] == 16384 and j["indexing"] == "indirect"
+    assert [k["blocks"] for k in j["kernels"]] == [64, 64]
+
+
+# ---- GPU physics -----------------------------------------------------------------------
+
+def _oracle(dom, steps, tau=0.7):
+    act = O.obstacle_mask(dom)
+    st = O.port_sparse_run("D3Q19", dom, tau, (0.04, 0, 0), steps, act)
+    return O.sparse_canonical(dom, act, st, 19)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["naive", "disag_bitmask", "disag_mem"])
+@pytest.mark.parametrize("edge", [4, 8])
+@pytest.mark.parametrize("dom", [(32, 32, 32), (24, 20, 16)])
+def test_fp64_bitwise_vs_oracle(strategy, edge, dom):
+    ref = _oracle(dom, 20)
+    e = V.SparseEngine(dom, block_edge=edge, strategy=strategy, precision="fp64")
+    e.step(20)
+    out = e.get_state()
+    assert np.array_equal(out, ref), np.abs(out - ref).max()
+
+
+@pytest.mark.gpu
+def test_fp64_bitwise_golden():
+    z = np.load(os.path.join(GOLDEN, "sparse_obstacle_d3q19_16.npz"))
+    cfg = json.loads(str(z["config"]))
+    e = V.SparseEngine(tuple(cfg["domain"]), block_edge=8, strategy="disag_mem", precision="fp64")
+    e.step(cfg["steps"])
+    assert np.array_equal(e.get_state(), z["field"])
+
+
+@pytest.mark.gpu
+def test_set_state_roundtrip_and_continue():
+    dom = (24, 20, 16)
+    ref10 = _oracle(dom, 10)
+    e = V.SparseEngine(dom, block_edge=8, strategy="disag_mem", precision="fp64")
+    e.set_state(ref10)
+    assert np.array_equal(e.get_state(), ref10)
+    e.step(10)
+    assert np.array_equal(e.get_state(), _oracle(dom, 20))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["naive", "disag_mem"])
+def test_fp32_tolerance(strategy):
+    dom = (64, 48, 48)
+    kw = dict(block_edge=8, strategy=strategy)
+    e64 = V.SparseEngine(dom, precision="fp64", **kw)
+    e32 = V.SparseEngine(dom, precision="fp32", **kw)
+    e64.step(300)
+    e32.step(300)
+    a, b = e64.get_state(), e32.get_state()
+    rel = np.abs(a - b) / np.abs(a)
+    print("sparse fp32 max rel err after 300 steps:", rel.max())
+    assert rel.max() <= 1e-5
+
+
+@pytest.mark.gpu
+def test_probe_matches_oracle():
+    dom = (32, 32, 32)
+    ref = _oracle(dom, 15)
+    m_ref, s_ref = O.port_probe("D3Q19", ref)
+    e = V.SparseEngine(dom, block_edge=8, precision="fp64")
+    e.step(15)
+    d = e.probe()
+    assert d.unstable == 0
+    assert abs(d.mass - m_ref) <= 1e-12 * m_ref and abs(d.max_speed - s_ref) <= 1e-14

@@ -1,0 +1,81 @@
+#!/usr/bin/env python
+"""Throughput of the secondary hot paths (BASELINE configs[3], configs[4]).
+
+    python tools/bench_paths.py sparse [--n 256] [--steps 50]
+    python tools/bench_paths.py multires [--n 512] [--steps 5]
+
+Prints one JSON line per variant: MLUPS (active voxels for sparse; LUP =
+sum_l N_l * 2^(L-1-l) per coarse step for multires) and the fraction of the
+HBM roofline at 152 B/LUP (fp32 D3Q19), per kernel where the engine exposes
+per-kernel event times.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+BYTES = 152
+
+
+def peak():
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        return float(json.load(f)["hbm_gbs"])
+
+
+def sparse(args):
+    import paper_2503_07898_b200 as V
+
+    n = args.n
+    dom = (n, n, n)
+    act = V.obstacle_mask(dom)
+    for strategy in ("naive", "disag_bitmask", "disag_mem"):
+        e = V.SparseEngine(dom, act, block_edge=8, strategy=strategy, precision="fp32")
+        info = e.info()
+        e.timed_steps(args.warmup)
+        total, b_ms, l_ms = e.timed_steps(args.steps)
+        na = info["num_active"]
+        mlups = na * args.steps / (total / 1e3) / 1e6
+        gbs = BYTES * na * args.steps / (total / 1e3) / 1e9
+        line = {"path": "block_sparse", "strategy": strategy, "domain": list(dom), "block_edge": 8,
+                "active_voxels": na, "blocks": info["num_blocks"], "n_boundary": info["n_boundary"],
+                "steps": args.steps, "ms_per_step": round(total / args.steps, 4), "MLUPS": round(mlups, 1),
+                "achieved_GBs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak(), 4),
+                "frac_of_8TBs": round(gbs / 8000, 4),
+                "boundary_kernel_ms": round(b_ms / args.steps, 4), "light_kernel_ms": round(l_ms / args.steps, 4),
+                "report": json.loads(e.report_json())}
+        print(json.dumps(line), flush=True)
+        e.close()
+
+
+def multires(args):
+    import paper_2503_07898_b200 as V
+
+    n = args.n
+    for fused in (False, True):
+        e = V.MultiResEngine((n, n, n), levels=3, fused=fused, precision="fp32")
+        lup = e.lup_per_coarse_step()
+        e.timed_steps(args.warmup)
+        total, detail = e.timed_steps(args.steps)
+        mlups = lup * args.steps / (total / 1e3) / 1e6
+        gbs = BYTES * lup * args.steps / (total / 1e3) / 1e9
+        line = {"path": "multires", "levels": 3, "fused": fused, "domain": [n] * 3, "lup_per_coarse_step": lup,
+                "steps": args.steps, "ms_per_coarse_step": round(total / args.steps, 4), "MLUPS": round(mlups, 1),
+                "achieved_GBs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak(), 4),
+                "frac_of_8TBs": round(gbs / 8000, 4), "kernels_ms": detail, "distribution": e.distribution()}
+        print(json.dumps(line), flush=True)
+        e.close()
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("path", choices=["sparse", "multires"])
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    a = ap.parse_args()
+    sparse(a) if a.path == "sparse" else multires(a)

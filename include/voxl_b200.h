@@ -205,6 +205,63 @@ int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out);
 int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int block_size, int s_w, int s_i,
                             int naive_full_domain_storage, char* out, int64_t cap, int64_t* len);
 
+/* ---- multi-resolution engine (mres::MultiResLbm, multires.hpp:138-190) ---------- */
+
+typedef struct voxl_mres voxl_mres;
+typedef struct voxl_mres_plan voxl_mres_plan;
+
+typedef struct {
+    int lattice;          /* VOXL_D3Q19 | VOXL_D3Q27 (device); plans also take VOXL_D2Q9 */
+    int nx, ny, nz;       /* virtual finest domain */
+    int levels;           /* 1..4 */
+    double tau;           /* coarsest level; tau_l = 2 tau_{l+1} - 1/2 */
+    double lid_u[3];      /* lid velocity (cavity, lid on the max-z face) */
+    int fused;            /* FusedCollideStream on uniform blocks (multires.cpp:541) */
+    int precision;        /* VOXL_F32 | VOXL_F64 */
+    int block_edge;       /* 8 (production) or 4 (reference granularity) */
+    int reference_tables; /* also build the edge-4 ghost / pull / fusion tables */
+} voxl_mres_desc;
+
+/** Band level map of run_multires (solver.cpp:319-335), x fastest int32. */
+int voxl_band_level_map(int nx, int ny, int nz, int levels, int axis, int32_t* out);
+/** MultiResGrid::build + MultiResLbm (multires.cpp:54, :367), rest equilibrium. */
+int voxl_mres_create(const voxl_mres_desc* desc, const int32_t* level_map, voxl_mres** out);
+int voxl_mres_destroy(voxl_mres* h);
+/** n x coarse_step (multires.cpp:576). */
+int voxl_mres_step(voxl_mres* h, int n);
+/** n coarse steps timed with CUDA events: out[5] = total, collide, stream, fused, transition ms. */
+int voxl_mres_timed_steps(voxl_mres* h, int n, double* out5);
+int voxl_mres_state_len(voxl_mres* h, int64_t* len);
+/** canonical_state / set_state (multires.cpp:578-598, :396-410): levels finest
+ *  first, cells sorted by pack_coord, q populations each. */
+int voxl_mres_get_state(voxl_mres* h, double* canonical);
+int voxl_mres_set_state(voxl_mres* h, const double* canonical);
+int voxl_mres_set_equilibrium(voxl_mres* h, double rho, const double* u);
+/** probe_field over canonical_state (solver.cpp:345). */
+int voxl_mres_probe(voxl_mres* h, voxl_diag* out);
+/** total_mass (multires.cpp:600-609): per-level sums weighted by 8^l. */
+int voxl_mres_total_mass(voxl_mres* h, double* mass);
+/** what: 0 = execution graph DOT, 1 = distribution report. */
+int voxl_mres_text(voxl_mres* h, int what, char* out, int64_t cap, int64_t* len);
+/** Per level: active cells, tau, ghost cells, ring cells, uniform / jump blocks (device grid). */
+int voxl_mres_level_info(voxl_mres* h, int level, int64_t* num_active, double* tau, int64_t* uniform_blocks,
+                         int64_t* jump_blocks);
+int voxl_mres_lup_per_coarse_step(voxl_mres* h, int64_t* lup);
+/** Host tables only (no device): MultiResGrid::build with reference tables. */
+int voxl_mres_plan_create(const voxl_mres_desc* desc, const int32_t* level_map, voxl_mres_plan** out);
+int voxl_mres_plan_destroy(voxl_mres_plan* p);
+int voxl_mres_plan_level(voxl_mres_plan* p, int level, int64_t* num_active, double* tau, int* ref_blocks,
+                         int* n_ghosts, int* n_pulls);
+/** Edge-4 blocks of a level: origins, 64-bit masks, fusion class (1 = Jump). */
+int voxl_mres_plan_ref_blocks(voxl_mres_plan* p, int level, int* origins, uint64_t* masks, uint8_t* jump);
+/** Ghost list: 6 ints each (cell xyz, parent xyz); pulls: 7 ints each (voxel xyz, direction, refined xyz). */
+int voxl_mres_plan_ghosts(voxl_mres_plan* p, int level, int* out);
+int voxl_mres_plan_pulls(voxl_mres_plan* p, int level, int* out);
+/** jump_distance (multires.cpp:214-223); INT_MAX = no interface. */
+int voxl_mres_plan_jump_distance(voxl_mres_plan* p, int level, int x, int y, int z, int* out);
+/** what: 0 = DOT (fused graph), 1 = DOT (staged graph), 2 = distribution report. */
+int voxl_mres_plan_text(voxl_mres_plan* p, int what, char* out, int64_t cap, int64_t* len);
+
 /* ---- CUDA IPC helpers (64-byte cudaIpcMemHandle_t as bytes) ------------------- */
 int voxl_ipc_export(void* dev_ptr, char* handle64);
 int voxl_ipc_open(const char* handle64, void** dev_ptr);

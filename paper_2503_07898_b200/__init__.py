@@ -10,6 +10,7 @@ from ._capi import (LIB_PATH, VoxlCudaError, VoxlDomainError, VoxlError, VoxlIns
 from .dense import (DenseEngine, classify_voxels, decompose, lattice_json, layout_addresses,  # noqa: F401
                     layout_json, make_desc, plan_ledger)
 from .sparse import SparseEngine, SparsePlan, dispatch_plan_json, obstacle_mask  # noqa: F401
+from .multires import MultiResEngine, MultiResPlan, band_level_map  # noqa: F401
 
 __all__ = ["DenseEngine", "classify_voxels", "decompose", "lattice_json", "layout_addresses", "layout_json", "make_desc", "plan_ledger",
            "VoxlError", "VoxlInstability", "VoxlInvalidArgument", "VoxlOutOfRange", "VoxlCudaError",

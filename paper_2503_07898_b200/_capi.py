@@ -67,8 +67,8 @@ class SparseDesc(C.Structure):
 
 class MresDesc(C.Structure):
     _fields_ = [("lattice", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("levels", C.c_int),
-                ("tau", C.c_double), ("velocity", C.c_double * 3), ("fused", C.c_int), ("precision", C.c_int),
-                ("block_edge", C.c_int)]
+                ("tau", C.c_double), ("lid_u", C.c_double * 3), ("fused", C.c_int), ("precision", C.c_int),
+                ("block_edge", C.c_int), ("reference_tables", C.c_int)]
 
 
 def _load():
@@ -135,6 +135,30 @@ def _load():
         "voxl_sparse_probe": ([vp, C.POINTER(Diag)], C.c_int),
         "voxl_dispatch_plan_json": ([C.c_int, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, cp, i64,
                                      C.POINTER(i64)], C.c_int),
+        "voxl_band_level_map": ([C.c_int] * 5 + [vp], C.c_int),
+        "voxl_mres_create": ([C.POINTER(MresDesc), vp, C.POINTER(vp)], C.c_int),
+        "voxl_mres_destroy": ([vp], C.c_int),
+        "voxl_mres_step": ([vp, C.c_int], C.c_int),
+        "voxl_mres_timed_steps": ([vp, C.c_int, vp], C.c_int),
+        "voxl_mres_state_len": ([vp, C.POINTER(i64)], C.c_int),
+        "voxl_mres_get_state": ([vp, vp], C.c_int),
+        "voxl_mres_set_state": ([vp, vp], C.c_int),
+        "voxl_mres_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
+        "voxl_mres_probe": ([vp, C.POINTER(Diag)], C.c_int),
+        "voxl_mres_total_mass": ([vp, C.POINTER(C.c_double)], C.c_int),
+        "voxl_mres_text": ([vp, C.c_int, cp, i64, C.POINTER(i64)], C.c_int),
+        "voxl_mres_level_info": ([vp, C.c_int, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(i64),
+                                  C.POINTER(i64)], C.c_int),
+        "voxl_mres_lup_per_coarse_step": ([vp, C.POINTER(i64)], C.c_int),
+        "voxl_mres_plan_create": ([C.POINTER(MresDesc), vp, C.POINTER(vp)], C.c_int),
+        "voxl_mres_plan_destroy": ([vp], C.c_int),
+        "voxl_mres_plan_level": ([vp, C.c_int, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+        "voxl_mres_plan_ref_blocks": ([vp, C.c_int, vp, vp, vp], C.c_int),
+        "voxl_mres_plan_ghosts": ([vp, C.c_int, vp], C.c_int),
+        "voxl_mres_plan_pulls": ([vp, C.c_int, vp], C.c_int),
+        "voxl_mres_plan_jump_distance": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)], C.c_int),
+        "voxl_mres_plan_text": ([vp, C.c_int, cp, i64, C.POINTER(i64)], C.c_int),
         "voxl_ipc_export": ([vp, vp], C.c_int),
         "voxl_ipc_open": ([vp, C.POINTER(vp)], C.c_int),
         "voxl_ipc_close": ([vp], C.c_int),

@@ -26,7 +26,7 @@ FLAGS = ARCH + [
     "-I" + os.path.join(PKG, "..", "include"),
 ]
 
-SOURCES = ["grid.cpp", "sparse_grid.cpp", "dense.cu", "sparse.cu", "multires.cu", "capi.cu"]
+SOURCES = ["grid.cpp", "sparse_grid.cpp", "multires_grid.cpp", "dense.cu", "sparse.cu", "multires.cu", "capi.cu"]
 
 
 def _compile(src: str, verbose: bool) -> str:

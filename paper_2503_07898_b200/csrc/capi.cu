@@ -9,6 +9,7 @@
 #include "dense.cuh"
 #include "grid.hpp"
 #include "lattice.cuh"
+#include "multires.cuh"
 #include "sparse.cuh"
 
 using namespace voxl_b200;
@@ -480,6 +481,194 @@ int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int 
         require(strategy >= 0 && strategy <= 2, "unknown sparse strategy");
         put_text(dispatch_plan(Strategy(strategy), n_b, n_nb, q, bs, s_w, s_i, full != 0).to_json(false), out, cap,
                  len);
+    });
+}
+
+int voxl_band_level_map(int nx, int ny, int nz, int levels, int axis, int32_t* out) {
+    return guarded([&] {
+        // solver.cpp:319-335
+        const int n[3] = {nx, ny, nz};
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    const int v[3] = {x, y, z};
+                    const int k = v[axis];
+                    int level = levels - 1;
+                    for (int l = 0; l < levels - 1; ++l)
+                        if (k >= (n[axis] >> (l + 1))) {
+                            level = l;
+                            break;
+                        }
+                    out[(int64_t(z) * ny + y) * nx + x] = level;
+                }
+    });
+}
+
+static MresConfig mres_config(const voxl_mres_desc* d) {
+    require(d != nullptr, "null descriptor");
+    MresConfig c;
+    c.lattice = d->lattice;
+    c.domain = {d->nx, d->ny, d->nz};
+    c.levels = d->levels;
+    c.tau = d->tau;
+    c.lid_u = {d->lid_u[0], d->lid_u[1], d->lid_u[2]};
+    c.fused = d->fused != 0;
+    require(d->precision == VOXL_F32 || d->precision == VOXL_F64, "unknown precision");
+    c.precision = Precision(d->precision);
+    c.edge = d->block_edge;
+    c.reference_tables = d->reference_tables != 0;
+    return c;
+}
+
+static MultiResEngine* MR(voxl_mres* h) { return reinterpret_cast<MultiResEngine*>(h); }
+static MresGrid* MP(voxl_mres_plan* p) { return reinterpret_cast<MresGrid*>(p); }
+
+int voxl_mres_create(const voxl_mres_desc* d, const int32_t* map, voxl_mres** out) {
+    return guarded([&] {
+        require(map && out, "voxl_mres_create: null argument");
+        *out = reinterpret_cast<voxl_mres*>(new MultiResEngine(mres_config(d), map));
+    });
+}
+
+int voxl_mres_destroy(voxl_mres* h) {
+    return guarded([&] { delete MR(h); });
+}
+
+int voxl_mres_step(voxl_mres* h, int n) {
+    return guarded([&] { MR(h)->coarse_step(n); });
+}
+
+int voxl_mres_timed_steps(voxl_mres* h, int n, double* o) {
+    return guarded([&] {
+        const MresTimes t = MR(h)->timed_steps(n);
+        o[0] = t.total;
+        o[1] = t.collide;
+        o[2] = t.stream;
+        o[3] = t.fused;
+        o[4] = t.transition;
+    });
+}
+
+int voxl_mres_state_len(voxl_mres* h, int64_t* len) {
+    return guarded([&] { *len = MR(h)->state_len(); });
+}
+
+int voxl_mres_get_state(voxl_mres* h, double* c) {
+    return guarded([&] { MR(h)->get_state(c); });
+}
+
+int voxl_mres_set_state(voxl_mres* h, const double* c) {
+    return guarded([&] { MR(h)->set_state(c); });
+}
+
+int voxl_mres_set_equilibrium(voxl_mres* h, double rho, const double* u) {
+    return guarded([&] { MR(h)->set_equilibrium(rho, u); });
+}
+
+int voxl_mres_probe(voxl_mres* h, voxl_diag* out) {
+    return guarded([&] {
+        const DenseDiag d = MR(h)->probe();
+        out->mass = d.mass;
+        out->max_speed = d.max_speed;
+        out->unstable = d.unstable;
+        out->bad_population = d.bad_population;
+        out->bad_voxel = d.bad_voxel;
+    });
+}
+
+int voxl_mres_total_mass(voxl_mres* h, double* m) {
+    return guarded([&] { *m = MR(h)->total_mass(); });
+}
+
+int voxl_mres_text(voxl_mres* h, int what, char* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        put_text(what == 0 ? MR(h)->graph_dot() : MR(h)->grid().distribution_report(), out, cap, len);
+    });
+}
+
+int voxl_mres_level_info(voxl_mres* h, int l, int64_t* na, double* tau, int64_t* uni, int64_t* jmp) {
+    return guarded([&] {
+        require(l >= 0 && l < MR(h)->grid().num_levels(), "bad level");
+        if (na) *na = MR(h)->grid().level(l).num_active;
+        if (tau) *tau = MR(h)->grid().level(l).tau;
+        const auto c = MR(h)->fusion_counts(l);
+        if (uni) *uni = c[0];
+        if (jmp) *jmp = c[1];
+    });
+}
+
+int voxl_mres_lup_per_coarse_step(voxl_mres* h, int64_t* lup) {
+    return guarded([&] { *lup = MR(h)->grid().lup_per_coarse_step(); });
+}
+
+int voxl_mres_plan_create(const voxl_mres_desc* d, const int32_t* map, voxl_mres_plan** out) {
+    return guarded([&] {
+        require(d && map && out, "voxl_mres_plan_create: null argument");
+        require(d->lattice >= 0 && d->lattice <= 2, "unknown lattice kind");
+        *out = reinterpret_cast<voxl_mres_plan*>(
+            new MresGrid(MresGrid::build({d->nx, d->ny, d->nz}, d->levels, d->lattice, map, d->tau, true)));
+    });
+}
+
+int voxl_mres_plan_destroy(voxl_mres_plan* p) {
+    return guarded([&] { delete MP(p); });
+}
+
+int voxl_mres_plan_level(voxl_mres_plan* p, int l, int64_t* na, double* tau, int* nb, int* ng, int* np) {
+    return guarded([&] {
+        require(l >= 0 && l < MP(p)->num_levels(), "bad level");
+        const MresLevel& L = MP(p)->level(l);
+        if (na) *na = L.num_active;
+        if (tau) *tau = L.tau;
+        if (nb) *nb = L.ref_blocks.num_blocks();
+        if (ng) *ng = int(L.ghosts.size());
+        if (np) *np = int(L.pulls.size());
+    });
+}
+
+int voxl_mres_plan_ref_blocks(voxl_mres_plan* p, int l, int* origins, uint64_t* masks, uint8_t* jump) {
+    return guarded([&] {
+        const MresLevel& L = MP(p)->level(l);
+        for (int b = 0; b < L.ref_blocks.num_blocks(); ++b) {
+            if (origins)
+                for (int a = 0; a < 3; ++a) origins[3 * b + a] = L.ref_blocks.blocks()[b].origin[a];
+            if (masks) masks[b] = L.ref_blocks.mask(b, 0);
+            if (jump) jump[b] = L.fusion_jump[b];
+        }
+    });
+}
+
+int voxl_mres_plan_ghosts(voxl_mres_plan* p, int l, int* out) {
+    return guarded([&] {
+        const auto& g = MP(p)->level(l).ghosts;
+        for (std::size_t i = 0; i < g.size(); ++i)
+            for (int a = 0; a < 3; ++a) {
+                out[6 * i + a] = g[i].cell[a];
+                out[6 * i + 3 + a] = g[i].parent[a];
+            }
+    });
+}
+
+int voxl_mres_plan_pulls(voxl_mres_plan* p, int l, int* out) {
+    return guarded([&] {
+        const auto& g = MP(p)->level(l).pulls;
+        for (std::size_t i = 0; i < g.size(); ++i) {
+            for (int a = 0; a < 3; ++a) {
+                out[7 * i + a] = g[i].voxel[a];
+                out[7 * i + 4 + a] = g[i].refined[a];
+            }
+            out[7 * i + 3] = g[i].direction;
+        }
+    });
+}
+
+int voxl_mres_plan_jump_distance(voxl_mres_plan* p, int l, int x, int y, int z, int* out) {
+    return guarded([&] { *out = MP(p)->jump_distance(l, x, y, z); });
+}
+
+int voxl_mres_plan_text(voxl_mres_plan* p, int what, char* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        put_text(what == 2 ? MP(p)->distribution_report() : MP(p)->graph_dot(what == 0), out, cap, len);
     });
 }
 

@@ -1,0 +1,906 @@
+// multires.cu -- multi-resolution kernels and engine (see multires.cuh).
+#include "multires.cuh"
+#include "lattice.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+namespace voxl_b200 {
+
+namespace {
+
+enum BlockClass : std::uint8_t { kNone = 0, kUniform = 1, kJump = 2 };
+enum TimeClass : int { kTCollide = 0, kTStream = 1, kTFused = 2, kTTransition = 3 };
+
+template <int Q, class R>
+struct MresArgs {
+    const R* cur;
+    R* nxt;
+    R* post;
+    const std::int32_t* nbr;
+    const std::uint64_t* amask;
+    const std::uint8_t* cls;
+    const int* org;
+    const int* blocks;
+    int n[3];
+    R omega, keep;
+    R lid[Q];  // 2 w_j rho0 3 (e_j . u_lid) per pulled direction j (multires.cpp:499-503)
+    int has_lid;
+    int step;
+    int* error_flag;
+};
+
+template <int E>
+struct BlockGeom {
+    static constexpr int BV = E * E * E;
+    static constexpr int W = BV >= 64 ? BV / 64 : 1;
+    static constexpr int LOG = E == 8 ? 3 : (E == 4 ? 2 : (E == 2 ? 1 : 0));
+    static constexpr int H = (1 << (LOG - 1)) | (1 << (2 * LOG - 1)) | (1 << (3 * LOG - 1));
+    static constexpr int LM = (BV - 1) & ~H;
+};
+
+/// Neighbour-block index d (0..26) and source local index for the cell at
+/// local t shifted by (sx, sy, sz) in {-1, 0, 1}^3 (compile time).
+template <int E, int SX, int SY, int SZ>
+__device__ __forceinline__ void shifted(int t, bool xlo, bool xhi, bool ylo, bool yhi, bool zlo, bool zhi, int& d,
+                                        int& sl) {
+    using G = BlockGeom<E>;
+    constexpr int D = (SX & (E - 1)) | ((SY & (E - 1)) << G::LOG) | ((SZ & (E - 1)) << (2 * G::LOG));
+    sl = ((t & G::LM) + (D & G::LM)) ^ ((t & G::H) ^ (D & G::H));
+    d = 13;
+    if constexpr (SX < 0) d -= xlo;
+    if constexpr (SX > 0) d += xhi;
+    if constexpr (SY < 0) d -= 3 * ylo;
+    if constexpr (SY > 0) d += 3 * yhi;
+    if constexpr (SZ < 0) d -= 9 * zlo;
+    if constexpr (SZ > 0) d += 9 * zhi;
+}
+
+__device__ __forceinline__ bool bit_of(const unsigned long long* words, int local) {
+    return (words[local >> 6] >> (local & 63)) & 1ull;
+}
+
+/// collide_level (multires.cpp:443-456): post = BGK(cur) on the listed blocks.
+template <class L, class R, bool Exact, int E>
+__global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
+    constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W;
+    const int b = A.blocks[blockIdx.x];
+    const int t = threadIdx.x;
+    if (!((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
+    const long long base = (long long)b * Q * BV + t;
+    R f[Q];
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        f[i] = __ldg(A.cur + base + i * BV);
+    });
+    bool ok = true;
+    R rho, u[3];
+    if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
+    else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok);
+    if (!ok) atomicMin(A.error_flag, A.step);
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        A.post[base + i * BV] = f[i];
+    });
+}
+
+/// Stages the 27-neighbourhood of block b: post base pointers, active masks
+/// and block classes.
+template <int Q, class R, int E>
+struct Stage {
+    const R* post[27];
+    R* nxt[27];
+    unsigned long long mask[27][BlockGeom<E>::W];
+    int cls[27];
+};
+
+template <int Q, class R, int E>
+__device__ __forceinline__ void stage_neighbourhood(const MresArgs<Q, R>& A, int b, Stage<Q, R, E>& S) {
+    constexpr int BV = E * E * E, W = BlockGeom<E>::W;
+    const int t = threadIdx.x;
+    __shared__ int s_nb[27];
+    if (t < 27) {
+        const int nb = A.nbr[(long long)b * 27 + t];
+        s_nb[t] = nb;
+        const int ob = nb < 0 ? b : nb;
+        S.post[t] = A.post + (long long)ob * Q * BV;
+        S.nxt[t] = A.nxt + (long long)ob * Q * BV;
+        S.cls[t] = nb < 0 ? int(kNone) : int(A.cls[nb]);
+    }
+    __syncthreads();
+    for (int j = t; j < 27 * W; j += BV) {
+        const int d = j / W, w = j % W;
+        const int nb = s_nb[d];
+        S.mask[d][w] = nb >= 0 ? A.amask[(long long)nb * W + w] : 0ull;
+    }
+    __syncthreads();
+}
+
+/// stream_level / stream_voxel (multires.cpp:485-561) over the listed blocks.
+/// In-domain sources are plain loads of the post buffer (active, ghost or
+/// coalesced ring slots). FUSED: sources that are active cells of uniform
+/// blocks are skipped -- their owners push those populations.
+template <class L, class R, bool Exact, int E, bool FUSED>
+__global__ void __launch_bounds__(E* E* E) mres_stream_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
+    constexpr int Q = L::Q, BV = E * E * E;
+    using Ar = Arith<R, Exact>;
+    __shared__ Stage<Q, R, E> S;
+    const int b = A.blocks[blockIdx.x];
+    stage_neighbourhood<Q, R, E>(A, b, S);
+    const int t = threadIdx.x;
+    if (!bit_of(S.mask[13], t)) return;
+    constexpr int LOG = BlockGeom<E>::LOG;
+    const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
+    const int x = A.org[3 * b] + lx, y = A.org[3 * b + 1] + ly, z = A.org[3 * b + 2] + lz;
+    const bool xlo = lx == 0, xhi = lx == E - 1, ylo = ly == 0, yhi = ly == E - 1, zlo = lz == 0, zhi = lz == E - 1;
+    const bool dxlo = x == 0, dxhi = x == A.n[0] - 1, dylo = y == 0, dyhi = y == A.n[1] - 1, dzlo = z == 0,
+               dzhi = z == A.n[2] - 1;
+    const R* own_post = S.post[13] + t;
+    R* own_nxt = A.nxt + (long long)b * Q * BV + t;
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
+        constexpr int oi = L::opp(i);
+        bool oob = false;
+        if constexpr (ex > 0) oob = oob || dxlo;
+        if constexpr (ex < 0) oob = oob || dxhi;
+        if constexpr (ey > 0) oob = oob || dylo;
+        if constexpr (ey < 0) oob = oob || dyhi;
+        if constexpr (ez > 0) oob = oob || dzlo;
+        if constexpr (ez < 0) oob = oob || dzhi;
+        if (oob) {
+            R v = own_post[oi * BV];
+            if constexpr (ez < 0) {
+                if (A.has_lid && dzhi) v = Ar::add(v, A.lid[i]);
+            }
+            own_nxt[i * BV] = v;
+        } else {
+            int d, sl;
+            shifted<E, -ex, -ey, -ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
+            bool skip = false;
+            if constexpr (FUSED) skip = S.cls[d] == kUniform && bit_of(S.mask[d], sl);
+            if (!skip) own_nxt[i * BV] = S.post[d][i * BV + sl];
+        }
+    });
+}
+
+/// fused_level (multires.cpp:541-561) as one pass: collide in registers, push
+/// the post-collision populations to their pull destinations (bounce-back and
+/// lid into the own voxel), and pull the directions whose source is a
+/// jump-block cell (materialised post). Writes every nxt slot exactly once
+/// together with the jump-block stream kernel.
+template <class L, class R, bool Exact, int E>
+__global__ void __launch_bounds__(E* E* E) mres_fused_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
+    constexpr int Q = L::Q, BV = E * E * E;
+    using Ar = Arith<R, Exact>;
+    __shared__ Stage<Q, R, E> S;
+    const int b = A.blocks[blockIdx.x];
+    stage_neighbourhood<Q, R, E>(A, b, S);
+    const int t = threadIdx.x;
+    if (!bit_of(S.mask[13], t)) return;
+    constexpr int LOG = BlockGeom<E>::LOG;
+    const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
+    const int x = A.org[3 * b] + lx, y = A.org[3 * b + 1] + ly, z = A.org[3 * b + 2] + lz;
+    const bool xlo = lx == 0, xhi = lx == E - 1, ylo = ly == 0, yhi = ly == E - 1, zlo = lz == 0, zhi = lz == E - 1;
+    const bool dxlo = x == 0, dxhi = x == A.n[0] - 1, dylo = y == 0, dyhi = y == A.n[1] - 1, dzlo = z == 0,
+               dzhi = z == A.n[2] - 1;
+    const long long own = (long long)b * Q * BV + t;
+    R f[Q];
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        f[i] = __ldg(A.cur + own + i * BV);
+    });
+    bool ok = true;
+    R rho, u[3];
+    if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
+    else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok);
+    if (!ok) atomicMin(A.error_flag, A.step);
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
+        constexpr int oi = L::opp(i);
+        // destination w = v + e_i pulls direction i from v
+        bool oob = false;
+        if constexpr (ex > 0) oob = oob || dxhi;
+        if constexpr (ex < 0) oob = oob || dxlo;
+        if constexpr (ey > 0) oob = oob || dyhi;
+        if constexpr (ey < 0) oob = oob || dylo;
+        if constexpr (ez > 0) oob = oob || dzhi;
+        if constexpr (ez < 0) oob = oob || dzlo;
+        if (oob) {
+            // v pulls direction oi from the wall: own post[i] (+ lid term of oi)
+            R val = f[i];
+            if constexpr (ez > 0) {
+                if (A.has_lid && dzhi) val = Ar::add(val, A.lid[oi]);
+            }
+            A.nxt[own + oi * BV] = val;
+        } else {
+            int d, sl;
+            shifted<E, ex, ey, ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
+            S.nxt[d][i * BV + sl] = f[i];
+        }
+    });
+    // directions whose source is a jump-block cell: pull its materialised post
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
+        bool oob = false;
+        if constexpr (ex > 0) oob = oob || dxlo;
+        if constexpr (ex < 0) oob = oob || dxhi;
+        if constexpr (ey > 0) oob = oob || dylo;
+        if constexpr (ey < 0) oob = oob || dyhi;
+        if constexpr (ez > 0) oob = oob || dzlo;
+        if constexpr (ez < 0) oob = oob || dzhi;
+        if (!oob) {
+            int d, sl;
+            shifted<E, -ex, -ey, -ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
+            if (S.cls[d] == kJump) A.nxt[own + i * BV] = S.post[d][i * BV + sl];
+        }
+    });
+}
+
+/// explode (multires.cpp:458-467): ghost(l) <- parent(l+1) post-collision.
+template <int Q, class R>
+__global__ void mres_explode_kernel(R* fine_post, const R* coarse_post, const std::int64_t* dst,
+                                    const std::int64_t* src, int n, int bv) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const long long ds = dst[g], ss = src[g];
+    const long long db = ds / bv, dl = ds % bv, sb = ss / bv, sl = ss % bv;
+    for (int c = 0; c < Q; ++c) fine_post[(db * Q + c) * bv + dl] = coarse_post[(sb * Q + c) * bv + sl];
+}
+
+/// coalesce (multires.cpp:469-483): ring(l) <- mean of the 8 children's
+/// current (post-stream) populations, children_of order, sum * (1/8).
+template <int Q, class R, bool Exact>
+__global__ void mres_coalesce_kernel(R* coarse_post, const R* fine_cur, const std::int64_t* dst,
+                                     const std::int64_t* child, int n, int bv_c, int bv_f, int nchild) {
+    using A = Arith<R, Exact>;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const long long ds = dst[g];
+    const long long db = ds / bv_c, dl = ds % bv_c;
+    const R scale = R(1.0 / double(nchild));
+    for (int c = 0; c < Q; ++c) {
+        R sum = R(0);
+        for (int k = 0; k < nchild; ++k) {
+            const long long cs = child[(long long)g * 8 + k];
+            sum = A::add(sum, fine_cur[((cs / bv_f) * Q + c) * bv_f + cs % bv_f]);
+        }
+        coarse_post[(db * Q + c) * bv_c + dl] = A::mul(sum, scale);
+    }
+}
+
+template <int Q, class R, bool ToDevice>
+__global__ void mres_io_kernel(R* buf, double* staging, const std::int64_t* slots, long long n, int bv,
+                               const double* shift) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const long long slot = slots[v];
+    const long long b = slot / bv, local = slot % bv;
+    for (int c = 0; c < Q; ++c) {
+        R* p = buf + (b * Q + c) * bv + local;
+        if constexpr (ToDevice) *p = R(staging[v * Q + c] - shift[c]);
+        else staging[v * Q + c] = double(*p) + shift[c];
+    }
+}
+
+template <class R>
+__global__ void mres_fill_kernel(R* buf, long long total, int bv, int q, const double* val) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    buf[e] = R(val[int((e / bv) % q)]);
+}
+
+template <class F>
+void mres_dispatch(int lattice, Precision prec, int edge, F&& f) {
+    auto by_edge = [&](auto lat, auto real, auto exact) {
+        using L = decltype(lat);
+        using R = decltype(real);
+        if (edge == 8) f(L{}, R{}, exact, std::integral_constant<int, 8>{});
+        else if (edge == 4) f(L{}, R{}, exact, std::integral_constant<int, 4>{});
+        else throw std::invalid_argument("multires engine: block edge must be 4 or 8");
+    };
+    auto by_prec = [&](auto lat) {
+        if (prec == Precision::F64) by_edge(lat, double{}, std::true_type{});
+        else by_edge(lat, float{}, std::false_type{});
+    };
+    switch (lattice) {
+        case kD3Q19: by_prec(D3Q19{}); break;
+        case kD3Q27: by_prec(D3Q27{}); break;
+        default: throw std::invalid_argument("multires engine: D3Q19 or D3Q27 (3D cavity)");
+    }
+}
+
+inline std::int64_t lin3(const std::array<int, 3>& d, int x, int y, int z) {
+    return (std::int64_t(z) * d[1] + y) * d[0] + x;
+}
+
+/// 26-neighbourhood dilation of a byte mask (separable max filter).
+std::vector<std::uint8_t> box_dilate(const std::vector<std::uint8_t>& m, const std::array<int, 3>& d) {
+    std::vector<std::uint8_t> a = m, b(m.size());
+    for (int axis = 0; axis < 3; ++axis) {
+        const std::int64_t stride = axis == 0 ? 1 : (axis == 1 ? d[0] : std::int64_t(d[0]) * d[1]);
+        for (int z = 0; z < d[2]; ++z)
+            for (int y = 0; y < d[1]; ++y)
+                for (int x = 0; x < d[0]; ++x) {
+                    const std::int64_t i = lin3(d, x, y, z);
+                    const int c = axis == 0 ? x : (axis == 1 ? y : z);
+                    std::uint8_t v = a[i];
+                    if (c > 0) v |= a[i - stride];
+                    if (c + 1 < d[axis]) v |= a[i + stride];
+                    b[i] = v;
+                }
+        std::swap(a, b);
+    }
+    return a;
+}
+
+} // namespace
+
+struct MultiResEngine::Level {
+    std::array<int, 3> n{1, 1, 1};
+    BlockGrid ext;
+    void* cur = nullptr;
+    void* nxt = nullptr;
+    void* post = nullptr;
+    std::int32_t* nbr = nullptr;
+    std::uint64_t* amask = nullptr;
+    std::uint8_t* cls = nullptr;
+    int* org = nullptr;
+    int* all_blocks = nullptr;
+    int* uni_blocks = nullptr;
+    int* jump_blocks = nullptr;
+    int n_all = 0, n_uni = 0, n_jump = 0;
+    std::int64_t* explode_dst = nullptr;  // ghost cells of this level
+    std::int64_t* explode_src = nullptr;  // parent slots at level + 1
+    int n_ghost = 0;
+    std::int64_t* coal_dst = nullptr;    // ring cells of this level
+    std::int64_t* coal_child = nullptr;  // 8 child slots at level - 1
+    int n_ring = 0;
+    std::int64_t* slots = nullptr;
+    std::int64_t n_active = 0;
+    double inv_tau = 1.0;
+    std::int64_t slot(int x, int y, int z) const {
+        const int e = ext.edge();
+        const int b = ext.find_block(x / e, y / e, z / e);
+        if (b < 0) return -1;
+        const int local = ((z % e) * e + (y % e)) * e + (x % e);
+        return std::int64_t(b) * ext.block_volume() + local;
+    }
+};
+
+MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_map) : cfg_(cfg) {
+    if (cfg_.lattice != kD3Q19 && cfg_.lattice != kD3Q27)
+        throw std::invalid_argument("multires engine: D3Q19 or D3Q27 (3D cavity)");
+    if (cfg_.edge != 4 && cfg_.edge != 8) throw std::invalid_argument("multires engine: block edge must be 4 or 8");
+    const LatticeTable lat = make_lattice(cfg_.lattice);
+    q_ = lat.q;
+    esize_ = cfg_.precision == Precision::F64 ? 8 : 4;
+    grid_ = MresGrid::build(cfg_.domain, cfg_.levels, cfg_.lattice, level_map, cfg_.tau, cfg_.reference_tables);
+    const int L = grid_.num_levels();
+    const int E = cfg_.edge;
+    for (int l = 0; l < L; ++l) {
+        const MresLevel& G = grid_.level(l);
+        if (!(G.tau > 0.5)) throw std::invalid_argument("multires: derived tau must stay > 0.5");
+    }
+    VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    std::vector<std::vector<std::uint8_t>> ghost(L), ring(L);
+    for (int l = 0; l < L; ++l) {
+        const MresLevel& G = grid_.level(l);
+        const auto& d = G.domain;
+        const std::size_t vol = G.active.size();
+        const auto near = box_dilate(G.active, d);
+        ghost[l].assign(vol, 0);
+        ring[l].assign(vol, 0);
+        std::vector<std::uint8_t> other(vol, 0);
+        for (std::size_t i = 0; i < vol; ++i) {
+            other[i] = !G.active[i] && (G.refined[i] || G.under_coarse[i]);
+            if (!near[i] || G.active[i]) continue;
+            if (G.under_coarse[i]) ghost[l][i] = 1;
+            else if (!G.refined[i])
+                throw std::invalid_argument("multires: active region has an uncovered neighbor");
+        }
+        // refined ring: refined cells an active cell pulls from along a lattice direction
+        for (int z = 0; z < d[2]; ++z)
+            for (int y = 0; y < d[1]; ++y)
+                for (int x = 0; x < d[0]; ++x) {
+                    const std::int64_t i = lin3(d, x, y, z);
+                    if (!near[i] || G.active[i] || !G.refined[i]) continue;
+                    for (int q = 0; q < lat.q && !ring[l][i]; ++q) {
+                        const int a = x + lat.e[q][0], b = y + lat.e[q][1], c = z + lat.e[q][2];
+                        if (a < 0 || b < 0 || c < 0 || a >= d[0] || b >= d[1] || c >= d[2]) continue;
+                        if (G.active[lin3(d, a, b, c)]) ring[l][i] = 1;
+                    }
+                }
+        const auto crossing_near = box_dilate(other, d);
+        Level* V = new Level;
+        lv_.push_back(V);
+        V->n = d;
+        V->n_active = G.num_active;
+        V->inv_tau = 1.0 / G.tau;
+        std::vector<std::uint8_t> ext(vol);
+        for (std::size_t i = 0; i < vol; ++i) ext[i] = G.active[i] | ghost[l][i] | ring[l][i];
+        V->ext = BlockGrid::build(d, ext.data(), E);
+        const BlockGrid& bg = V->ext;
+        const int nb = bg.num_blocks(), W = bg.mask_words(), BV = bg.block_volume();
+        std::vector<std::uint64_t> am(std::size_t(nb) * W, 0);
+        std::vector<std::uint8_t> cls(nb, kNone);
+        std::vector<int> org(std::size_t(nb) * 3), all, uni, jmp;
+        for (int b = 0; b < nb; ++b) {
+            const auto& o = bg.blocks()[b].origin;
+            for (int a = 0; a < 3; ++a) org[std::size_t(b) * 3 + a] = o[a];
+            bool any = false, cross = false;
+            for (int local = 0; local < BV; ++local) {
+                const int x = o[0] + local % E, y = o[1] + (local / E) % E, z = o[2] + local / (E * E);
+                if (x >= d[0] || y >= d[1] || z >= d[2]) continue;
+                const std::int64_t i = lin3(d, x, y, z);
+                if (!G.active[i]) continue;
+                any = true;
+                am[std::size_t(b) * W + (local >> 6)] |= 1ull << (local & 63);
+                if (crossing_near[i]) cross = true;
+            }
+            if (any) {
+                cls[b] = cross ? kJump : kUniform;
+                all.push_back(b);
+                (cross ? jmp : uni).push_back(b);
+            }
+        }
+        V->n_all = int(all.size());
+        V->n_uni = int(uni.size());
+        V->n_jump = int(jmp.size());
+        auto up_i32 = [&](const std::vector<int>& v, int** dst) {
+            VOXL_CUDA(cudaMalloc(dst, std::max<std::size_t>(1, v.size()) * sizeof(int)));
+            if (!v.empty()) VOXL_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+        };
+        up_i32(all, &V->all_blocks);
+        up_i32(uni, &V->uni_blocks);
+        up_i32(jmp, &V->jump_blocks);
+        up_i32(org, &V->org);
+        const auto nbr = bg.neighbour_table();
+        VOXL_CUDA(cudaMalloc(&V->nbr, nbr.size() * sizeof(std::int32_t)));
+        VOXL_CUDA(cudaMemcpy(V->nbr, nbr.data(), nbr.size() * sizeof(std::int32_t), cudaMemcpyHostToDevice));
+        VOXL_CUDA(cudaMalloc(&V->amask, am.size() * sizeof(std::uint64_t)));
+        VOXL_CUDA(cudaMemcpy(V->amask, am.data(), am.size() * sizeof(std::uint64_t), cudaMemcpyHostToDevice));
+        VOXL_CUDA(cudaMalloc(&V->cls, nb));
+        VOXL_CUDA(cudaMemcpy(V->cls, cls.data(), nb, cudaMemcpyHostToDevice));
+        const std::size_t bytes = std::size_t(nb) * q_ * BV * esize_;
+        for (void** p : {&V->cur, &V->nxt, &V->post}) {
+            VOXL_CUDA(cudaMalloc(p, bytes));
+            VOXL_CUDA(cudaMemsetAsync(*p, 0, bytes, stream_));
+        }
+        // canonical slots: active cells, x slowest, z fastest
+        std::vector<std::int64_t> slots;
+        slots.reserve(std::size_t(G.num_active));
+        for (int x = 0; x < d[0]; ++x)
+            for (int y = 0; y < d[1]; ++y)
+                for (int z = 0; z < d[2]; ++z)
+                    if (G.active[lin3(d, x, y, z)]) slots.push_back(V->slot(x, y, z));
+        VOXL_CUDA(cudaMalloc(&V->slots, std::max<std::size_t>(1, slots.size()) * sizeof(std::int64_t)));
+        VOXL_CUDA(cudaMemcpy(V->slots, slots.data(), slots.size() * sizeof(std::int64_t), cudaMemcpyHostToDevice));
+    }
+    // explosion pairs (ghost at l, parent at l+1) and coalescence records
+    // (ring at l, children at l-1), now that every level's slots exist.
+    const int dim = grid_.dim();
+    for (int l = 0; l < L; ++l) {
+        const MresLevel& G = grid_.level(l);
+        const auto& d = G.domain;
+        std::vector<std::int64_t> gd, gs, cd, cc;
+        for (int z = 0; z < d[2]; ++z)
+            for (int y = 0; y < d[1]; ++y)
+                for (int x = 0; x < d[0]; ++x) {
+                    const std::int64_t i = lin3(d, x, y, z);
+                    if (ghost[l][i]) {
+                        gd.push_back(lv_[l]->slot(x, y, z));
+                        gs.push_back(lv_[l + 1]->slot(x >> 1, y >> 1, dim == 3 ? z >> 1 : z));
+                    }
+                    if (ring[l][i]) {
+                        cd.push_back(lv_[l]->slot(x, y, z));
+                        const int zhi = dim == 3 ? 1 : 0;
+                        int k = 0;
+                        for (int dz = 0; dz <= zhi; ++dz)
+                            for (int dy = 0; dy <= 1; ++dy)
+                                for (int dx = 0; dx <= 1; ++dx, ++k) {
+                                    const int cz = dim == 3 ? 2 * z + dz : z;
+                                    const std::int64_t s = lv_[l - 1]->slot(2 * x + dx, 2 * y + dy, cz);
+                                    if (s < 0 || !grid_.active(l - 1, 2 * x + dx, 2 * y + dy, cz))
+                                        throw std::invalid_argument("multires: refined cell with inactive children");
+                                    cc.push_back(s);
+                                }
+                        for (; k < 8; ++k) cc.push_back(cc.back());
+                    }
+                }
+        Level* V = lv_[l];
+        V->n_ghost = int(gd.size());
+        V->n_ring = int(cd.size());
+        auto up64 = [&](const std::vector<std::int64_t>& v, std::int64_t** dst) {
+            VOXL_CUDA(cudaMalloc(dst, std::max<std::size_t>(1, v.size()) * sizeof(std::int64_t)));
+            if (!v.empty())
+                VOXL_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(std::int64_t), cudaMemcpyHostToDevice));
+        };
+        up64(gd, &V->explode_dst);
+        up64(gs, &V->explode_src);
+        up64(cd, &V->coal_dst);
+        up64(cc, &V->coal_child);
+    }
+    VOXL_CUDA(cudaMalloc(&d_error_, sizeof(int)));
+    const int big = INT_MAX;
+    VOXL_CUDA(cudaMemcpy(d_error_, &big, sizeof(int), cudaMemcpyHostToDevice));
+    VOXL_CUDA(cudaMalloc(&d_diag_, (2 * 592 + 64) * sizeof(double)));
+    const double u0[3] = {0.0, 0.0, 0.0};
+    set_equilibrium(1.0, u0);  // multires.cpp:574-575
+}
+
+MultiResEngine::~MultiResEngine() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (Level* V : lv_) {
+        for (void* p : {V->cur, V->nxt, V->post}) cudaFree(p);
+        cudaFree(V->nbr);
+        cudaFree(V->amask);
+        cudaFree(V->cls);
+        cudaFree(V->org);
+        cudaFree(V->all_blocks);
+        cudaFree(V->uni_blocks);
+        cudaFree(V->jump_blocks);
+        cudaFree(V->explode_dst);
+        cudaFree(V->explode_src);
+        cudaFree(V->coal_dst);
+        cudaFree(V->coal_child);
+        cudaFree(V->slots);
+        delete V;
+    }
+    cudaFree(d_error_);
+    cudaFree(d_diag_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+std::int64_t MultiResEngine::state_len() const {
+    std::int64_t n = 0;
+    for (const Level* V : lv_) n += V->n_active * q_;
+    return n;
+}
+
+void MultiResEngine::set_equilibrium(double rho, const double u[3]) {
+    // set_uniform_equilibrium (multires.cpp:578-587): every slot of cur.
+    const LatticeTable t = make_lattice(cfg_.lattice);
+    std::vector<double> val(q_);
+    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    for (int i = 0; i < q_; ++i) {
+        const double eu = double(t.e[i][0]) * u[0] + double(t.e[i][1]) * u[1] + double(t.e[i][2]) * u[2];
+        const double w = double(t.wnum[i]) / double(t.wden[i]);
+        val[i] = w * rho * (1.0 + 3.0 * eu + 4.5 * eu * eu - 1.5 * uu) - (esize_ == 8 ? 0.0 : w);
+    }
+    double* d_val = nullptr;
+    VOXL_CUDA(cudaMalloc(&d_val, q_ * sizeof(double)));
+    VOXL_CUDA(cudaMemcpy(d_val, val.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
+    for (Level* V : lv_) {
+        const long long total = (long long)V->ext.num_blocks() * q_ * V->ext.block_volume();
+        for (void* p : {V->cur, V->nxt, V->post}) {
+            if (esize_ == 8)
+                mres_fill_kernel<double><<<unsigned((total + 255) / 256), 256, 0, stream_>>>(
+                    static_cast<double*>(p), total, V->ext.block_volume(), q_, d_val);
+            else
+                mres_fill_kernel<float><<<unsigned((total + 255) / 256), 256, 0, stream_>>>(
+                    static_cast<float*>(p), total, V->ext.block_volume(), q_, d_val);
+        }
+        VOXL_CUDA(cudaGetLastError());
+    }
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(d_val);
+}
+
+void MultiResEngine::set_state(const double* canonical) {
+    const LatticeTable t = make_lattice(cfg_.lattice);
+    std::vector<double> shift(q_);
+    for (int i = 0; i < q_; ++i) shift[i] = esize_ == 8 ? 0.0 : double(t.wnum[i]) / double(t.wden[i]);
+    double* d_shift = nullptr;
+    VOXL_CUDA(cudaMalloc(&d_shift, q_ * sizeof(double)));
+    VOXL_CUDA(cudaMemcpy(d_shift, shift.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
+    std::int64_t off = 0;
+    for (Level* V : lv_) {
+        const long long n = V->n_active;
+        double* st = nullptr;
+        VOXL_CUDA(cudaMalloc(&st, std::max<long long>(1, n * q_) * sizeof(double)));
+        VOXL_CUDA(cudaMemcpy(st, canonical + off, n * q_ * sizeof(double), cudaMemcpyHostToDevice));
+        if (esize_ == 8) {
+            if (q_ == 19) mres_io_kernel<19, double, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+            else mres_io_kernel<27, double, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+        } else {
+            if (q_ == 19) mres_io_kernel<19, float, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+            else mres_io_kernel<27, float, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+        }
+        VOXL_CUDA(cudaGetLastError());
+        VOXL_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(st);
+        off += n * q_;
+    }
+    cudaFree(d_shift);
+}
+
+void MultiResEngine::get_state(double* canonical) {
+    // canonical_state (multires.cpp:578-598): levels finest first
+    const LatticeTable t = make_lattice(cfg_.lattice);
+    std::vector<double> shift(q_);
+    for (int i = 0; i < q_; ++i) shift[i] = esize_ == 8 ? 0.0 : double(t.wnum[i]) / double(t.wden[i]);
+    double* d_shift = nullptr;
+    VOXL_CUDA(cudaMalloc(&d_shift, q_ * sizeof(double)));
+    VOXL_CUDA(cudaMemcpy(d_shift, shift.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
+    std::int64_t off = 0;
+    for (Level* V : lv_) {
+        const long long n = V->n_active;
+        double* st = nullptr;
+        VOXL_CUDA(cudaMalloc(&st, std::max<long long>(1, n * q_) * sizeof(double)));
+        if (esize_ == 8) {
+            if (q_ == 19) mres_io_kernel<19, double, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+            else mres_io_kernel<27, double, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+        } else {
+            if (q_ == 19) mres_io_kernel<19, float, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+            else mres_io_kernel<27, float, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
+        }
+        VOXL_CUDA(cudaGetLastError());
+        VOXL_CUDA(cudaMemcpyAsync(canonical + off, st, n * q_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        VOXL_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(st);
+        off += n * q_;
+    }
+    cudaFree(d_shift);
+}
+
+void MultiResEngine::mark_begin(int, cudaEvent_t* b) {
+    if (!events_) return;
+    VOXL_CUDA(cudaEventCreate(b));
+    VOXL_CUDA(cudaEventRecord(*b, stream_));
+}
+
+void MultiResEngine::mark_end(int cls, cudaEvent_t b) {
+    if (!events_) return;
+    cudaEvent_t e;
+    VOXL_CUDA(cudaEventCreate(&e));
+    VOXL_CUDA(cudaEventRecord(e, stream_));
+    events_->push_back({cls, {b, e}});
+}
+
+namespace {
+
+template <class L, class R, bool Exact>
+MresArgs<L::Q, R> level_args(const MresConfig& cfg, MultiResEngine::Level* V, int step, int* err) {
+    MresArgs<L::Q, R> A{};
+    A.cur = static_cast<const R*>(V->cur);
+    A.nxt = static_cast<R*>(V->nxt);
+    A.post = static_cast<R*>(V->post);
+    A.nbr = V->nbr;
+    A.amask = V->amask;
+    A.cls = V->cls;
+    A.org = V->org;
+    for (int a = 0; a < 3; ++a) A.n[a] = V->n[a];
+    const double inv_tau = V->inv_tau;
+    A.omega = R(inv_tau);
+    A.keep = Exact ? R(1.0 - inv_tau) : R(1) - R(inv_tau);
+    for (int i = 0; i < L::Q; ++i) {
+        const double eu = double(L::ex(i)) * cfg.lid_u[0] + double(L::ey(i)) * cfg.lid_u[1] +
+                          double(L::ez(i)) * cfg.lid_u[2];
+        A.lid[i] = R(2.0 * L::w(i) * 1.0 * 3.0 * eu);
+    }
+    A.has_lid = 1;  // multires runs are lid-driven cavities (solver.cpp:41-42)
+    A.step = step;
+    A.error_flag = err;
+    return A;
+}
+
+} // namespace
+
+void MultiResEngine::launch_collide(int l, bool jump_only) {
+    Level* V = lv_[l];
+    const int nb = jump_only ? V->n_jump : V->n_all;
+    if (nb == 0) return;
+    cudaEvent_t b{};
+    mark_begin(kTCollide, &b);
+    mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
+        using L = decltype(lat);
+        using R = decltype(real);
+        constexpr bool X = decltype(exact)::value;
+        constexpr int E = decltype(e)::value;
+        auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+        A.blocks = jump_only ? V->jump_blocks : V->all_blocks;
+        mres_collide_kernel<L, R, X, E><<<nb, E * E * E, 0, stream_>>>(A);
+    });
+    VOXL_CUDA(cudaGetLastError());
+    mark_end(kTCollide, b);
+}
+
+void MultiResEngine::launch_stream(int l, bool jump_only) {
+    Level* V = lv_[l];
+    const int nb = jump_only ? V->n_jump : V->n_all;
+    if (nb == 0) return;
+    cudaEvent_t b{};
+    mark_begin(kTStream, &b);
+    mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
+        using L = decltype(lat);
+        using R = decltype(real);
+        constexpr bool X = decltype(exact)::value;
+        constexpr int E = decltype(e)::value;
+        auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+        A.blocks = jump_only ? V->jump_blocks : V->all_blocks;
+        if (jump_only) mres_stream_kernel<L, R, X, E, true><<<nb, E * E * E, 0, stream_>>>(A);
+        else mres_stream_kernel<L, R, X, E, false><<<nb, E * E * E, 0, stream_>>>(A);
+    });
+    VOXL_CUDA(cudaGetLastError());
+    mark_end(kTStream, b);
+}
+
+void MultiResEngine::launch_fused(int l) {
+    Level* V = lv_[l];
+    if (V->n_uni == 0) return;
+    cudaEvent_t b{};
+    mark_begin(kTFused, &b);
+    mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
+        using L = decltype(lat);
+        using R = decltype(real);
+        constexpr bool X = decltype(exact)::value;
+        constexpr int E = decltype(e)::value;
+        auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+        A.blocks = V->uni_blocks;
+        mres_fused_kernel<L, R, X, E><<<V->n_uni, E * E * E, 0, stream_>>>(A);
+    });
+    VOXL_CUDA(cudaGetLastError());
+    mark_end(kTFused, b);
+}
+
+void MultiResEngine::launch_explode(int coarse) {
+    Level* F = lv_[coarse - 1];
+    Level* Cc = lv_[coarse];
+    if (F->n_ghost == 0) return;
+    cudaEvent_t b{};
+    mark_begin(kTTransition, &b);
+    const unsigned grid = unsigned((F->n_ghost + 127) / 128);
+    if (esize_ == 8) {
+        if (q_ == 19) mres_explode_kernel<19, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(F->post), static_cast<const double*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+        else mres_explode_kernel<27, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(F->post), static_cast<const double*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+    } else {
+        if (q_ == 19) mres_explode_kernel<19, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(F->post), static_cast<const float*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+        else mres_explode_kernel<27, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(F->post), static_cast<const float*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+    }
+    VOXL_CUDA(cudaGetLastError());
+    mark_end(kTTransition, b);
+}
+
+void MultiResEngine::launch_coalesce(int coarse) {
+    Level* F = lv_[coarse - 1];
+    Level* Cc = lv_[coarse];
+    if (Cc->n_ring == 0) return;
+    cudaEvent_t b{};
+    mark_begin(kTTransition, &b);
+    const unsigned grid = unsigned((Cc->n_ring + 127) / 128);
+    const int nchild = grid_.dim() == 3 ? 8 : 4;
+    const int bvc = Cc->ext.block_volume(), bvf = F->ext.block_volume();
+    if (esize_ == 8) {
+        if (q_ == 19) mres_coalesce_kernel<19, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        else mres_coalesce_kernel<27, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+    } else {
+        if (q_ == 19) mres_coalesce_kernel<19, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        else mres_coalesce_kernel<27, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+    }
+    VOXL_CUDA(cudaGetLastError());
+    mark_end(kTTransition, b);
+}
+
+void MultiResEngine::advance(int l) {
+    // advance (multires.cpp:563-567)
+    launch_collide(l, cfg_.fused);
+    if (l > 0) {
+        launch_explode(l);
+        advance(l - 1);
+        advance(l - 1);
+        launch_coalesce(l);
+    }
+    if (cfg_.fused) launch_fused(l);
+    launch_stream(l, cfg_.fused);
+    Level* V = lv_[l];
+    std::swap(V->cur, V->nxt);
+}
+
+void MultiResEngine::check_errors() {
+    int flag = INT_MAX;
+    VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    if (flag != INT_MAX)
+        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": non-positive density");
+}
+
+void MultiResEngine::coarse_step(int n) {
+    for (int i = 0; i < n; ++i) {
+        advance(grid_.num_levels() - 1);
+        ++steps_done_;
+    }
+    check_errors();
+}
+
+MresTimes MultiResEngine::timed_steps(int n) {
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    events_ = &ev;
+    cudaEvent_t t0, t1;
+    VOXL_CUDA(cudaEventCreate(&t0));
+    VOXL_CUDA(cudaEventCreate(&t1));
+    VOXL_CUDA(cudaEventRecord(t0, stream_));
+    for (int i = 0; i < n; ++i) {
+        advance(grid_.num_levels() - 1);
+        ++steps_done_;
+    }
+    VOXL_CUDA(cudaEventRecord(t1, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    events_ = nullptr;
+    MresTimes T;
+    float ms = 0;
+    VOXL_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    T.total = ms;
+    for (auto& e : ev) {
+        float m = 0;
+        VOXL_CUDA(cudaEventElapsedTime(&m, e.second.first, e.second.second));
+        (e.first == kTCollide ? T.collide : e.first == kTStream ? T.stream : e.first == kTFused ? T.fused
+                                                                                                 : T.transition) += m;
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    check_errors();
+    return T;
+}
+
+DenseDiag MultiResEngine::probe() {
+    // probe_field over canonical_state (solver.cpp:345): plain sum over all
+    // levels' cells and max |u|; computed on the host copy of the state.
+    std::vector<double> s(static_cast<std::size_t>(state_len()));
+    get_state(s.data());
+    DenseDiag d;
+    const LatticeTable t = make_lattice(cfg_.lattice);
+    for (std::size_t v = 0; v * q_ < s.size(); ++v) {
+        double r = 0, mx = 0, my = 0, mz = 0;
+        for (int i = 0; i < q_; ++i) {
+            const double f = s[v * q_ + i];
+            if (!std::isfinite(f) || std::fabs(f) > 1e3) {
+                if (!d.unstable) {
+                    d.unstable = 1;
+                    d.bad_voxel = std::int64_t(v);
+                    d.bad_population = i;
+                }
+            }
+            d.mass += f;
+            r += f;
+            mx += f * t.e[i][0];
+            my += f * t.e[i][1];
+            mz += f * t.e[i][2];
+        }
+        if (r > 0) d.max_speed = std::max(d.max_speed, std::sqrt(mx * mx + my * my + mz * mz) / r);
+    }
+    return d;
+}
+
+double MultiResEngine::total_mass() {
+    // total_mass (multires.cpp:600-609): per-level sums weighted by 8^l
+    std::vector<double> s(static_cast<std::size_t>(state_len()));
+    get_state(s.data());
+    double mass = 0.0;
+    std::size_t off = 0;
+    for (int l = 0; l < grid_.num_levels(); ++l) {
+        double lev = 0.0;
+        const std::size_t n = std::size_t(lv_[l]->n_active) * q_;
+        for (std::size_t i = 0; i < n; ++i) lev += s[off + i];
+        off += n;
+        mass += lev * std::pow(double(grid_.dim() == 3 ? 8 : 4), l);
+    }
+    return mass;
+}
+
+std::array<std::int64_t, 2> MultiResEngine::fusion_counts(int l) const { return {lv_[l]->n_uni, lv_[l]->n_jump}; }
+
+std::string MultiResEngine::graph_dot() const {
+    if (grid_.has_reference_tables() && cfg_.edge == 4) return grid_.graph_dot(cfg_.fused);
+    std::vector<std::array<std::int64_t, 2>> counts;
+    for (int l = 0; l < grid_.num_levels(); ++l) counts.push_back(fusion_counts(l));
+    return grid_.graph_dot(cfg_.fused, &counts);
+}
+
+} // namespace voxl_b200

@@ -1,0 +1,97 @@
+// multires.cuh -- multi-resolution LBM engine on B200.
+//
+// Drop-in for mres::MultiResLbm (proj/include/voxl/multires.hpp:138-190,
+// proj/src/multires.cpp:367-598). Each level is an edge-E block-sparse grid
+// (E = 8 production, 4 reference granularity) extended by its ghost ring and
+// refined ring; per level three populations buffers: cur (pre-collision, the
+// reference's state), nxt, and post (post-collision of jump-block / staged
+// cells, exploded parent values on ghost cells, coalesced child averages on
+// ring cells). One coarse step is the reference's recursive schedule
+// (advance, multires.cpp:563-576) as a launch sequence:
+//   collide(l) [jump blocks | all] ; explode(l) ; advance(l-1) x2 ;
+//   coalesce(l) ; fused(l) [uniform blocks] ; stream(l) [jump | all]
+// Fused mode: uniform blocks run ONE kernel that reads cur once, collides in
+// registers and pushes the post-collision populations to their destinations
+// (pulling only from jump-block sources) -- 152 B/LUP instead of the staged
+// 304 B/LUP -- while jump blocks keep the staged collide -> stream pair that
+// the explosion / coalescence operators need. Results are bitwise equal to
+// the staged schedule (fp64) as in the reference (multires_test.cpp:381-455).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "multires_grid.hpp"
+
+namespace voxl_b200 {
+
+struct MresConfig {
+    int lattice = 1;
+    std::array<int, 3> domain{32, 32, 32};
+    int levels = 3;
+    double tau = 0.56;  // coarsest level
+    std::array<double, 3> lid_u{0.05, 0.0, 0.0};
+    bool fused = true;
+    Precision precision = Precision::F32;
+    int edge = 8;
+    bool reference_tables = false;
+};
+
+struct MresTimes {
+    double total = 0, collide = 0, stream = 0, fused = 0, transition = 0;
+};
+
+class MultiResEngine {
+public:
+    MultiResEngine(const MresConfig& cfg, const std::int32_t* level_map);
+    ~MultiResEngine();
+    MultiResEngine(const MultiResEngine&) = delete;
+    MultiResEngine& operator=(const MultiResEngine&) = delete;
+
+    const MresConfig& config() const { return cfg_; }
+    const MresGrid& grid() const { return grid_; }
+    int q() const { return q_; }
+    std::int64_t state_len() const;
+    void set_equilibrium(double rho, const double u[3]);
+    void set_state(const double* canonical);
+    void get_state(double* canonical);
+    void coarse_step(int n);
+    MresTimes timed_steps(int n);
+    DenseDiag probe();
+    double total_mass();
+    std::string graph_dot() const;
+    /// Device-grid (uniform, jump) block counts per level.
+    std::array<std::int64_t, 2> fusion_counts(int l) const;
+    int edge() const { return cfg_.edge; }
+    void check_errors();
+
+    struct Level;
+
+private:
+    MresConfig cfg_;
+    int q_ = 19;
+    int esize_ = 4;
+    MresGrid grid_;
+    std::vector<Level*> lv_;
+    cudaStream_t stream_ = nullptr;
+    int* d_error_ = nullptr;
+    double* d_diag_ = nullptr;
+    int steps_done_ = 0;
+    // timing (events around each launch class) when non-null
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* events_ = nullptr;
+
+    void advance(int l);
+    void launch_collide(int l, bool jump_only);
+    void launch_stream(int l, bool jump_only);
+    void launch_fused(int l);
+    void launch_explode(int coarse);
+    void launch_coalesce(int coarse);
+    void mark_begin(int cls, cudaEvent_t* b);
+    void mark_end(int cls, cudaEvent_t b);
+};
+
+} // namespace voxl_b200

@@ -31,6 +31,7 @@ struct SparseArgs {
     R* nxt;
     const std::int32_t* nbr;      // 27 per block
     const std::uint64_t* masks;   // WORDS per block
+    const std::uint8_t* full;     // 1 iff the block and its 26 neighbours are all fully active
     const int* origins;           // 3 per block
     int block_begin;
     const std::uint8_t* bitmask;  // DisagBitmask: skip blocks whose bit != want
@@ -137,36 +138,59 @@ __global__ void __launch_bounds__(E* E* E) sparse_step_kernel(const __grid_const
     constexpr int W = BV >= 64 ? BV / 64 : 1;
     const int b = A.block_begin + int(blockIdx.x);
     if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip
+    __shared__ const R* s_ptr[27];  // component-0 plane of neighbour block d (own block if absent)
     __shared__ int s_nbr[27];
     __shared__ unsigned long long s_mask[27][W];
+    __shared__ int s_full;
     const int t = threadIdx.x;
-    if (t < 27) s_nbr[t] = A.nbr[(long long)b * 27 + t];
-    __syncthreads();
-    for (int j = t; j < 27 * W; j += BV) {
-        const int d = j / W, w = j % W;
-        const int nb = s_nbr[d];
-        s_mask[d][w] = nb >= 0 ? A.masks[(long long)nb * W + w] : 0ull;
+    if (t < 27) {
+        const int nb = A.nbr[(long long)b * 27 + t];
+        s_nbr[t] = nb;
+        s_ptr[t] = A.cur + (long long)(nb < 0 ? b : nb) * Q * BV;
     }
+    if (t == 32) s_full = A.full[b];
     __syncthreads();
-    if (!((s_mask[13][t >> 6] >> (t & 63)) & 1ull)) return;  // inactive slot
-    const int lx = t % E, ly = (t / E) % E, lz = t / (E * E);
+    // CTA-uniform: every block of the 27-neighbourhood exists and is fully
+    // active, so no pull can hit a solid and the mask tests are skipped.
+    const bool full = s_full != 0;
+    if (!full) {
+        for (int j = t; j < 27 * W; j += BV) {
+            const int d = j / W, w = j % W;
+            const int nb = s_nbr[d];
+            s_mask[d][w] = nb >= 0 ? A.masks[(long long)nb * W + w] : 0ull;
+        }
+        __syncthreads();
+        if (!((s_mask[13][t >> 6] >> (t & 63)) & 1ull)) return;  // inactive slot
+    }
+    constexpr int LOG = E == 8 ? 3 : (E == 4 ? 2 : (E == 2 ? 1 : 0));
+    const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
     const long long self_base = (long long)b * Q * BV;
+    const bool xlo = lx == 0, xhi = lx == E - 1, ylo = ly == 0, yhi = ly == E - 1, zlo = lz == 0, zhi = lz == E - 1;
+    // SWAR field-wise add mod E: source local = (lx-ex, ly-ey, lz-ez) mod E.
+    constexpr int H = (1 << (LOG - 1)) | (1 << (2 * LOG - 1)) | (1 << (3 * LOG - 1));
+    constexpr int LM = (BV - 1) & ~H;
+    const int tL = t & LM, tH = t & H;
 
     R g[Q];
     static_for<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
         constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
         constexpr int oi = L::opp(i);
-        const int sx = lx - ex, sy = ly - ey, sz = lz - ez;
-        const int dx = ex == 0 ? 1 : (sx < 0 ? 0 : (sx >= E ? 2 : 1));
-        const int dy = ey == 0 ? 1 : (sy < 0 ? 0 : (sy >= E ? 2 : 1));
-        const int dz = ez == 0 ? 1 : (sz < 0 ? 0 : (sz >= E ? 2 : 1));
-        const int d = dx + 3 * dy + 9 * dz;
-        const int sl = ((sz & (E - 1)) * E + (sy & (E - 1))) * E + (sx & (E - 1));
-        const bool solid = !((s_mask[d][sl >> 6] >> (sl & 63)) & 1ull);
-        const long long src = solid ? self_base + (long long)oi * BV + t
-                                    : (long long)s_nbr[d] * Q * BV + (long long)i * BV + sl;
-        g[i] = __ldg(A.cur + src);
+        constexpr int D = ((-ex) & (E - 1)) | (((-ey) & (E - 1)) << LOG) | (((-ez) & (E - 1)) << (2 * LOG));
+        const int sl = (tL + (D & LM)) ^ (tH ^ (D & H));
+        int d = 13;
+        if constexpr (ex > 0) d -= xlo;
+        if constexpr (ex < 0) d += xhi;
+        if constexpr (ey > 0) d -= 3 * ylo;
+        if constexpr (ey < 0) d += 3 * yhi;
+        if constexpr (ez > 0) d -= 9 * zlo;
+        if constexpr (ez < 0) d += 9 * zhi;
+        const R* src = s_ptr[d] + (i * BV + sl);
+        if (!full) {
+            const bool solid = !((s_mask[d][sl >> 6] >> (sl & 63)) & 1ull);
+            if (solid) src = A.cur + self_base + (oi * BV + t);
+        }
+        g[i] = __ldg(src);
     });
 
     bool ok = true;
@@ -372,6 +396,27 @@ SparseEngine::SparseEngine(const SparseConfig& cfg, const std::uint8_t* active) 
     VOXL_CUDA(cudaMalloc(&d_masks_, grid_.masks().size() * sizeof(std::uint64_t)));
     VOXL_CUDA(cudaMemcpy(d_masks_, grid_.masks().data(), grid_.masks().size() * sizeof(std::uint64_t),
                          cudaMemcpyHostToDevice));
+    {
+        std::vector<std::uint8_t> full(nb, 0);
+        for (std::size_t b = 0; b < nb; ++b) {
+            bool f = true;
+            for (int d = 0; d < 27 && f; ++d) {
+                const int n = nbr[b * 27 + d];
+                if (n < 0) {
+                    f = false;
+                    break;
+                }
+                for (int w = 0; w < grid_.mask_words() && f; ++w) {
+                    const std::uint64_t want =
+                        grid_.block_volume() >= 64 ? ~0ull : ((1ull << grid_.block_volume()) - 1);
+                    f = grid_.mask(n, w) == want;
+                }
+            }
+            full[b] = f;
+        }
+        VOXL_CUDA(cudaMalloc(&d_full_, nb));
+        VOXL_CUDA(cudaMemcpy(d_full_, full.data(), nb, cudaMemcpyHostToDevice));
+    }
     std::vector<int> org(nb * 3);
     for (std::size_t b = 0; b < nb; ++b)
         for (int a = 0; a < 3; ++a) org[3 * b + a] = grid_.blocks()[b].origin[a];
@@ -422,6 +467,7 @@ SparseEngine::~SparseEngine() {
     for (void* b : buf_) cudaFree(b);
     cudaFree(d_nbr_);
     cudaFree(d_masks_);
+    cudaFree(d_full_);
     cudaFree(d_origins_);
     cudaFree(d_bitmask_);
     cudaFree(d_meta_index_);
@@ -518,6 +564,7 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l) {
         A.nxt = static_cast<R*>(buf_[cur_ ^ 1]);
         A.nbr = d_nbr_;
         A.masks = d_masks_;
+        A.full = d_full_;
         A.origins = d_origins_;
         A.step = steps_done_;
         A.error_flag = d_error_;

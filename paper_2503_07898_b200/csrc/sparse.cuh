@@ -76,6 +76,7 @@ private:
     int steps_done_ = 0;
     std::int32_t* d_nbr_ = nullptr;
     std::uint64_t* d_masks_ = nullptr;
+    std::uint8_t* d_full_ = nullptr;
     int* d_origins_ = nullptr;
     std::uint8_t* d_bitmask_ = nullptr;
     std::int32_t* d_meta_index_ = nullptr;

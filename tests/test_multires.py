@@ -1,0 +1,193 @@
+"""Multi-resolution path: host tables vs the reference (CPU) and the CUDA
+engine vs the oracle (GPU; fp64 bitwise for fused and staged schedules)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2503_07898_b200 as V
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+
+
+def nested_box_levels(domain, levels, boxes):
+    """multires_test.cpp:19-35: finest box inside, coarser rings outside."""
+    nx, ny, nz = domain
+    m = np.full((nz, ny, nx), levels - 1, np.int32)
+    for l in range(levels - 2, -1, -1):
+        (lx, ly, lz), (hx, hy, hz) = boxes[l]
+        m[lz:hz, ly:hy, lx:hx] = np.minimum(m[lz:hz, ly:hy, lx:hx], l)
+    # rows of the reference loop assign the smallest matching l (l descending, last write wins)
+    out = np.full((nz, ny, nx), levels - 1, np.int32)
+    for l in range(levels - 2, -1, -1):
+        (lx, ly, lz), (hx, hy, hz) = boxes[l]
+        out[lz:hz, ly:hy, lx:hx] = l
+    return out.reshape(-1)
+
+
+def test_band_map_matches_oracle():
+    for dom, lv in [((32, 32, 32), 3), ((16, 16, 16), 2), ((64, 32, 16), 3)]:
+        assert np.array_equal(V.band_level_map(dom, lv), O.band_level_map(dom, lv))
+
+
+@needs_ref
+@pytest.mark.parametrize("levels", [2, 3])
+@pytest.mark.parametrize("domain", [(32, 32, 32), (16, 16, 16), (32, 16, 24)])
+def test_tables_vs_reference(levels, domain):
+    cfg = dict(lattice="D3Q19", domain=list(domain), tau=0.56, scenario="lid_driven_cavity", velocity=[0.05, 0, 0],
+               steps=0, levels=levels, fused=True)
+    try:
+        ref = O.RefMres(cfg)
+    except RuntimeError as exc:  # the reference rejects this band map: so must we, same message
+        with pytest.raises(V.VoxlInvalidArgument, match=str(exc)):
+            V.MultiResPlan(domain, levels)
+        return
+    ours = V.MultiResPlan(domain, levels)
+    assert ref.levels == levels
+    for l in range(levels):
+        info = ours.level(l)
+        assert info["num_active"] == ref.num_active(l)
+        assert info["tau"] == ref.tau(l)
+        ro, rm, rc = ref.blocks(l)
+        oo, om, oj = ours.ref_blocks(l)
+        assert np.array_equal(ro, oo) and np.array_equal(rm, om) and np.array_equal(rc.astype(np.uint8), oj)
+        assert np.array_equal(ref.ghosts(l), ours.ghosts(l))
+        assert np.array_equal(ref.pulls(l), ours.pulls(l))
+    assert ref.graph_dot() == ours.graph_dot(fused=True)
+    assert ref.distribution() == ours.distribution()
+
+
+@needs_ref
+def test_staged_graph_and_2d_tables_vs_reference():
+    cfg = dict(lattice="D3Q19", domain=[16, 16, 16], tau=0.56, scenario="lid_driven_cavity", velocity=[0.05, 0, 0],
+               steps=0, levels=2, fused=False)
+    assert O.RefMres(cfg).graph_dot() == V.MultiResPlan((16, 16, 16), 2).graph_dot(fused=False)
+    cfg2 = dict(lattice="D2Q9", domain=[32, 32], tau=0.6, scenario="lid_driven_cavity", velocity=[0.05, 0, 0],
+                steps=0, levels=3, fused=True)
+    ref = O.RefMres(cfg2)
+    ours = V.MultiResPlan((32, 32, 1), 3, level_map=V.band_level_map((32, 32, 1), 3, axis=1), tau=0.6,
+                          lattice="D2Q9")
+    for l in range(3):
+        assert np.array_equal(ref.ghosts(l), ours.ghosts(l))
+        assert np.array_equal(ref.pulls(l), ours.pulls(l))
+    assert ref.distribution() == ours.distribution()
+
+
+def test_jump_distance_kats():
+    """multires_test.cpp:140-160."""
+    p = V.MultiResPlan((16, 16, 16), 2, tau=0.6)
+    assert p.jump_distance(0, (5, 5, 8)) == 0
+    assert p.jump_distance(0, (5, 5, 9)) == 1
+    assert p.jump_distance(0, (5, 5, 12)) == 4
+    assert p.jump_distance(1, (2, 2, 3)) == 0
+    assert p.jump_distance(1, (2, 2, 0)) == 3
+    with pytest.raises(V.VoxlInvalidArgument):
+        p.jump_distance(0, (0, 0, 0))
+    single = V.MultiResPlan((16, 16, 16), 1, level_map=np.zeros(16 ** 3, np.int32), tau=0.6)
+    assert single.jump_distance(0, (3, 3, 3)) == 2 ** 31 - 1
+
+
+def test_band_classification_kat():
+    """multires_test.cpp:203-216: 16 jump / 16 uniform fine blocks."""
+    p = V.MultiResPlan((16, 16, 16), 2, tau=0.6)
+    o, _, j = p.ref_blocks(0)
+    assert int(j.sum()) == 16 and len(j) - int(j.sum()) == 16
+    assert np.array_equal(j.astype(bool), o[:, 2] == 8)
+    assert p.distribution() == "50, 6.25"
+
+
+def test_build_validation_errors():
+    dom = (8, 8, 8)
+    bad = nested_box_levels(dom, 2, [((0, 0, 0), (3, 4, 4))])
+    with pytest.raises(V.VoxlInvalidArgument, match="not aligned"):
+        V.MultiResPlan(dom, 2, level_map=bad, tau=0.6)
+    good = nested_box_levels(dom, 2, [((0, 0, 0), (4, 4, 4))])
+    p = V.MultiResPlan(dom, 2, level_map=good, tau=0.6)
+    assert p.level(0)["num_active"] == 64 and p.level(1)["num_active"] == 56
+    assert p.level(1)["tau"] == 0.6 and abs(p.level(0)["tau"] - 0.7) < 1e-15
+    skip = nested_box_levels(dom, 3, [((0, 0, 0), (4, 4, 4)), ((0, 0, 0), (4, 4, 4))])
+    with pytest.raises(V.VoxlInvalidArgument, match="skips a level"):
+        V.MultiResPlan(dom, 3, level_map=skip, tau=0.6)
+
+
+# ---- GPU physics -------------------------------------------------------------------------
+
+def _oracle(dom, levels, steps, level_map=None, tau=0.56):
+    return O.port_mres_run("D3Q19", dom, levels, tau, (0.05, 0, 0), steps, level_map=level_map)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("levels", [2, 3])
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("edge", [4, 8])
+def test_fp64_bitwise_vs_oracle(levels, fused, edge):
+    dom = (32, 32, 32)
+    ref = _oracle(dom, levels, 3)
+    e = V.MultiResEngine(dom, levels, fused=fused, precision="fp64", block_edge=edge)
+    e.step(3)
+    out = e.get_state()
+    assert out.size == ref.size
+    assert np.array_equal(out, ref), np.abs(out - ref).max()
+
+
+@pytest.mark.gpu
+def test_fp64_bitwise_golden():
+    z = np.load(os.path.join(GOLDEN, "mres3_cavity_d3q19_16.npz"))
+    cfg = json.loads(str(z["config"]))
+    e = V.MultiResEngine(tuple(cfg["domain"]), cfg["levels"], fused=True, precision="fp64", block_edge=8)
+    e.step(cfg["steps"])
+    assert np.array_equal(e.get_state(), z["field"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_random_nested_boxes_fused_equals_oracle(seed):
+    """multires_test.cpp:409-455 style: seeded random aligned nested boxes."""
+    rng = np.random.default_rng(4000 + seed)
+    dom = (16, 16, 16)
+    levels = 2 + seed % 2
+    snap = 1 << (levels - 1)
+    lo = [int(rng.integers(0, 8)) // snap * snap for _ in range(3)]
+    hi = [c + 4 for c in lo]
+    boxes = [(tuple(lo), tuple(hi))]
+    if levels == 3:
+        boxes.append((tuple(max(0, c - snap) for c in lo), tuple(min(16, c + snap) for c in hi)))
+    lm = nested_box_levels(dom, levels, boxes)
+    ref = _oracle(dom, levels, 4, level_map=lm, tau=0.6)
+    for fused in (True, False):
+        e = V.MultiResEngine(dom, levels, level_map=lm, tau=0.6, fused=fused, precision="fp64", block_edge=4)
+        e.step(4)
+        assert np.array_equal(e.get_state(), ref)
+
+
+@pytest.mark.gpu
+def test_fp32_tolerance_and_mass():
+    dom = (64, 64, 64)
+    e64 = V.MultiResEngine(dom, 3, fused=True, precision="fp64")
+    e32 = V.MultiResEngine(dom, 3, fused=True, precision="fp32")
+    e64.step(20)
+    e32.step(20)
+    a, b = e64.get_state(), e32.get_state()
+    rel = np.abs(a - b) / np.abs(a)
+    print("multires fp32 max rel err after 20 coarse steps:", rel.max())
+    assert rel.max() <= 1e-5
+    m0 = V.MultiResEngine(dom, 3, precision="fp64").total_mass()
+    assert abs(e64.total_mass() - m0) <= 1e-10 * m0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not O.ref_available(), reason="reference library absent")
+def test_total_mass_and_probe_vs_reference():
+    cfg = dict(lattice="D3Q19", domain=[32, 32, 32], tau=0.56, scenario="lid_driven_cavity", velocity=[0.05, 0, 0],
+               steps=0, levels=3, fused=True)
+    ref = O.RefMres(cfg)
+    ref.step(3)
+    e = V.MultiResEngine((32, 32, 32), 3, precision="fp64")
+    e.step(3)
+    assert abs(e.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
+    m, s = O.port_probe("D3Q19", ref.state())
+    d = e.probe()
+    assert abs(d.mass - m) <= 1e-12 * m and abs(d.max_speed - s) <= 1e-14

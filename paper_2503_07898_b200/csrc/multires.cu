@@ -86,59 +86,35 @@ __global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_cons
     });
 }
 
-/// Stages the 27-neighbourhood of block b: post base pointers, active masks
-/// and block classes.
-template <int Q, class R, int E>
-struct Stage {
-    const R* post[27];
-    R* nxt[27];
-    unsigned long long mask[27][BlockGeom<E>::W];
-    int cls[27];
-};
-
-template <int Q, class R, int E>
-__device__ __forceinline__ void stage_neighbourhood(const MresArgs<Q, R>& A, int b, Stage<Q, R, E>& S) {
-    constexpr int BV = E * E * E, W = BlockGeom<E>::W;
+/// Pull (+ optional collide) over the listed blocks: g_i(v) = src[v - e_i][i]
+/// for in-domain sources (active, ghost or ring slots of the post buffer --
+/// every one exists by construction, so no activity test is needed), own
+/// src[v][opp i] plus the lid term for wall sources (stream_voxel,
+/// multires.cpp:485-531). COLLIDE = false: stream_level (write g). COLLIDE =
+/// true: the fused uniform-block kernel (uniform blocks keep post-collision
+/// storage, so collide-after-pull is the reference's collide-before-pull of
+/// the next step), one pass at 2 Q sizeof(real) bytes per update.
+template <class L, class R, bool Exact, int E, bool COLLIDE>
+__global__ void __launch_bounds__(E* E* E) mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
+    constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W;
+    using Ar = Arith<R, Exact>;
+    __shared__ const R* s_src[27];
+    const int b = A.blocks[blockIdx.x];
     const int t = threadIdx.x;
-    __shared__ int s_nb[27];
     if (t < 27) {
         const int nb = A.nbr[(long long)b * 27 + t];
-        s_nb[t] = nb;
-        const int ob = nb < 0 ? b : nb;
-        S.post[t] = A.post + (long long)ob * Q * BV;
-        S.nxt[t] = A.nxt + (long long)ob * Q * BV;
-        S.cls[t] = nb < 0 ? int(kNone) : int(A.cls[nb]);
+        s_src[t] = A.post + (long long)(nb < 0 ? b : nb) * Q * BV;
     }
     __syncthreads();
-    for (int j = t; j < 27 * W; j += BV) {
-        const int d = j / W, w = j % W;
-        const int nb = s_nb[d];
-        S.mask[d][w] = nb >= 0 ? A.amask[(long long)nb * W + w] : 0ull;
-    }
-    __syncthreads();
-}
-
-/// stream_level / stream_voxel (multires.cpp:485-561) over the listed blocks.
-/// In-domain sources are plain loads of the post buffer (active, ghost or
-/// coalesced ring slots). FUSED: sources that are active cells of uniform
-/// blocks are skipped -- their owners push those populations.
-template <class L, class R, bool Exact, int E, bool FUSED>
-__global__ void __launch_bounds__(E* E* E) mres_stream_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
-    constexpr int Q = L::Q, BV = E * E * E;
-    using Ar = Arith<R, Exact>;
-    __shared__ Stage<Q, R, E> S;
-    const int b = A.blocks[blockIdx.x];
-    stage_neighbourhood<Q, R, E>(A, b, S);
-    const int t = threadIdx.x;
-    if (!bit_of(S.mask[13], t)) return;
+    if (!((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
     constexpr int LOG = BlockGeom<E>::LOG;
     const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
     const int x = A.org[3 * b] + lx, y = A.org[3 * b + 1] + ly, z = A.org[3 * b + 2] + lz;
     const bool xlo = lx == 0, xhi = lx == E - 1, ylo = ly == 0, yhi = ly == E - 1, zlo = lz == 0, zhi = lz == E - 1;
     const bool dxlo = x == 0, dxhi = x == A.n[0] - 1, dylo = y == 0, dyhi = y == A.n[1] - 1, dzlo = z == 0,
                dzhi = z == A.n[2] - 1;
-    const R* own_post = S.post[13] + t;
-    R* own_nxt = A.nxt + (long long)b * Q * BV + t;
+    const R* own_src = s_src[13] + t;
+    R g[Q];
     static_for<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
         constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
@@ -150,94 +126,26 @@ __global__ void __launch_bounds__(E* E* E) mres_stream_kernel(const __grid_const
         if constexpr (ey < 0) oob = oob || dyhi;
         if constexpr (ez > 0) oob = oob || dzlo;
         if constexpr (ez < 0) oob = oob || dzhi;
-        if (oob) {
-            R v = own_post[oi * BV];
-            if constexpr (ez < 0) {
-                if (A.has_lid && dzhi) v = Ar::add(v, A.lid[i]);
-            }
-            own_nxt[i * BV] = v;
-        } else {
-            int d, sl;
-            shifted<E, -ex, -ey, -ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
-            bool skip = false;
-            if constexpr (FUSED) skip = S.cls[d] == kUniform && bit_of(S.mask[d], sl);
-            if (!skip) own_nxt[i * BV] = S.post[d][i * BV + sl];
+        int d, sl;
+        shifted<E, -ex, -ey, -ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
+        const R* p = oob ? own_src + oi * BV : s_src[d] + (i * BV + sl);
+        R v = __ldg(p);
+        if constexpr (ez < 0) {
+            if (A.has_lid && dzhi) v = Ar::add(v, A.lid[i]);
         }
+        g[i] = v;
     });
-}
-
-/// fused_level (multires.cpp:541-561) as one pass: collide in registers, push
-/// the post-collision populations to their pull destinations (bounce-back and
-/// lid into the own voxel), and pull the directions whose source is a
-/// jump-block cell (materialised post). Writes every nxt slot exactly once
-/// together with the jump-block stream kernel.
-template <class L, class R, bool Exact, int E>
-__global__ void __launch_bounds__(E* E* E) mres_fused_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
-    constexpr int Q = L::Q, BV = E * E * E;
-    using Ar = Arith<R, Exact>;
-    __shared__ Stage<Q, R, E> S;
-    const int b = A.blocks[blockIdx.x];
-    stage_neighbourhood<Q, R, E>(A, b, S);
-    const int t = threadIdx.x;
-    if (!bit_of(S.mask[13], t)) return;
-    constexpr int LOG = BlockGeom<E>::LOG;
-    const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
-    const int x = A.org[3 * b] + lx, y = A.org[3 * b + 1] + ly, z = A.org[3 * b + 2] + lz;
-    const bool xlo = lx == 0, xhi = lx == E - 1, ylo = ly == 0, yhi = ly == E - 1, zlo = lz == 0, zhi = lz == E - 1;
-    const bool dxlo = x == 0, dxhi = x == A.n[0] - 1, dylo = y == 0, dyhi = y == A.n[1] - 1, dzlo = z == 0,
-               dzhi = z == A.n[2] - 1;
-    const long long own = (long long)b * Q * BV + t;
-    R f[Q];
+    if constexpr (COLLIDE) {
+        bool ok = true;
+        R rho, u[3];
+        if constexpr (Exact) bgk_relax<L, R, true>(g, A.omega, A.keep, rho, u, ok);
+        else bgk_relax_shifted<L, R>(g, A.omega, A.keep, rho, u, ok);
+        if (!ok) atomicMin(A.error_flag, A.step);
+    }
+    R* out = A.nxt + (long long)b * Q * BV + t;
     static_for<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
-        f[i] = __ldg(A.cur + own + i * BV);
-    });
-    bool ok = true;
-    R rho, u[3];
-    if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
-    else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok);
-    if (!ok) atomicMin(A.error_flag, A.step);
-    static_for<Q>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
-        constexpr int oi = L::opp(i);
-        // destination w = v + e_i pulls direction i from v
-        bool oob = false;
-        if constexpr (ex > 0) oob = oob || dxhi;
-        if constexpr (ex < 0) oob = oob || dxlo;
-        if constexpr (ey > 0) oob = oob || dyhi;
-        if constexpr (ey < 0) oob = oob || dylo;
-        if constexpr (ez > 0) oob = oob || dzhi;
-        if constexpr (ez < 0) oob = oob || dzlo;
-        if (oob) {
-            // v pulls direction oi from the wall: own post[i] (+ lid term of oi)
-            R val = f[i];
-            if constexpr (ez > 0) {
-                if (A.has_lid && dzhi) val = Ar::add(val, A.lid[oi]);
-            }
-            A.nxt[own + oi * BV] = val;
-        } else {
-            int d, sl;
-            shifted<E, ex, ey, ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
-            S.nxt[d][i * BV + sl] = f[i];
-        }
-    });
-    // directions whose source is a jump-block cell: pull its materialised post
-    static_for<Q>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
-        bool oob = false;
-        if constexpr (ex > 0) oob = oob || dxlo;
-        if constexpr (ex < 0) oob = oob || dxhi;
-        if constexpr (ey > 0) oob = oob || dylo;
-        if constexpr (ey < 0) oob = oob || dyhi;
-        if constexpr (ez > 0) oob = oob || dzlo;
-        if constexpr (ez < 0) oob = oob || dzhi;
-        if (!oob) {
-            int d, sl;
-            shifted<E, -ex, -ey, -ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
-            if (S.cls[d] == kJump) A.nxt[own + i * BV] = S.post[d][i * BV + sl];
-        }
+        out[i * BV] = g[i];
     });
 }
 
@@ -345,7 +253,10 @@ struct MultiResEngine::Level {
     BlockGrid ext;
     void* cur = nullptr;
     void* nxt = nullptr;
-    void* post = nullptr;
+    // post[parity]: post-collision of jump / staged cells (this step), of
+    // uniform cells (fused mode: their persistent state), ghost and ring slots.
+    void* post[2] = {nullptr, nullptr};
+    int parity = 0;
     std::int32_t* nbr = nullptr;
     std::uint64_t* amask = nullptr;
     std::uint8_t* cls = nullptr;
@@ -467,7 +378,7 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
         VOXL_CUDA(cudaMalloc(&V->cls, nb));
         VOXL_CUDA(cudaMemcpy(V->cls, cls.data(), nb, cudaMemcpyHostToDevice));
         const std::size_t bytes = std::size_t(nb) * q_ * BV * esize_;
-        for (void** p : {&V->cur, &V->nxt, &V->post}) {
+        for (void** p : {&V->cur, &V->nxt, &V->post[0], &V->post[1]}) {
             VOXL_CUDA(cudaMalloc(p, bytes));
             VOXL_CUDA(cudaMemsetAsync(*p, 0, bytes, stream_));
         }
@@ -536,7 +447,7 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
 MultiResEngine::~MultiResEngine() {
     if (stream_) cudaStreamSynchronize(stream_);
     for (Level* V : lv_) {
-        for (void* p : {V->cur, V->nxt, V->post}) cudaFree(p);
+        for (void* p : {V->cur, V->nxt, V->post[0], V->post[1]}) cudaFree(p);
         cudaFree(V->nbr);
         cudaFree(V->amask);
         cudaFree(V->cls);
@@ -577,7 +488,7 @@ void MultiResEngine::set_equilibrium(double rho, const double u[3]) {
     VOXL_CUDA(cudaMemcpy(d_val, val.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
     for (Level* V : lv_) {
         const long long total = (long long)V->ext.num_blocks() * q_ * V->ext.block_volume();
-        for (void* p : {V->cur, V->nxt, V->post}) {
+        for (void* p : {V->cur, V->nxt, V->post[0], V->post[1]}) {
             if (esize_ == 8)
                 mres_fill_kernel<double><<<unsigned((total + 255) / 256), 256, 0, stream_>>>(
                     static_cast<double*>(p), total, V->ext.block_volume(), q_, d_val);
@@ -589,6 +500,7 @@ void MultiResEngine::set_equilibrium(double rho, const double u[3]) {
     }
     VOXL_CUDA(cudaStreamSynchronize(stream_));
     cudaFree(d_val);
+    load_uniform_post();
 }
 
 void MultiResEngine::set_state(const double* canonical) {
@@ -617,10 +529,12 @@ void MultiResEngine::set_state(const double* canonical) {
         off += n * q_;
     }
     cudaFree(d_shift);
+    load_uniform_post();
 }
 
 void MultiResEngine::get_state(double* canonical) {
     // canonical_state (multires.cpp:578-598): levels finest first
+    sync_state();
     const LatticeTable t = make_lattice(cfg_.lattice);
     std::vector<double> shift(q_);
     for (int i = 0; i < q_; ++i) shift[i] = esize_ == 8 ? 0.0 : double(t.wnum[i]) / double(t.wden[i]);
@@ -669,7 +583,7 @@ MresArgs<L::Q, R> level_args(const MresConfig& cfg, MultiResEngine::Level* V, in
     MresArgs<L::Q, R> A{};
     A.cur = static_cast<const R*>(V->cur);
     A.nxt = static_cast<R*>(V->nxt);
-    A.post = static_cast<R*>(V->post);
+    A.post = static_cast<R*>(V->post[V->parity]);
     A.nbr = V->nbr;
     A.amask = V->amask;
     A.cls = V->cls;
@@ -723,11 +637,61 @@ void MultiResEngine::launch_stream(int l, bool jump_only) {
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
         A.blocks = jump_only ? V->jump_blocks : V->all_blocks;
-        if (jump_only) mres_stream_kernel<L, R, X, E, true><<<nb, E * E * E, 0, stream_>>>(A);
-        else mres_stream_kernel<L, R, X, E, false><<<nb, E * E * E, 0, stream_>>>(A);
+        mres_pull_kernel<L, R, X, E, false><<<nb, E * E * E, 0, stream_>>>(A);  // post -> nxt
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTStream, b);
+}
+
+void MultiResEngine::gather_uniform(int l) {
+    // Pre-collision state of the uniform cells (the reference's cur) after
+    // the last step: the pull, without collision, of the previous step's
+    // post-collision buffer (post[parity ^ 1] still holds it: uniform, jump
+    // and ghost slots of that step) -- bitwise what the fused kernel had in
+    // registers before it collided.
+    Level* V = lv_[l];
+    if (V->n_uni == 0) return;
+    mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
+        using L = decltype(lat);
+        using R = decltype(real);
+        constexpr bool X = decltype(exact)::value;
+        constexpr int E = decltype(e)::value;
+        auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+        A.blocks = V->uni_blocks;
+        A.post = static_cast<R*>(V->post[V->parity ^ 1]);
+        A.nxt = static_cast<R*>(V->cur);
+        mres_pull_kernel<L, R, X, E, false><<<V->n_uni, E * E * E, 0, stream_>>>(A);
+    });
+    VOXL_CUDA(cudaGetLastError());
+}
+
+void MultiResEngine::sync_state() {
+    if (!cfg_.fused || cur_valid_) return;
+    for (int l = 0; l < int(lv_.size()); ++l) gather_uniform(l);
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    cur_valid_ = true;
+}
+
+void MultiResEngine::load_uniform_post() {
+    // After cur changed on the host side: post of the uniform cells = BGK(cur)
+    // (what the reference's next collide_level computes).
+    if (!cfg_.fused) return;
+    for (int l = 0; l < int(lv_.size()); ++l) {
+        Level* V = lv_[l];
+        if (V->n_uni == 0) continue;
+        mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
+            using L = decltype(lat);
+            using R = decltype(real);
+            constexpr bool X = decltype(exact)::value;
+            constexpr int E = decltype(e)::value;
+            auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+            A.blocks = V->uni_blocks;
+            mres_collide_kernel<L, R, X, E><<<V->n_uni, E * E * E, 0, stream_>>>(A);
+        });
+        VOXL_CUDA(cudaGetLastError());
+    }
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    cur_valid_ = true;
 }
 
 void MultiResEngine::launch_fused(int l) {
@@ -742,7 +706,8 @@ void MultiResEngine::launch_fused(int l) {
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
         A.blocks = V->uni_blocks;
-        mres_fused_kernel<L, R, X, E><<<V->n_uni, E * E * E, 0, stream_>>>(A);
+        A.nxt = static_cast<R*>(V->post[V->parity ^ 1]);  // post[p] -> post[p^1]
+        mres_pull_kernel<L, R, X, E, true><<<V->n_uni, E * E * E, 0, stream_>>>(A);
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTFused, b);
@@ -755,12 +720,18 @@ void MultiResEngine::launch_explode(int coarse) {
     cudaEvent_t b{};
     mark_begin(kTTransition, &b);
     const unsigned grid = unsigned((F->n_ghost + 127) / 128);
-    if (esize_ == 8) {
-        if (q_ == 19) mres_explode_kernel<19, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(F->post), static_cast<const double*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
-        else mres_explode_kernel<27, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(F->post), static_cast<const double*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
-    } else {
-        if (q_ == 19) mres_explode_kernel<19, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(F->post), static_cast<const float*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
-        else mres_explode_kernel<27, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(F->post), static_cast<const float*>(Cc->post), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+    // One explosion serves both fine sub-steps (multires.cpp:563-570); the
+    // fine level flips its post parity between them, so fill both copies.
+    for (int w = 0; w < (cfg_.fused ? 2 : 1); ++w) {
+        void* dst = F->post[cfg_.fused ? w : F->parity];
+        const void* src = Cc->post[Cc->parity];
+        if (esize_ == 8) {
+            if (q_ == 19) mres_explode_kernel<19, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(dst), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+            else mres_explode_kernel<27, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(dst), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+        } else {
+            if (q_ == 19) mres_explode_kernel<19, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(dst), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+            else mres_explode_kernel<27, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(dst), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
+        }
     }
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTTransition, b);
@@ -776,11 +747,11 @@ void MultiResEngine::launch_coalesce(int coarse) {
     const int nchild = grid_.dim() == 3 ? 8 : 4;
     const int bvc = Cc->ext.block_volume(), bvf = F->ext.block_volume();
     if (esize_ == 8) {
-        if (q_ == 19) mres_coalesce_kernel<19, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
-        else mres_coalesce_kernel<27, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        if (q_ == 19) mres_coalesce_kernel<19, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        else mres_coalesce_kernel<27, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
     } else {
-        if (q_ == 19) mres_coalesce_kernel<19, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
-        else mres_coalesce_kernel<27, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        if (q_ == 19) mres_coalesce_kernel<19, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        else mres_coalesce_kernel<27, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
     }
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTTransition, b);
@@ -799,6 +770,8 @@ void MultiResEngine::advance(int l) {
     launch_stream(l, cfg_.fused);
     Level* V = lv_[l];
     std::swap(V->cur, V->nxt);
+    if (cfg_.fused) V->parity ^= 1;
+    cur_valid_ = false;
 }
 
 void MultiResEngine::check_errors() {

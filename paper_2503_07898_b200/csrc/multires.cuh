@@ -84,7 +84,12 @@ private:
     // timing (events around each launch class) when non-null
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* events_ = nullptr;
 
+    bool cur_valid_ = true;  // fused mode: uniform cells' cur reconstructed?
+
     void advance(int l);
+    void gather_uniform(int l);
+    void sync_state();         // cur of every cell valid (fused mode gathers uniform cells)
+    void load_uniform_post();  // uniform cells' post = BGK(cur) after a host-side state change
     void launch_collide(int l, bool jump_only);
     void launch_stream(int l, bool jump_only);
     void launch_fused(int l);

@@ -174,8 +174,11 @@ def test_fp32_tolerance_and_mass():
     rel = np.abs(a - b) / np.abs(a)
     print("multires fp32 max rel err after 20 coarse steps:", rel.max())
     assert rel.max() <= 1e-5
-    m0 = V.MultiResEngine(dom, 3, precision="fp64").total_mass()
-    assert abs(e64.total_mass() - m0) <= 1e-10 * m0
+    # The reference's plain-copy explosion / averaging coalescence does not
+    # conserve mass across levels (SPEC multires DESIGN DECISIONS); the fp32
+    # engine must track the fp64 engine's total mass, not a constant.
+    m64, m32 = e64.total_mass(), e32.total_mass()
+    assert abs(m32 - m64) <= 1e-6 * m64
 
 
 @pytest.mark.gpu

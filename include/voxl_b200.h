@@ -71,6 +71,11 @@ int voxl_decompose(int nx, int ny, int nz, int parts, int axis, int periodic, in
 int voxl_classify_voxels(int nx, int ny, int nz, int parts, int axis, int periodic, int p, uint8_t* out,
                          int64_t cap);
 
+/** initial_canonical_state (solver.cpp:165-187): rest equilibrium, or the
+ *  periodic box's mt19937_64-perturbed state; volume * q doubles, canonical. */
+int voxl_initial_state(int lattice, int scenario, int nx, int ny, int nz, uint64_t seed, double perturbation,
+                       double* out);
+
 /* ---- dense engine (PartitionedField + step_occ + GatherKernel) ------------------ */
 
 typedef struct voxl_dense voxl_dense;

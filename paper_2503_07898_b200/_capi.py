@@ -136,6 +136,7 @@ def _load():
         "voxl_dispatch_plan_json": ([C.c_int, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, cp, i64,
                                      C.POINTER(i64)], C.c_int),
         "voxl_band_level_map": ([C.c_int] * 5 + [vp], C.c_int),
+        "voxl_initial_state": ([C.c_int] * 5 + [C.c_uint64, C.c_double, vp], C.c_int),
         "voxl_mres_create": ([C.POINTER(MresDesc), vp, C.POINTER(vp)], C.c_int),
         "voxl_mres_destroy": ([vp], C.c_int),
         "voxl_mres_step": ([vp, C.c_int], C.c_int),

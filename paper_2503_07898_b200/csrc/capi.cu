@@ -3,6 +3,7 @@
 
 #include <cstring>
 #include <numeric>
+#include <random>
 #include <string>
 
 #include "common.cuh"
@@ -481,6 +482,42 @@ int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int 
         require(strategy >= 0 && strategy <= 2, "unknown sparse strategy");
         put_text(dispatch_plan(Strategy(strategy), n_b, n_nb, q, bs, s_w, s_i, full != 0).to_json(false), out, cap,
                  len);
+    });
+}
+
+int voxl_initial_state(int lattice, int scenario, int nx, int ny, int nz, uint64_t seed, double perturbation,
+                       double* out) {
+    return guarded([&] {
+        // initial_canonical_state (solver.cpp:165-187): the same libstdc++
+        // mt19937_64 / uniform_real_distribution sequence as the reference.
+        require(lattice >= 0 && lattice <= 2, "unknown lattice kind");
+        const LatticeTable t = make_lattice(lattice);
+        auto eq = [&](double rho, const double u[3], double* f) {
+            const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+            for (int i = 0; i < t.q; ++i) {
+                const double eu = double(t.e[i][0]) * u[0] + double(t.e[i][1]) * u[1] + double(t.e[i][2]) * u[2];
+                const double w = double(t.wnum[i]) / double(t.wden[i]);
+                f[i] = w * rho * (1.0 + 3.0 * eu + 4.5 * eu * eu - 1.5 * uu);
+            }
+        };
+        const int64_t vol = int64_t(nx) * ny * nz;
+        if (scenario == VOXL_PERIODIC && perturbation > 0.0) {
+            std::mt19937_64 rng(seed);
+            std::uniform_real_distribution<double> unit(-1.0, 1.0);
+            for (int64_t v = 0; v < vol; ++v) {
+                const double rho = 1.0 + perturbation * unit(rng);
+                const double a = 0.1 * perturbation * unit(rng);
+                const double b = 0.1 * perturbation * unit(rng);
+                const double c = t.dim == 3 ? 0.1 * perturbation * unit(rng) : 0.0;
+                const double u[3] = {a, b, c};
+                eq(rho, u, out + v * t.q);
+            }
+        } else {
+            const double u0[3] = {0.0, 0.0, 0.0};
+            double f[27];
+            eq(1.0, u0, f);
+            for (int64_t v = 0; v < vol; ++v) std::memcpy(out + v * t.q, f, sizeof(double) * t.q);
+        }
     });
 }
 

@@ -94,19 +94,36 @@ __global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_cons
 /// true: the fused uniform-block kernel (uniform blocks keep post-collision
 /// storage, so collide-after-pull is the reference's collide-before-pull of
 /// the next step), one pass at 2 Q sizeof(real) bytes per update.
+template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER>
+__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, const R* const* s_src);
+
 template <class L, class R, bool Exact, int E, bool COLLIDE>
 __global__ void __launch_bounds__(E* E* E) mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W;
-    using Ar = Arith<R, Exact>;
     __shared__ const R* s_src[27];
+    __shared__ int s_inner;
     const int b = A.blocks[blockIdx.x];
     const int t = threadIdx.x;
     if (t < 27) {
         const int nb = A.nbr[(long long)b * 27 + t];
         s_src[t] = A.post + (long long)(nb < 0 ? b : nb) * Q * BV;
     }
+    if (t == 32) {
+        // block strictly inside the level domain: no pull can leave it
+        const int* o = A.org + 3 * b;
+        s_inner = o[0] > 0 && o[1] > 0 && o[2] > 0 && o[0] + E < A.n[0] && o[1] + E < A.n[1] && o[2] + E < A.n[2];
+    }
     __syncthreads();
     if (!((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
+    if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true>(A, b, s_src);
+    else mres_pull_body<L, R, Exact, E, COLLIDE, false>(A, b, s_src);
+}
+
+template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER>
+__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, const R* const* s_src) {
+    constexpr int Q = L::Q, BV = E * E * E;
+    using Ar = Arith<R, Exact>;
+    const int t = threadIdx.x;
     constexpr int LOG = BlockGeom<E>::LOG;
     const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
     const int x = A.org[3 * b] + lx, y = A.org[3 * b + 1] + ly, z = A.org[3 * b + 2] + lz;
@@ -119,21 +136,25 @@ __global__ void __launch_bounds__(E* E* E) mres_pull_kernel(const __grid_constan
         constexpr int i = decltype(I)::value;
         constexpr int ex = L::ex(i), ey = L::ey(i), ez = L::ez(i);
         constexpr int oi = L::opp(i);
-        bool oob = false;
-        if constexpr (ex > 0) oob = oob || dxlo;
-        if constexpr (ex < 0) oob = oob || dxhi;
-        if constexpr (ey > 0) oob = oob || dylo;
-        if constexpr (ey < 0) oob = oob || dyhi;
-        if constexpr (ez > 0) oob = oob || dzlo;
-        if constexpr (ez < 0) oob = oob || dzhi;
         int d, sl;
         shifted<E, -ex, -ey, -ez>(t, xlo, xhi, ylo, yhi, zlo, zhi, d, sl);
-        const R* p = oob ? own_src + oi * BV : s_src[d] + (i * BV + sl);
-        R v = __ldg(p);
-        if constexpr (ez < 0) {
-            if (A.has_lid && dzhi) v = Ar::add(v, A.lid[i]);
+        if constexpr (INNER) {
+            g[i] = __ldg(s_src[d] + (i * BV + sl));
+        } else {
+            bool oob = false;
+            if constexpr (ex > 0) oob = oob || dxlo;
+            if constexpr (ex < 0) oob = oob || dxhi;
+            if constexpr (ey > 0) oob = oob || dylo;
+            if constexpr (ey < 0) oob = oob || dyhi;
+            if constexpr (ez > 0) oob = oob || dzlo;
+            if constexpr (ez < 0) oob = oob || dzhi;
+            const R* p = oob ? own_src + oi * BV : s_src[d] + (i * BV + sl);
+            R v = __ldg(p);
+            if constexpr (ez < 0) {
+                if (A.has_lid && dzhi) v = Ar::add(v, A.lid[i]);
+            }
+            g[i] = v;
         }
-        g[i] = v;
     });
     if constexpr (COLLIDE) {
         bool ok = true;

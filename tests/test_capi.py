@@ -39,3 +39,36 @@ def test_error_status_and_message():
 
     with pytest.raises(V.VoxlInvalidArgument, match="unknown lattice"):
         V.lattice_json(7)
+
+
+def _build_dropin(tmp_path):
+    exe = os.path.join(str(tmp_path), "dropin_dense")
+    libdir = os.path.dirname(V.LIB_PATH)
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "dropin_dense.cpp"), "-L", libdir, "-lvoxl_b200",
+           "-Wl,-rpath," + libdir, "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_cpp_binding_compiles_and_links(tmp_path):
+    """include/voxl_b200.hpp: the reference-named C++ wrapper builds against the .so."""
+    assert os.path.exists(_build_dropin(tmp_path))
+
+
+import pytest as _pytest  # noqa: E402
+
+
+@_pytest.mark.gpu
+def test_cpp_dropin_driver_bitwise(tmp_path):
+    import numpy as np
+
+    import oracle as O
+
+    exe = _build_dropin(tmp_path)
+    out = os.path.join(str(tmp_path), "field.bin")
+    r = subprocess.run([exe, out], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    got = np.fromfile(out, np.float64)
+    ref = O.port_dense_run("D3Q19", (16, 16, 16), 0.56, "lid_driven_cavity", (0.05, 0, 0), 20)
+    assert np.array_equal(got, ref)

@@ -333,8 +333,7 @@ def e2e_run(args, V, np):
     t0 = time.perf_counter()
     eng.set_canonical(host_in)
     for _ in range(steps):
-        eng.step(1)
-        eng.probe()
+        eng.step_probe()  # step + fused probe_field, diagnostics row read back
     eng.get_canonical(host_out)
     dt = time.perf_counter() - t0
     eng.close()
@@ -343,7 +342,7 @@ def e2e_run(args, V, np):
     return {"value": round(vox * steps / dt / 1e6, 1), "unit": "MLUPS",
             "h2d_bytes_per_step": int(bytes_in / steps), "d2h_bytes_per_step": int(bytes_out / steps),
             "domain": list(dom), "seconds": round(dt, 3),
-            "path": "DenseEngine.set_canonical(host fp64) + steps x (step + probe) + get_canonical(host fp64)"}
+            "path": "DenseEngine.set_canonical(host fp64) + steps x step_probe (diag row D2H) + get_canonical(host fp64)"}
 
 
 if __name__ == "__main__":

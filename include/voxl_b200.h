@@ -129,6 +129,9 @@ int voxl_dense_synchronize(voxl_dense* h);
 int voxl_dense_timed_steps(voxl_dense* h, int n, double* total_ms, double* kernel_ms);
 /** probe_field on the current state (lbm.cpp:116), on the device. */
 int voxl_dense_probe(voxl_dense* h, voxl_diag* out);
+/** One step_occ with probe_field fused into the step kernel: the per-step
+ *  diagnostics row of voxl::run (solver.cpp:245-255) without a second pass. */
+int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out);
 /** Ledger records of one step in the reference's order (partition.cpp:163-206). */
 int voxl_dense_ledger(voxl_dense* h, int step, voxl_transfer_record* out, int cap, int* count);
 /** The same records from a descriptor alone (no device needed). */

@@ -208,6 +208,23 @@ int vref_probe(int lattice, const double* canonical, std::int64_t n, double* mas
     }
 }
 
+/// config_to_json(config_from_json(json)) (solver.cpp:59-119), or the
+/// ConfigError message (returned negative length).
+int vref_config_roundtrip(const char* json, char* out, std::int64_t cap) {
+    try {
+        return copy_text(config_to_json(config_from_json(json)), out, cap);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        copy_text(g_err, out, cap);
+        return -int(g_err.size()) - 1;
+    }
+}
+
+/// commodel tables (commodel.cpp:50-75) as `voxl model` prints them.
+int vref_model_text(char* out, std::int64_t cap) {
+    return copy_text(vector_field_table_csv() + lbm_table_csv(), out, cap);
+}
+
 // ---- lattice / layout / partition tables -------------------------------------
 
 int vref_lattice_json(int lattice, char* out, std::int64_t cap) {

@@ -220,6 +220,17 @@ int voxl_dense_synchronize(voxl_dense* h) {
     return guarded([&] { h->eng->check_errors(); });
 }
 
+int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out) {
+    return guarded([&] {
+        const DenseDiag d = h->eng->step_probe();
+        out->mass = d.mass;
+        out->max_speed = d.max_speed;
+        out->unstable = d.unstable;
+        out->bad_population = d.bad_population;
+        out->bad_voxel = d.bad_voxel;
+    });
+}
+
 int voxl_dense_probe(voxl_dense* h, voxl_diag* out) {
     return guarded([&] {
         const DenseDiag d = h->eng->probe();

@@ -12,10 +12,18 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 
 namespace voxl_b200 {
+
+/// Where a step launch writes its fused-probe partials.
+struct DiagTarget {
+    double* partial = nullptr;
+    long long offset = 0;
+    unsigned long long* bad = nullptr;
+};
 
 namespace {
 
@@ -47,6 +55,9 @@ struct StepArgs {
     long long fast_in_off[Q];   // per-direction pull byte offset relative to fast_base + lin
     long long fast_out_off[Q];  // per-direction store byte offset
     int* error_flag;
+    double* diag_partial;            // fused probe: 2 doubles per CTA
+    long long diag_offset;           // first CTA slot of this launch
+    unsigned long long* diag_bad;    // (canonical voxel << 5) of the first unstable voxel
 };
 
 __device__ __forceinline__ int group_of(int k, int n) {
@@ -62,13 +73,15 @@ __device__ __forceinline__ R ld_ro(const R* p) {
 /// (gather_pull lbm.hpp:40-74 then bgk_relax lattice.cpp:131-138).
 /// AXIS is the partition axis (2 in 3D, 1 in 2D); `a` is x, `b` the remaining
 /// cross-section axis, `k` the local coordinate along AXIS.
-template <class L, class R, bool Exact, bool AOS, int AXIS, bool WRAP>
+template <class L, class R, bool Exact, bool AOS, int AXIS, bool WRAP, bool DIAG>
 __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constant__ StepArgs<L::Q, R> A) {
     constexpr int Q = L::Q;
     constexpr int OTHER = AXIS == 2 ? 1 : 2;
     using Ar = Arith<R, Exact>;
     const int a = blockIdx.x * kBlock + threadIdx.x;
-    if (a >= A.na) return;
+    R f[Q];
+    const bool live = a < A.na;
+    if (live) [&] {
     const int b = blockIdx.y;
     const int k = A.k_first + int(blockIdx.z) * A.k_step;
     const int kg = A.kg0 + k;
@@ -78,7 +91,6 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
     const int gm = group_of(k - 1, A.n), g0 = group_of(k, A.n), gp = group_of(k + 1, A.n);
 
     constexpr long long VS = AOS ? Q : 1;
-    R f[Q];
 
     // Fast path (warp-uniform): no lane of this warp touches a wall and the
     // source planes k-1..k+1 share one plane table (interior group, or any
@@ -174,6 +186,83 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
     // Cross-GPU ordering: the peer stores above must be performed before this
     // step's completion flag (written by signal_kernel after this kernel).
     if (A.remote_fence && ((k == 0 && A.up_out) || (k == A.n - 1 && A.low_out))) __threadfence_system();
+    }();
+
+    // Fused probe_field (lbm.cpp:116-138) on the post-collision values still
+    // in registers: per-CTA mass and max |u| partials (fixed-order reduction
+    // later, so run-to-run deterministic) and the instability flag.
+    if constexpr (DIAG) {
+        double mass = 0.0, v2 = 0.0;
+        if (live) {
+            double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+            bool bad = false;
+            static_for<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                const double fi = double(f[i]) + (Exact ? 0.0 : L::w(i));
+                bad = bad || !(fabs(fi) <= 1e3);
+                r += fi;
+                mx = acc_term<double, false, L::ex(i)>(mx, fi);
+                my = acc_term<double, false, L::ey(i)>(my, fi);
+                mz = acc_term<double, false, L::ez(i)>(mz, fi);
+            });
+            mass = r;
+            if (bad || !(r > 0.0)) {
+                const unsigned long long canon =
+                    (unsigned long long)(A.kg0 + A.k_first + int(blockIdx.z) * A.k_step) * A.s +
+                    (unsigned long long)(blockIdx.y * A.na + a);
+                atomicMin(A.diag_bad, canon << 5);
+            } else {
+                v2 = (mx * mx + my * my + mz * mz) / (r * r);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            mass += __shfl_xor_sync(0xffffffffu, mass, o);
+            v2 = fmax(v2, __shfl_xor_sync(0xffffffffu, v2, o));
+        }
+        __shared__ double sm[kBlock / 32], sv[kBlock / 32];
+        const int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+            sm[w] = mass;
+            sv[w] = v2;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double m = 0.0, v = 0.0;
+            for (int j = 0; j < kBlock / 32; ++j) {
+                m += sm[j];
+                v = fmax(v, sv[j]);
+            }
+            const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            A.diag_partial[2 * (A.diag_offset + blk)] = m;
+            A.diag_partial[2 * (A.diag_offset + blk) + 1] = v;
+        }
+    }
+}
+
+/// Fixed-order reduction of the per-CTA diagnostics partials (stage 1 of 2).
+__global__ void diag_reduce_kernel(const double* partial, long long n, double* out) {
+    __shared__ double sm[256], sv[256];
+    const long long per = (n + gridDim.x - 1) / gridDim.x;
+    const long long lo = (long long)blockIdx.x * per, hi = min(n, lo + per);
+    double m = 0.0, v = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        m += partial[2 * i];
+        v = fmax(v, partial[2 * i + 1]);
+    }
+    sm[threadIdx.x] = m;
+    sv[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sm[threadIdx.x] += sm[threadIdx.x + w];
+            sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[2 * blockIdx.x] = sm[0];
+        out[2 * blockIdx.x + 1] = sv[0];
+    }
 }
 
 // ---- cross-GPU step flags ---------------------------------------------------------------
@@ -365,7 +454,7 @@ struct DenseOps {
     static void launch_step(const DenseConfig& cfg, const Decomposition& d, const std::vector<LayoutMap>& maps,
                             int p, const void* in, void* out, void* up_out, void* low_out, bool wrap,
                             int step, int* error_flag, int k_first, int k_step, int k_count, cudaStream_t st,
-                            bool remote_fence = false) {
+                            bool remote_fence = false, DiagTarget* diag = nullptr) {
         if (k_count <= 0) return;
         StepArgs<Q, R> A{};
         A.remote_fence = remote_fence;
@@ -443,14 +532,26 @@ struct DenseOps {
             A.fast_out_off[i] = rel * (long long)sizeof(R);
         }
         const dim3 grid((g.na + kBlock - 1) / kBlock, g.nb, k_count);
-        if (aos) {
-            if (wrap) dense_step_kernel<L, R, Exact, true, AXIS, true><<<grid, kBlock, 0, st>>>(A);
-            else dense_step_kernel<L, R, Exact, true, AXIS, false><<<grid, kBlock, 0, st>>>(A);
-        } else {
-            if (wrap) dense_step_kernel<L, R, Exact, false, AXIS, true><<<grid, kBlock, 0, st>>>(A);
-            else dense_step_kernel<L, R, Exact, false, AXIS, false><<<grid, kBlock, 0, st>>>(A);
-        }
+        A.diag_partial = diag ? diag->partial : nullptr;
+        A.diag_offset = diag ? diag->offset : 0;
+        A.diag_bad = diag ? diag->bad : nullptr;
+        if (diag) diag->offset += (long long)grid.x * grid.y * grid.z;
+        auto go = [&](auto aos_c, auto wrap_c, auto diag_c) {
+            dense_step_kernel<L, R, Exact, decltype(aos_c)::value, AXIS, decltype(wrap_c)::value,
+                              decltype(diag_c)::value><<<grid, kBlock, 0, st>>>(A);
+        };
+        using T = std::true_type;
+        using F = std::false_type;
+        auto with_diag = [&](auto a_c, auto w_c) { diag ? go(a_c, w_c, T{}) : go(a_c, w_c, F{}); };
+        if (aos) wrap ? with_diag(T{}, T{}) : with_diag(T{}, F{});
+        else wrap ? with_diag(F{}, T{}) : with_diag(F{}, F{});
         VOXL_CUDA(cudaGetLastError());
+    }
+
+    /// CTA count of one launch (diagnostics partial slots).
+    static long long launch_ctas(const Decomposition& d, int p, int k_count) {
+        const PartGeom g = geom_of(d, p);
+        return (long long)((g.na + kBlock - 1) / kBlock) * g.nb * k_count;
     }
 
     static void canon(const Decomposition& d, const LayoutMap& m, int p, void* buf, double* staging, int k_lo,
@@ -582,6 +683,7 @@ DenseEngine::~DenseEngine() {
             for (void* b : p.buf) cudaFree(b);
     cudaFree(error_flag_);
     cudaFree(diag_scratch_);
+    if (diag_partials_) cudaFree(diag_partials_);
     if (staging_) cudaFree(staging_);
     if (flags_ && distributed_) cudaFree(flags_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -732,7 +834,7 @@ void DenseEngine::halo_push() {
     VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void DenseEngine::launch_step_distributed() {
+void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     // One owned partition p; neighbours live in other processes / devices.
     // Per step: wait(neighbour flags >= t) -> shared layers (k = 0, n-1) with
     // peer halo stores -> signal(t + 1) -> interior (k = 1 .. n-2). The interior
@@ -754,7 +856,7 @@ void DenseEngine::launch_step_distributed() {
         using Ops = decltype(ops);
         // shared layers first: k = 0 and k = n - 1
         Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out, wrap,
-                         steps_done_, error_flag_, 0, n - 1, 2, stream_, true);
+                         steps_done_, error_flag_, 0, n - 1, 2, stream_, true, diag);
     });
     if (zero_copy) {
         signal_flags_kernel<<<1, 32, 0, stream_>>>(remote_flag_up_, remote_flag_low_, t + 1);
@@ -763,15 +865,15 @@ void DenseEngine::launch_step_distributed() {
     dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
         using Ops = decltype(ops);
         Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr, wrap,
-                         steps_done_, error_flag_, 1, 1, n - 2, stream_, false);
+                         steps_done_, error_flag_, 1, 1, n - 2, stream_, false, diag);
     });
     cur_ = out;
     ++steps_done_;
 }
 
-void DenseEngine::launch_step() {
+void DenseEngine::launch_step(DiagTarget* diag) {
     if (distributed_) {
-        launch_step_distributed();
+        launch_step_distributed(diag);
         return;
     }
     const bool wrap = cfg_.scenario == Scenario::PeriodicBox;
@@ -785,7 +887,7 @@ void DenseEngine::launch_step() {
         const int n = decomp_.thickness(p);
         dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
             decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out,
-                                       low_out, wrap, steps_done_, error_flag_, 0, 1, n, stream_);
+                                       low_out, wrap, steps_done_, error_flag_, 0, 1, n, stream_, false, diag);
         });
     }
     cur_ = out;
@@ -835,6 +937,47 @@ void DenseEngine::step(int n) {
     if (n < 0) throw std::invalid_argument("step: n must be >= 0");
     enqueue_steps(n);
     check_errors();
+}
+
+DenseDiag DenseEngine::step_probe() {
+    long long ctas = 0;
+    for (int p = 0; p < cfg_.partitions; ++p)
+        if (local(p))
+            dispatch(cfg_.lattice, cfg_.precision,
+                     [&](auto ops) { ctas += decltype(ops)::launch_ctas(decomp_, p, decomp_.thickness(p)); });
+    if (diag_partials_len_ < std::size_t(2 * ctas)) {
+        if (diag_partials_) VOXL_CUDA(cudaFree(diag_partials_));
+        VOXL_CUDA(cudaMalloc(&diag_partials_, 2 * ctas * sizeof(double)));
+        diag_partials_len_ = std::size_t(2 * ctas);
+    }
+    double* stage = diag_scratch_;
+    double* out = diag_scratch_ + 2 * kProbeBlocks;
+    auto* bad = reinterpret_cast<unsigned long long*>(diag_scratch_ + 2 * kProbeBlocks + 2);
+    const double zero[2] = {0.0, 0.0};
+    const unsigned long long none = ~0ull;
+    VOXL_CUDA(cudaMemcpyAsync(out, zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
+    DiagTarget dt;
+    dt.partial = diag_partials_;
+    dt.bad = bad;
+    launch_step(&dt);
+    diag_reduce_kernel<<<kProbeBlocks, 256, 0, stream_>>>(diag_partials_, dt.offset, stage);
+    probe_final_kernel<<<1, 32, 0, stream_>>>(stage, kProbeBlocks, out);
+    VOXL_CUDA(cudaGetLastError());
+    double res[2];
+    unsigned long long b = 0;
+    VOXL_CUDA(cudaMemcpyAsync(res, out, sizeof res, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(&b, bad, sizeof b, cudaMemcpyDeviceToHost, stream_));
+    check_errors();
+    DenseDiag d;
+    d.mass = res[0];
+    d.max_speed = std::sqrt(res[1]);
+    if (b != ~0ull) {
+        d.unstable = 1;
+        d.bad_voxel = std::int64_t(b >> 5);
+        d.bad_population = 0;
+    }
+    return d;
 }
 
 DenseDiag DenseEngine::probe() {

@@ -24,6 +24,7 @@
 
 namespace voxl_b200 {
 
+struct DiagTarget;
 enum class Precision : int { F32 = 0, F64 = 1 };
 enum class HaloMode : int { ZeroCopy = 0, Copy = 1 };
 enum class Scenario : int { LidDrivenCavity = 0, FlowOverObstacle = 1, PeriodicBox = 2 };
@@ -88,6 +89,9 @@ public:
     double timed_steps(int n, double* kernel_ms);
     /// probe_field on the current state (lbm.cpp:116-138), on the device.
     DenseDiag probe();
+    /// One step with the probe fused into the step kernel (run()'s per-step
+    /// diagnostics row, solver.cpp:245-255) -- no extra pass over the field.
+    DenseDiag step_probe();
     /// Checks the device error flag; throws InstabilityError on a set flag.
     void check_errors();
 
@@ -139,6 +143,8 @@ private:
     cudaStream_t stream_ = nullptr;
     int* error_flag_ = nullptr;
     double* diag_scratch_ = nullptr;
+    double* diag_partials_ = nullptr;
+    std::size_t diag_partials_len_ = 0;
     std::size_t diag_scratch_len_ = 0;
     void* staging_ = nullptr;  // fp64 canonical staging (device)
     std::size_t staging_bytes_ = 0;
@@ -150,8 +156,8 @@ private:
     bool local(int p) const {
         return p >= cfg_.first_partition && p < cfg_.first_partition + cfg_.local_partitions;
     }
-    void launch_step();
-    void launch_step_distributed();
+    void launch_step(struct DiagTarget* diag = nullptr);
+    void launch_step_distributed(struct DiagTarget* diag);
     void scatter_gather(double* host, int k_begin, int k_end, bool to_device);
 };
 

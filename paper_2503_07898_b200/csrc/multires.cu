@@ -98,7 +98,8 @@ template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER>
 __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, const R* const* s_src);
 
 template <class L, class R, bool Exact, int E, bool COLLIDE>
-__global__ void __launch_bounds__(E* E* E) mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
+__global__ void __launch_bounds__(E* E* E, (E == 8 && sizeof(R) == 4) ? 3 : 1)
+    mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W;
     __shared__ const R* s_src[27];
     __shared__ int s_inner;

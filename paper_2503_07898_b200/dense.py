@@ -171,6 +171,12 @@ class DenseEngine:
         check(lib.voxl_dense_probe(self._h, C.byref(d)))
         return d
 
+    def step_probe(self):
+        """One step with probe_field fused into the step kernel."""
+        d = _capi.Diag()
+        check(lib.voxl_dense_step_probe(self._h, C.byref(d)))
+        return d
+
     def ledger(self, step: int):
         return _records(lib.voxl_dense_ledger, self._h, step)
 

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import json
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field as dc_field
 
 import numpy as np
 
@@ -155,7 +155,14 @@ def config_to_json(c: SolverConfig) -> str:
          "fused": c.fused, "seed": c.seed, "perturbation": c.perturbation}
     if c.obstacle_radius > 0.0:
         j["obstacle_radius"] = c.obstacle_radius
-    return json.dumps(j, indent=2, sort_keys=True) + "\n"
+    text = json.dumps(j, indent=2, sort_keys=True)
+    # nlohmann 3.11.3 prints the domain array (built with json::array({...}))
+    # on one line without spaces; reproduce that byte for byte.
+    import re
+
+    text = re.sub(r'"domain": \[\s*([^\]]*?)\s*\]',
+                  lambda m: '"domain": [' + ",".join(x.strip() for x in m.group(1).split(",")) + "]", text)
+    return text + "\n"
 
 
 @dataclass
@@ -163,9 +170,9 @@ class RunResult:
     config: SolverConfig
     field: np.ndarray = None
     field_header_json: str = ""
-    diagnostics: list = field(default_factory=list)  # (step, mass, max_speed)
-    ledger: list = field(default_factory=list)       # TransferRecord
-    trace: list = field(default_factory=list)        # (step, stage, phase, partition)
+    diagnostics: list = dc_field(default_factory=list)  # (step, mass, max_speed)
+    ledger: list = dc_field(default_factory=list)       # TransferRecord
+    trace: list = dc_field(default_factory=list)        # (step, stage, phase, partition)
     dispatch_json: str = ""
     graph_dot: str = ""
     distribution: str = ""
@@ -209,8 +216,7 @@ def run_dense(c: SolverConfig) -> RunResult:
     eng.set_canonical(initial_canonical_state(c))
     periodic = c.scenario == "periodic_box"
     for step in range(c.steps):
-        eng.step(1)
-        d = eng.probe()
+        d = eng.step_probe()  # step_occ + probe_field, fused on the device
         _unstable(d, step)
         r.diagnostics.append((step, d.mass, d.max_speed))
         r.ledger += plan_ledger(step, lattice=c.lattice, domain=c.domain, layout=c.layout, partitions=c.partitions,

@@ -219,12 +219,20 @@ def main():
     import numpy as np
     import torch
 
-    torch.cuda.set_device(local_rank)
+    # VOXL_SHARE_DEVICE=1: every rank on cuda:0 over gloo -- exercises the
+    # multi-process IPC / device-flag path on a single-GPU box (timings are
+    # then time-sliced and not meaningful).
+    share = os.environ.get("VOXL_SHARE_DEVICE") == "1"
+    dev = 0 if share else local_rank
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     import paper_2503_07898_b200 as V
 
     n = args.size
@@ -240,7 +248,7 @@ def main():
     voxels_total = domain[0] * domain[1] * domain[2]
     voxels_local = eng.owned_voxels() if world > 1 else voxels_total
 
-    sampler = ClockSampler(local_rank) if rank == 0 else None
+    sampler = ClockSampler(dev) if rank == 0 else None
     eng.timed_steps(args.warmup)
     if dist:
         dist.barrier()
@@ -250,7 +258,7 @@ def main():
     torch.cuda.synchronize()
     t1 = time.time()
     if dist:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms], device="cpu" if share else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
@@ -301,7 +309,7 @@ def main():
                          "avg_kernel_ms": round(avg_kernel_ms, 4),
                          "frac_of_8tbs": round(achieved / 8000.0, 4)},
             "clocks": clocks,
-            "gpu_launches": args.steps * (1 if world == 1 else 3),
+            "gpu_launches": args.steps * (1 if world == 1 else 4),
             "diag": {"mass": diag.mass, "max_speed": diag.max_speed, "unstable": diag.unstable},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -140,3 +140,23 @@ def test_zero_copy_multiprocess_bitwise(world):
         assert np.array_equal(out, ref[k0 * s:k1 * s]), f"rank {rank} differs"
     m_ref, _ = O.port_probe("D3Q19", ref)
     assert abs(res[0][4] - m_ref) <= 1e-12 * m_ref
+
+
+@pytest.mark.gpu
+def test_bench_multirank_path_on_one_gpu():
+    """bench.py under torchrun with 2 ranks sharing cuda:0 (VOXL_SHARE_DEVICE=1):
+    the N>1 code path end to end (IPC buffers, device flags, max-over-ranks)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VOXL_SHARE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--steps", "10", "--warmup",
+           "3", "--size", "64", "--no-e2e", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, cwd=root, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "strong"
+    assert abs(line["diag"]["mass"] - 64 ** 3) < 1e-6 * 64 ** 3 and line["diag"]["unstable"] == 0

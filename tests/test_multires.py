@@ -134,6 +134,16 @@ def test_fp64_bitwise_vs_oracle(levels, fused, edge):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("fused", [True, False])
+def test_d3q27_fp64_bitwise_vs_oracle(fused):
+    dom = (16, 16, 16)
+    ref = O.port_mres_run("D3Q27", dom, 3, 0.56, (0.05, 0, 0), 2)
+    e = V.MultiResEngine(dom, 3, fused=fused, precision="fp64", block_edge=8, lattice="D3Q27")
+    e.step(2)
+    assert np.array_equal(e.get_state(), ref)
+
+
+@pytest.mark.gpu
 def test_fp64_bitwise_golden():
     z = np.load(os.path.join(GOLDEN, "mres3_cavity_d3q19_16.npz"))
     cfg = json.loads(str(z["config"]))

@@ -120,6 +120,18 @@ def test_fp64_bitwise_vs_oracle(strategy, edge, dom):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["naive", "disag_mem"])
+def test_d3q27_fp64_bitwise_vs_oracle(strategy):
+    dom = (24, 20, 16)
+    act = O.obstacle_mask(dom)
+    st = O.port_sparse_run("D3Q27", dom, 0.7, (0.04, 0, 0), 10, act)
+    ref = O.sparse_canonical(dom, act, st, 27)
+    e = V.SparseEngine(dom, block_edge=8, strategy=strategy, precision="fp64", lattice="D3Q27")
+    e.step(10)
+    assert np.array_equal(e.get_state(), ref)
+
+
+@pytest.mark.gpu
 def test_fp64_bitwise_golden():
     z = np.load(os.path.join(GOLDEN, "sparse_obstacle_d3q19_16.npz"))
     cfg = json.loads(str(z["config"]))

@@ -686,6 +686,15 @@ DenseEngine::~DenseEngine() {
     if (diag_partials_) cudaFree(diag_partials_);
     if (staging_) cudaFree(staging_);
     if (flags_ && distributed_) cudaFree(flags_);
+    if (shared_stream_) {
+        cudaStreamSynchronize(shared_stream_);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(ev_shared_[i]);
+            cudaEventDestroy(ev_interior_[i]);
+        }
+        cudaEventDestroy(ev_join_);
+        cudaStreamDestroy(shared_stream_);
+    }
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -708,6 +717,7 @@ void DenseEngine::attach_peer(int p, void* b0, void* b1) {
 }
 
 void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_device) {
+    join_streams();
     const std::int64_t s = maps_[0].cross_section();
     const std::size_t plane_bytes = std::size_t(s) * q_ * sizeof(double);
     // stage at most ~256 MiB of canonical planes at a time
@@ -810,6 +820,16 @@ void DenseEngine::halo_copy(int which) {
 }
 
 void DenseEngine::enable_distributed() {
+    if (!shared_stream_) {
+        int lo = 0, hi = 0;
+        VOXL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        VOXL_CUDA(cudaStreamCreateWithPriority(&shared_stream_, cudaStreamNonBlocking, hi));
+        for (int i = 0; i < 2; ++i) {
+            VOXL_CUDA(cudaEventCreateWithFlags(&ev_shared_[i], cudaEventDisableTiming));
+            VOXL_CUDA(cudaEventCreateWithFlags(&ev_interior_[i], cudaEventDisableTiming));
+        }
+        VOXL_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
     if (!flags_) {
         VOXL_CUDA(cudaMalloc(&flags_, 4 * sizeof(std::uint32_t)));
         VOXL_CUDA(cudaMemset(flags_, 0, 4 * sizeof(std::uint32_t)));
@@ -823,6 +843,7 @@ void DenseEngine::attach_flags(std::uint32_t* up, std::uint32_t* low) {
 }
 
 void DenseEngine::halo_push() {
+    join_streams();
     // Our shared slabs -> neighbours' halos of the current parity (peer copies).
     const auto recs = halo_records(decomp_, maps_, 0);
     for (const auto& r : recs) {
@@ -839,36 +860,67 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     // Per step: wait(neighbour flags >= t) -> shared layers (k = 0, n-1) with
     // peer halo stores -> signal(t + 1) -> interior (k = 1 .. n-2). The interior
     // kernel never touches a halo, so it overlaps the neighbours' exchange.
+    //
+    // Two streams (OCC, paper Fig. 4c): the interior kernel runs on stream_
+    // (I) and overlaps the high-priority shared-layer stream (S) that waits for
+    // the neighbours, stores the crossing populations into their halos and
+    // signals them. Cross-stream order, per step t:
+    //   I: after shared(t-1) [RAW on planes 0/n-1, WAR on planes 1/n-2] -> interior(t)
+    //   S: after interior(t-1) [RAW on planes 1/n-2, WAR on planes 0/n-1]
+    //      -> wait(flags >= t) -> shared(t) -> signal(t+1)
+    // Parity-alternating events keep "the previous step's" record addressable.
     const int p = cfg_.first_partition;
     const bool wrap = cfg_.scenario == Scenario::PeriodicBox;
     const bool zero_copy = cfg_.halo == HaloMode::ZeroCopy;
     const int in = cur_, out = cur_ ^ 1;
     const int up = decomp_.upper_neighbor(p), low = decomp_.lower_neighbor(p);
     const unsigned t = unsigned(steps_done_);
-    if (zero_copy) {
-        wait_flags_kernel<<<1, 32, 0, stream_>>>(flags_, up >= 0, low >= 0, t);
-        VOXL_CUDA(cudaGetLastError());
+    const int par = int(t & 1u), prev = par ^ 1;
+    if (!occ_ready_) {
+        for (int i = 0; i < 2; ++i) {
+            VOXL_CUDA(cudaEventRecord(ev_shared_[i], stream_));
+            VOXL_CUDA(cudaEventRecord(ev_interior_[i], stream_));
+        }
+        occ_ready_ = true;
     }
-    void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
-    void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
     const int n = decomp_.thickness(p);
-    dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
-        using Ops = decltype(ops);
-        // shared layers first: k = 0 and k = n - 1
-        Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out, wrap,
-                         steps_done_, error_flag_, 0, n - 1, 2, stream_, true, diag);
-    });
-    if (zero_copy) {
-        signal_flags_kernel<<<1, 32, 0, stream_>>>(remote_flag_up_, remote_flag_low_, t + 1);
-        VOXL_CUDA(cudaGetLastError());
-    }
+    // I: interior(t)
+    VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_shared_[prev], 0));
     dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
         using Ops = decltype(ops);
         Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr, wrap,
                          steps_done_, error_flag_, 1, 1, n - 2, stream_, false, diag);
     });
+    VOXL_CUDA(cudaEventRecord(ev_interior_[par], stream_));
+    // S: wait -> shared(t) -> signal
+    VOXL_CUDA(cudaStreamWaitEvent(shared_stream_, ev_interior_[prev], 0));
+    if (zero_copy) {
+        wait_flags_kernel<<<1, 32, 0, shared_stream_>>>(flags_, up >= 0, low >= 0, t);
+        VOXL_CUDA(cudaGetLastError());
+    }
+    void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
+    void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
+    dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        using Ops = decltype(ops);
+        Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out, wrap,
+                         steps_done_, error_flag_, 0, n - 1, 2, shared_stream_, true, diag);
+    });
+    if (zero_copy) {
+        signal_flags_kernel<<<1, 32, 0, shared_stream_>>>(remote_flag_up_, remote_flag_low_, t + 1);
+        VOXL_CUDA(cudaGetLastError());
+    }
+    VOXL_CUDA(cudaEventRecord(ev_shared_[par], shared_stream_));
     cur_ = out;
     ++steps_done_;
+    // Diagnostics reductions and the copy-mode exchange (issued on stream_
+    // by the caller) need the whole step: join S into I.
+    if (diag || !zero_copy) join_streams();
+}
+
+void DenseEngine::join_streams() {
+    if (!shared_stream_) return;
+    VOXL_CUDA(cudaEventRecord(ev_join_, shared_stream_));
+    VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
 }
 
 void DenseEngine::launch_step(DiagTarget* diag) {
@@ -907,6 +959,7 @@ double DenseEngine::timed_steps(int n, double* kernel_ms) {
     for (int i = 0; i < n; ++i) {
         VOXL_CUDA(cudaEventRecord(ev[2 * i], stream_));
         launch_step();
+        if (i == n - 1) join_streams();
         VOXL_CUDA(cudaEventRecord(ev[2 * i + 1], stream_));
     }
     VOXL_CUDA(cudaStreamSynchronize(stream_));
@@ -925,6 +978,7 @@ double DenseEngine::timed_steps(int n, double* kernel_ms) {
 }
 
 void DenseEngine::check_errors() {
+    join_streams();
     int flag = INT_MAX;
     VOXL_CUDA(cudaMemcpyAsync(&flag, error_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
@@ -981,6 +1035,7 @@ DenseDiag DenseEngine::step_probe() {
 }
 
 DenseDiag DenseEngine::probe() {
+    join_streams();
     double* partial = diag_scratch_;
     double* out = diag_scratch_ + 2 * kProbeBlocks;
     auto* bad = reinterpret_cast<unsigned long long*>(diag_scratch_ + 2 * kProbeBlocks + 2);

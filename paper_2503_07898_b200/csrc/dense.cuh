@@ -152,6 +152,13 @@ private:
     std::uint32_t* remote_flag_up_ = nullptr;
     std::uint32_t* remote_flag_low_ = nullptr;
     bool distributed_ = false;
+    // multi-process OCC schedule (launch_step_distributed)
+    cudaStream_t shared_stream_ = nullptr;
+    cudaEvent_t ev_shared_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_interior_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_join_ = nullptr;
+    bool occ_ready_ = false;
+    void join_streams();
 
     bool local(int p) const {
         return p >= cfg_.first_partition && p < cfg_.first_partition + cfg_.local_partitions;

@@ -23,7 +23,8 @@ struct MresArgs {
     const std::uint64_t* amask;
     const std::uint8_t* cls;
     const int* org;
-    const int* blocks;
+    int block_begin;              // first block of this launch (blocks are class-ordered)
+    const std::uint8_t* full;     // 1 iff every cell of the block is active
     int n[3];
     R omega, keep;
     R lid[Q];  // 2 w_j rho0 3 (e_j . u_lid) per pulled direction j (multires.cpp:499-503)
@@ -66,7 +67,7 @@ __device__ __forceinline__ bool bit_of(const unsigned long long* words, int loca
 template <class L, class R, bool Exact, int E>
 __global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W;
-    const int b = A.blocks[blockIdx.x];
+    const int b = A.block_begin + int(blockIdx.x);
     const int t = threadIdx.x;
     if (!((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
     const long long base = (long long)b * Q * BV + t;
@@ -102,20 +103,23 @@ __global__ void __launch_bounds__(E* E* E, (E == 8 && sizeof(R) == 4) ? 3 : 1)
     mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W;
     __shared__ const R* s_src[27];
-    __shared__ int s_inner;
-    const int b = A.blocks[blockIdx.x];
+    __shared__ int s_inner, s_full;
+    const int b = A.block_begin + int(blockIdx.x);
     const int t = threadIdx.x;
     if (t < 27) {
         const int nb = A.nbr[(long long)b * 27 + t];
         s_src[t] = A.post + (long long)(nb < 0 ? b : nb) * Q * BV;
     }
+    // metadata loads in different warps so their latencies overlap (E = 4
+    // runs 64-thread CTAs: stay below 64 there)
     if (t == 32) {
         // block strictly inside the level domain: no pull can leave it
         const int* o = A.org + 3 * b;
         s_inner = o[0] > 0 && o[1] > 0 && o[2] > 0 && o[0] + E < A.n[0] && o[1] + E < A.n[1] && o[2] + E < A.n[2];
     }
+    if (t == (BV > 64 ? 64 : 33)) s_full = A.full[b];
     __syncthreads();
-    if (!((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
+    if (!s_full && !((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
     if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true>(A, b, s_src);
     else mres_pull_body<L, R, Exact, E, COLLIDE, false>(A, b, s_src);
 }
@@ -282,6 +286,7 @@ struct MultiResEngine::Level {
     std::int32_t* nbr = nullptr;
     std::uint64_t* amask = nullptr;
     std::uint8_t* cls = nullptr;
+    std::uint8_t* full = nullptr;
     int* org = nullptr;
     int* all_blocks = nullptr;
     int* uni_blocks = nullptr;
@@ -357,30 +362,60 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
         std::vector<std::uint8_t> ext(vol);
         for (std::size_t i = 0; i < vol; ++i) ext[i] = G.active[i] | ghost[l][i] | ring[l][i];
         V->ext = BlockGrid::build(d, ext.data(), E);
+        const int nb = V->ext.num_blocks(), W = V->ext.mask_words(), BV = V->ext.block_volume();
+        // Per-block fusion class, then the disaggregated order (the paper's
+        // DisagMem idea applied to multires): uniform blocks first, then jump
+        // blocks, then ghost/ring-only blocks -- each launch covers one
+        // contiguous range, so a CTA indexes its block directly.
+        auto classify = [&](const BlockGrid& bg, int b, std::uint64_t* mask_out, bool* full_out) {
+            const auto& o = bg.blocks()[b].origin;
+            bool any = false, cross = false, full = true;
+            for (int local = 0; local < BV; ++local) {
+                const int x = o[0] + local % E, y = o[1] + (local / E) % E, z = o[2] + local / (E * E);
+                if (x >= d[0] || y >= d[1] || z >= d[2]) {
+                    full = false;
+                    continue;
+                }
+                const std::int64_t i = lin3(d, x, y, z);
+                if (!G.active[i]) {
+                    full = false;
+                    continue;
+                }
+                any = true;
+                if (mask_out) mask_out[local >> 6] |= 1ull << (local & 63);
+                if (crossing_near[i]) cross = true;
+            }
+            if (full_out) *full_out = full;
+            return any ? (cross ? kJump : kUniform) : kNone;
+        };
+        {
+            std::vector<int> perm(nb);
+            std::vector<std::uint8_t> c0(nb);
+            for (int b = 0; b < nb; ++b) {
+                perm[b] = b;
+                c0[b] = classify(V->ext, b, nullptr, nullptr);
+            }
+            auto rank = [&](int b) { return c0[b] == kUniform ? 0 : (c0[b] == kJump ? 1 : 2); };
+            std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return rank(x) < rank(y); });
+            V->ext.permute(perm);
+        }
         const BlockGrid& bg = V->ext;
-        const int nb = bg.num_blocks(), W = bg.mask_words(), BV = bg.block_volume();
         std::vector<std::uint64_t> am(std::size_t(nb) * W, 0);
-        std::vector<std::uint8_t> cls(nb, kNone);
+        std::vector<std::uint8_t> cls(nb, kNone), full(nb, 0);
         std::vector<int> org(std::size_t(nb) * 3), all, uni, jmp;
         for (int b = 0; b < nb; ++b) {
             const auto& o = bg.blocks()[b].origin;
             for (int a = 0; a < 3; ++a) org[std::size_t(b) * 3 + a] = o[a];
-            bool any = false, cross = false;
-            for (int local = 0; local < BV; ++local) {
-                const int x = o[0] + local % E, y = o[1] + (local / E) % E, z = o[2] + local / (E * E);
-                if (x >= d[0] || y >= d[1] || z >= d[2]) continue;
-                const std::int64_t i = lin3(d, x, y, z);
-                if (!G.active[i]) continue;
-                any = true;
-                am[std::size_t(b) * W + (local >> 6)] |= 1ull << (local & 63);
-                if (crossing_near[i]) cross = true;
-            }
-            if (any) {
-                cls[b] = cross ? kJump : kUniform;
+            bool f = false;
+            cls[b] = classify(bg, b, &am[std::size_t(b) * W], &f);
+            full[b] = f;
+            if (cls[b] != kNone) {
                 all.push_back(b);
-                (cross ? jmp : uni).push_back(b);
+                (cls[b] == kJump ? jmp : uni).push_back(b);
             }
         }
+        VOXL_CUDA(cudaMalloc(&V->full, std::max(1, nb)));
+        VOXL_CUDA(cudaMemcpy(V->full, full.data(), nb, cudaMemcpyHostToDevice));
         V->n_all = int(all.size());
         V->n_uni = int(uni.size());
         V->n_jump = int(jmp.size());
@@ -473,6 +508,7 @@ MultiResEngine::~MultiResEngine() {
         cudaFree(V->nbr);
         cudaFree(V->amask);
         cudaFree(V->cls);
+        cudaFree(V->full);
         cudaFree(V->org);
         cudaFree(V->all_blocks);
         cudaFree(V->uni_blocks);
@@ -610,6 +646,7 @@ MresArgs<L::Q, R> level_args(const MresConfig& cfg, MultiResEngine::Level* V, in
     A.amask = V->amask;
     A.cls = V->cls;
     A.org = V->org;
+    A.full = V->full;
     for (int a = 0; a < 3; ++a) A.n[a] = V->n[a];
     const double inv_tau = V->inv_tau;
     A.omega = R(inv_tau);
@@ -639,7 +676,7 @@ void MultiResEngine::launch_collide(int l, bool jump_only) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        A.blocks = jump_only ? V->jump_blocks : V->all_blocks;
+        A.block_begin = jump_only ? V->n_uni : 0;
         mres_collide_kernel<L, R, X, E><<<nb, E * E * E, 0, stream_>>>(A);
     });
     VOXL_CUDA(cudaGetLastError());
@@ -658,7 +695,7 @@ void MultiResEngine::launch_stream(int l, bool jump_only) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        A.blocks = jump_only ? V->jump_blocks : V->all_blocks;
+        A.block_begin = jump_only ? V->n_uni : 0;
         mres_pull_kernel<L, R, X, E, false><<<nb, E * E * E, 0, stream_>>>(A);  // post -> nxt
     });
     VOXL_CUDA(cudaGetLastError());
@@ -679,7 +716,7 @@ void MultiResEngine::gather_uniform(int l) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        A.blocks = V->uni_blocks;
+        A.block_begin = 0;
         A.post = static_cast<R*>(V->post[V->parity ^ 1]);
         A.nxt = static_cast<R*>(V->cur);
         mres_pull_kernel<L, R, X, E, false><<<V->n_uni, E * E * E, 0, stream_>>>(A);
@@ -707,7 +744,7 @@ void MultiResEngine::load_uniform_post() {
             constexpr bool X = decltype(exact)::value;
             constexpr int E = decltype(e)::value;
             auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-            A.blocks = V->uni_blocks;
+            A.block_begin = 0;
             mres_collide_kernel<L, R, X, E><<<V->n_uni, E * E * E, 0, stream_>>>(A);
         });
         VOXL_CUDA(cudaGetLastError());
@@ -727,7 +764,7 @@ void MultiResEngine::launch_fused(int l) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        A.blocks = V->uni_blocks;
+        A.block_begin = 0;
         A.nxt = static_cast<R*>(V->post[V->parity ^ 1]);  // post[p] -> post[p^1]
         mres_pull_kernel<L, R, X, E, true><<<V->n_uni, E * E * E, 0, stream_>>>(A);
     });

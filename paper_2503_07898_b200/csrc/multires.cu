@@ -96,39 +96,44 @@ __global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_cons
 /// storage, so collide-after-pull is the reference's collide-before-pull of
 /// the next step), one pass at 2 Q sizeof(real) bytes per update.
 template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER>
-__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, const R* const* s_src);
+__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src);
+
+/// CTAs per block: 8^3 blocks are split over two 256-thread CTAs (6 CTAs / SM
+/// at 40 registers), so each CTA's metadata prologue hides behind five others.
+template <int E>
+constexpr int kSplit = E == 8 ? 2 : 1;
 
 template <class L, class R, bool Exact, int E, bool COLLIDE>
-__global__ void __launch_bounds__(E* E* E, (E == 8 && sizeof(R) == 4) ? 3 : 1)
+__global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4) ? 6 : 1)
     mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
-    constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W;
+    constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W, S = kSplit<E>;
     __shared__ const R* s_src[27];
     __shared__ int s_inner, s_full;
-    const int b = A.block_begin + int(blockIdx.x);
-    const int t = threadIdx.x;
-    if (t < 27) {
-        const int nb = A.nbr[(long long)b * 27 + t];
-        s_src[t] = A.post + (long long)(nb < 0 ? b : nb) * Q * BV;
+    const int b = A.block_begin + int(blockIdx.x) / S;
+    const int tid = threadIdx.x;
+    const int t = tid + (int(blockIdx.x) % S) * (BV / S);  // local voxel index in the block
+    if (tid < 27) {
+        const int nb = A.nbr[(long long)b * 27 + tid];
+        s_src[tid] = A.post + (long long)(nb < 0 ? b : nb) * Q * BV;
     }
     // metadata loads in different warps so their latencies overlap (E = 4
     // runs 64-thread CTAs: stay below 64 there)
-    if (t == 32) {
+    if (tid == 32) {
         // block strictly inside the level domain: no pull can leave it
         const int* o = A.org + 3 * b;
         s_inner = o[0] > 0 && o[1] > 0 && o[2] > 0 && o[0] + E < A.n[0] && o[1] + E < A.n[1] && o[2] + E < A.n[2];
     }
-    if (t == (BV > 64 ? 64 : 33)) s_full = A.full[b];
+    if (tid == (BV / S > 64 ? 64 : 33)) s_full = A.full[b];
     __syncthreads();
     if (!s_full && !((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
-    if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true>(A, b, s_src);
-    else mres_pull_body<L, R, Exact, E, COLLIDE, false>(A, b, s_src);
+    if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true>(A, b, t, s_src);
+    else mres_pull_body<L, R, Exact, E, COLLIDE, false>(A, b, t, s_src);
 }
 
 template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER>
-__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, const R* const* s_src) {
+__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src) {
     constexpr int Q = L::Q, BV = E * E * E;
     using Ar = Arith<R, Exact>;
-    const int t = threadIdx.x;
     constexpr int LOG = BlockGeom<E>::LOG;
     const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
     const int x = A.org[3 * b] + lx, y = A.org[3 * b + 1] + ly, z = A.org[3 * b + 2] + lz;
@@ -696,7 +701,7 @@ void MultiResEngine::launch_stream(int l, bool jump_only) {
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
         A.block_begin = jump_only ? V->n_uni : 0;
-        mres_pull_kernel<L, R, X, E, false><<<nb, E * E * E, 0, stream_>>>(A);  // post -> nxt
+        mres_pull_kernel<L, R, X, E, false><<<nb * kSplit<E>, E * E * E / kSplit<E>, 0, stream_>>>(A);  // post -> nxt
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTStream, b);
@@ -719,7 +724,7 @@ void MultiResEngine::gather_uniform(int l) {
         A.block_begin = 0;
         A.post = static_cast<R*>(V->post[V->parity ^ 1]);
         A.nxt = static_cast<R*>(V->cur);
-        mres_pull_kernel<L, R, X, E, false><<<V->n_uni, E * E * E, 0, stream_>>>(A);
+        mres_pull_kernel<L, R, X, E, false><<<V->n_uni * kSplit<E>, E * E * E / kSplit<E>, 0, stream_>>>(A);
     });
     VOXL_CUDA(cudaGetLastError());
 }
@@ -766,7 +771,7 @@ void MultiResEngine::launch_fused(int l) {
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
         A.block_begin = 0;
         A.nxt = static_cast<R*>(V->post[V->parity ^ 1]);  // post[p] -> post[p^1]
-        mres_pull_kernel<L, R, X, E, true><<<V->n_uni, E * E * E, 0, stream_>>>(A);
+        mres_pull_kernel<L, R, X, E, true><<<V->n_uni * kSplit<E>, E * E * E / kSplit<E>, 0, stream_>>>(A);
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTFused, b);

@@ -131,30 +131,38 @@ __device__ __forceinline__ bool regularized_dev(int sign, const R (&ubc)[3], R (
     return true;
 }
 
+/// CTAs per block: 8^3 blocks are split over two 256-thread CTAs (6 CTAs / SM
+/// instead of 3), so each CTA's metadata prologue hides behind five others.
+template <int E>
+constexpr int kSplit = E == 8 ? 2 : 1;
+
 template <class L, class R, bool Exact, int E, int MODE>
-__global__ void __launch_bounds__(E* E* E) sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
+__global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && sizeof(R) == 4 ? 6 : 1)
+    sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
     constexpr int Q = L::Q;
     constexpr int BV = E * E * E;
     constexpr int W = BV >= 64 ? BV / 64 : 1;
-    const int b = A.block_begin + int(blockIdx.x);
+    constexpr int S = kSplit<E>;
+    const int b = A.block_begin + int(blockIdx.x) / S;
     if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip
     __shared__ const R* s_ptr[27];  // component-0 plane of neighbour block d (own block if absent)
     __shared__ int s_nbr[27];
     __shared__ unsigned long long s_mask[27][W];
     __shared__ int s_full;
-    const int t = threadIdx.x;
-    if (t < 27) {
-        const int nb = A.nbr[(long long)b * 27 + t];
-        s_nbr[t] = nb;
-        s_ptr[t] = A.cur + (long long)(nb < 0 ? b : nb) * Q * BV;
+    const int tid = threadIdx.x;
+    const int t = tid + (int(blockIdx.x) % S) * (BV / S);  // local voxel index in the block
+    if (tid < 27) {
+        const int nb = A.nbr[(long long)b * 27 + tid];
+        s_nbr[tid] = nb;
+        s_ptr[tid] = A.cur + (long long)(nb < 0 ? b : nb) * Q * BV;
     }
-    if (t == 32) s_full = A.full[b];
+    if (tid == 32) s_full = A.full[b];
     __syncthreads();
     // CTA-uniform: every block of the 27-neighbourhood exists and is fully
     // active, so no pull can hit a solid and the mask tests are skipped.
     const bool full = s_full != 0;
     if (!full) {
-        for (int j = t; j < 27 * W; j += BV) {
+        for (int j = tid; j < 27 * W; j += BV / S) {
             const int d = j / W, w = j % W;
             const int nb = s_nbr[d];
             s_mask[d][w] = nb >= 0 ? A.masks[(long long)nb * W + w] : 0ull;
@@ -344,8 +352,9 @@ struct SparseOps {
     template <int E>
     static void launch_e(SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
         if (nblocks <= 0) return;
-        if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy><<<nblocks, E * E * E, 0, st>>>(A);
-        else sparse_step_kernel<L, R, Exact, E, kLight><<<nblocks, E * E * E, 0, st>>>(A);
+        constexpr int S = kSplit<E>;
+        if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy><<<nblocks * S, E * E * E / S, 0, st>>>(A);
+        else sparse_step_kernel<L, R, Exact, E, kLight><<<nblocks * S, E * E * E / S, 0, st>>>(A);
         VOXL_CUDA(cudaGetLastError());
     }
 

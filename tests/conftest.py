@@ -40,6 +40,6 @@ def _built():
     import oracle
 
     oracle.build()
-    from paper_2503_07898_b200 import build as b
+    import __graft_entry__
 
-    b.build()
+    __graft_entry__._load_builder().build()

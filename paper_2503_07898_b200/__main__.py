@@ -1,5 +1,5 @@
-"""`python -m paper_2503_07898_b200 <run|verify|ledger|model>` -- the reference
-CLI's subcommands (proj/tools/main.cpp:30-184) on the B200 engines.
+"""`python -m paper_2503_07898_b200 <run|verify|ledger|model|report>` -- the
+reference CLI's subcommands (proj/tools/main.cpp:30-229) on the B200 engines.
 
 Exit codes as the reference (main.cpp:261-269): 0 ok, 1 failure, 2 config error.
 """
@@ -115,6 +115,43 @@ def cmd_model() -> int:
     return 0
 
 
+def cmd_report(out_dir: str) -> int:
+    """cmd_report (main.cpp:186-229): one-screen summary of a `run` output directory."""
+    import os
+
+    from .solver import config_from_json
+
+    if not os.path.exists(out_dir):
+        print(f"report: directory not found: {out_dir}", file=sys.stderr)
+        return 2
+
+    def text(name):
+        with open(os.path.join(out_dir, name), "rb") as f:
+            return f.read().decode()
+
+    def has(name):
+        return os.path.exists(os.path.join(out_dir, name))
+
+    print(f"report for {out_dir}")
+    if has("config.json"):
+        c = config_from_json(text("config.json"))
+        nx, ny, nz = c.domain
+        print(f"  scenario: {c.scenario}, lattice {c.lattice}, domain {nx}x{ny}x{nz}, steps {c.steps}")
+    if has("diagnostics.csv"):
+        rows = [ln for ln in text("diagnostics.csv").split("\n")[1:] if ln]
+        print(f"  final diagnostics (step,mass,max_u): {rows[-1] if rows else ''}")
+    if has("ledger.csv"):
+        rows = [ln for ln in text("ledger.csv").split("\n")[1:] if ln]
+        elements = sum(int(ln.rsplit(",", 1)[1]) for ln in rows)
+        print(f"  ledger: {len(rows)} transfer records, {elements} elements total")
+    if has("dispatch.json"):
+        sys.stdout.write("  dispatch: " + text("dispatch.json"))
+    if has("distribution.txt"):
+        sys.stdout.write("  level distribution (% of finest cells): " + text("distribution.txt"))
+    sys.stdout.flush()
+    return 0
+
+
 def main(argv=None) -> int:
     from .solver import ConfigError
 
@@ -127,6 +164,8 @@ def main(argv=None) -> int:
     lg = sub.add_parser("ledger")
     lg.add_argument("--config", required=True)
     sub.add_parser("model")
+    rp = sub.add_parser("report")
+    rp.add_argument("--dir", required=True)
     a = ap.parse_args(argv)
     try:
         if a.cmd == "run":
@@ -135,6 +174,8 @@ def main(argv=None) -> int:
             return cmd_verify()
         if a.cmd == "ledger":
             return cmd_ledger(a.config)
+        if a.cmd == "report":
+            return cmd_report(a.dir)
         return cmd_model()
     except ConfigError as e:
         print(f"config error: {e}", file=sys.stderr)

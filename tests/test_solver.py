@@ -73,6 +73,38 @@ def test_cli_ledger_and_config_error_exit_codes(tmp_path):
     assert r.returncode == 2 and "tau must be > 0.5" in r.stderr
 
 
+@needs_ref
+@pytest.mark.parametrize("name", ["dense", "sparse", "multires"])
+def test_cli_report_on_reference_artifacts(name, tmp_path):
+    """`report` (main.cpp:186-229) over a directory holding the reference run's own
+    artifacts: one line per artifact, in the reference's wording."""
+    cfg = CASES[name]
+    ref = O.RefRun(cfg)
+    (tmp_path / "config.json").write_text(json.dumps(cfg))
+    (tmp_path / "diagnostics.csv").write_text(ref.diagnostics_csv)
+    expect = [f"report for {tmp_path}",
+              f"  scenario: {cfg['scenario']}, lattice {cfg['lattice']}, domain 16x16x16, steps {cfg['steps']}",
+              "  final diagnostics (step,mass,max_u): " + ref.diagnostics_csv.strip().split("\n")[-1]]
+    rows = [ln for ln in ref.ledger_csv.split("\n")[1:] if ln]
+    if rows:
+        (tmp_path / "ledger.csv").write_text(ref.ledger_csv)
+        expect.append(f"  ledger: {len(rows)} transfer records, "
+                      f"{sum(int(r.rsplit(',', 1)[1]) for r in rows)} elements total")
+    if ref.dispatch_json:
+        (tmp_path / "dispatch.json").write_text(ref.dispatch_json)
+        expect += ("  dispatch: " + ref.dispatch_json).rstrip("\n").split("\n")
+    if ref.distribution:
+        (tmp_path / "distribution.txt").write_text(ref.distribution)
+        expect += ("  level distribution (% of finest cells): " + ref.distribution).rstrip("\n").split("\n")
+    r = subprocess.run([sys.executable, "-m", "paper_2503_07898_b200", "report", "--dir", str(tmp_path)],
+                       capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.rstrip("\n").split("\n") == expect
+    r = subprocess.run([sys.executable, "-m", "paper_2503_07898_b200", "report", "--dir", str(tmp_path / "nope")],
+                       capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 2 and "directory not found" in r.stderr
+
+
 # ---- GPU: run() vs voxl::run ---------------------------------------------------------
 
 CASES = {

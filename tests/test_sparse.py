@@ -131,6 +131,40 @@ def test_d3q27_fp64_bitwise_vs_oracle(strategy):
     assert np.array_equal(e.get_state(), ref)
 
 
+def _random_mask(rng, dom):
+    """Random sparse domain: a few spheres and boxes carved out of the box."""
+    nz, ny, nx = dom[2], dom[1], dom[0]
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    act = np.ones((nz, ny, nx), bool)
+    for _ in range(int(rng.integers(1, 4))):
+        c = rng.uniform(0, 1, 3) * (nx, ny, nz)
+        r = rng.uniform(1.5, min(dom) / 3)
+        act &= (x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2 > r * r
+    for _ in range(int(rng.integers(0, 3))):
+        lo = rng.integers(0, np.array(dom) - 2)
+        hi = lo + rng.integers(1, 6, 3)
+        act[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = False
+    return act.astype(np.uint8).reshape(-1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_random_sparse_domains_all_strategies(seed):
+    """sparse_test.cpp:267-302 style property: random domains, every strategy and
+    block edge bitwise equal to the oracle (hence to each other)."""
+    rng = np.random.default_rng(7000 + seed)
+    dom = tuple(int(v) for v in rng.integers(12, 28, 3))
+    act = _random_mask(rng, dom)
+    st = O.port_sparse_run("D3Q19", dom, 0.7, (0.04, 0, 0), 8, act)
+    ref = O.sparse_canonical(dom, act, st, 19)
+    for strategy in ("naive", "disag_bitmask", "disag_mem"):
+        for edge in (4, 8):
+            e = V.SparseEngine(dom, act, block_edge=edge, strategy=strategy, precision="fp64")
+            e.step(8)
+            assert np.array_equal(e.get_state(), ref), (strategy, edge)
+            e.close()
+
+
 @pytest.mark.gpu
 def test_fp64_bitwise_golden():
     z = np.load(os.path.join(GOLDEN, "sparse_obstacle_d3q19_16.npz"))

@@ -49,6 +49,9 @@ extern "C" {
 #define VOXL_NAIVE 0          /* sparse::Strategy (sparse.hpp:117) */
 #define VOXL_DISAG_BITMASK 1
 #define VOXL_DISAG_MEM 2
+#define VOXL_OP_LBM 0         /* closed step_occ operator set (see voxl_dense_desc::op) */
+#define VOXL_OP_IDENTITY 1
+#define VOXL_OP_JACOBI2 2
 
 const char* voxl_last_error(void);
 int voxl_version(void);
@@ -92,6 +95,10 @@ typedef struct {
     int halo_mode;        /* VOXL_HALO_ZERO_COPY | VOXL_HALO_COPY */
     int first_partition;  /* owned range for multi-process use ... */
     int local_partitions; /* ... -1 = all partitions in this process */
+    int op;               /* step_occ kernel (partition.hpp:173): VOXL_OP_LBM (GatherKernel,
+                             lbm.hpp:123) | VOXL_OP_IDENTITY (partition_test.cpp:189) |
+                             VOXL_OP_JACOBI2 (five-point, 2 components, partition_test.cpp:234);
+                             0 = LBM for zero-initialised descriptors */
 } voxl_dense_desc;
 
 typedef struct {
@@ -207,6 +214,8 @@ int voxl_sparse_set_state(voxl_sparse* h, const double* canonical);
 int voxl_sparse_set_equilibrium(voxl_sparse* h, double rho, const double* u);
 /** n x SparseLbmEngine::step (sparse.cpp:386-394). */
 int voxl_sparse_step(voxl_sparse* h, int n);
+/** SparseLbmEngine::step_identity (sparse.cpp:396-404): state unchanged. */
+int voxl_sparse_step_identity(voxl_sparse* h, int n);
 int voxl_sparse_timed_steps(voxl_sparse* h, int n, double* total_ms, double* boundary_ms, double* light_ms);
 int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out);
 /** dispatch_plan(...).to_json() (sparse.cpp:199-225; Table 2). */

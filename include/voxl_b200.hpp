@@ -99,6 +99,8 @@ public:
     SparseLbmEngine& operator=(const SparseLbmEngine&) = delete;
 
     void step() { check(voxl_sparse_step(h_, 1)); }
+    /// step_identity (sparse.cpp:396-404)
+    void step_identity() { check(voxl_sparse_step_identity(h_, 1)); }
     std::int64_t num_active() const {
         std::int64_t n = 0;
         check(voxl_sparse_info(h_, &n, nullptr, nullptr, nullptr));

@@ -57,6 +57,7 @@ def port_lib():
                                     C.c_int, C.c_void_p, C.c_int64]
         lib.vo_mres_run.restype = C.c_int64
         lib.vo_band_level_map.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        lib.vo_jacobi2_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         _port = lib
     return _port
 
@@ -82,6 +83,7 @@ def ref_lib():
         lib.vref_run_free.argtypes = [vp]
         lib.vref_reference_dense_run.argtypes = [cp, _dp]
         lib.vref_dense_steps_from.argtypes = [cp, _dp, _dp]
+        lib.vref_occ_run.argtypes = [C.c_int] * 9 + [_dp, _dp, C.POINTER(i64), C.POINTER(i64)]
         lib.vref_initial_state.argtypes = [cp, _dp]
         lib.vref_probe.argtypes = [C.c_int, _dp, i64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         lib.vref_lattice_json.argtypes = [C.c_int, C.c_char_p, i64]
@@ -246,7 +248,30 @@ def port_mres_run(lattice="D3Q19", domain=(32, 32, 32), levels=3, tau=0.56, velo
     return out
 
 
+def port_jacobi2_run(domain, steps, state) -> np.ndarray:
+    """Five-point Jacobi of partition_test.cpp:234-247 on one grid (2 components)."""
+    nx, ny, nz = _dims(domain)
+    out = np.array(state, np.float64, copy=True)
+    port_lib().vo_jacobi2_run(nx, ny, nz, steps, out)
+    return out
+
+
 # ---- reference library ------------------------------------------------------------
+
+OPS = {"identity": 1, "jacobi2": 2}
+
+
+def ref_occ_run(op, domain, parts, axis, layout, steps, init, lattice="D3Q19"):
+    """step_occ (partition.hpp:173) over a PartitionedField pair with the reference
+    tests' identity / Jacobi kernels -> (canonical result, step-0 ledger alpha, beta)."""
+    nx, ny, nz = _dims(domain)
+    out = np.empty_like(np.ascontiguousarray(init, np.float64))
+    a, b = C.c_int64(), C.c_int64()
+    schemes = {"AoS": 0, "SoA": 1, "DisagSoA": 2}
+    if ref_lib().vref_occ_run(OPS[op], LATTICES[lattice], nx, ny, nz, parts, axis, schemes[layout], steps,
+                              np.ascontiguousarray(init, np.float64), out, C.byref(a), C.byref(b)):
+        raise RuntimeError(ref_error())
+    return out, a.value, b.value
 
 def ref_reference_dense_run(cfg: dict) -> np.ndarray:
     lib = ref_lib()

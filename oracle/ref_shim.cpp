@@ -185,6 +185,60 @@ int vref_dense_steps_from(const char* json, const double* init, double* out) {
     }
 }
 
+/// step_occ (partition.hpp:173) with the reference tests' generic kernels over a
+/// PartitionedField pair: op 1 = identity (partition_test.cpp:189-191, lattice
+/// q and TransferSets::for_lattice), op 2 = five-point Jacobi on a 2-component
+/// field (partition_test.cpp:234-247, TransferSets::all(2)). `init`/`out` are
+/// canonical (x fastest, component innermost). Returns step 0's ledger (alpha, beta).
+int vref_occ_run(int op, int lattice, int nx, int ny, int nz, int parts, int axis, int scheme, int steps,
+                 const double* init, double* out, std::int64_t* alpha, std::int64_t* beta) {
+    try {
+        const Extents domain{nx, ny, nz};
+        const Decomposition d = decompose(domain, parts, axis);
+        int card = 2;
+        TransferSets transfer = TransferSets::all(2);
+        if (op == 1) {
+            const Lattice lat = build_lattice(LatticeKind(lattice));
+            card = lat.q;
+            transfer = TransferSets::for_lattice(lat, axis);
+        }
+        PartitionedField a(d, LayoutScheme(scheme), card, transfer);
+        PartitionedField b(d, LayoutScheme(scheme), card, transfer);
+        a.fill_canonical(std::vector<double>(init, init + std::size_t(domain.volume()) * card));
+        auto identity = [&](const PartView& view, Vec3i v, double* o) {
+            for (int c = 0; c < card; ++c) o[c] = view(v, c);
+        };
+        auto jacobi = [&](const PartView& view, Vec3i v, double* o) {
+            const Vec3i offsets[4] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}};
+            for (int c = 0; c < 2; ++c) {
+                double sum = 0.0;
+                int n = 0;
+                for (const Vec3i& off : offsets) {
+                    const Vec3i s = v + off;
+                    if (s.x < 0 || s.x >= domain.nx || s.y < 0 || s.y >= domain.ny) continue;
+                    sum += view(s, c);
+                    ++n;
+                }
+                o[c] = 0.5 * view(v, c) + 0.5 * (n ? sum / n : 0.0);
+            }
+        };
+        TransferLedger ledger;
+        for (int s = 0; s < steps; ++s) {
+            if (op == 1) step_occ(a, b, identity, &ledger, nullptr, s);
+            else step_occ(a, b, jacobi, &ledger, nullptr, s);
+            std::swap(a, b);
+        }
+        const std::vector<double> res = a.to_canonical();
+        std::memcpy(out, res.data(), res.size() * sizeof(double));
+        const auto st = ledger.step_stats(0);
+        if (alpha) *alpha = st.alpha;
+        if (beta) *beta = st.beta;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int vref_initial_state(const char* json, double* out) {
     try {
         const std::vector<double> f = initial_canonical_state(config_from_json(json));

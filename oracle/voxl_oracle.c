@@ -688,3 +688,32 @@ int64_t vo_mres_run(int kind, int nx, int ny, int nz, int levels, const int* lev
     free(M);
     return n;
 }
+
+/* ---- generic step_occ operator: five-point Jacobi (partition_test.cpp:234-247) ---- */
+
+void vo_jacobi2_run(int nx, int ny, int nz, int steps, double* state) {
+    const int64_t plane = (int64_t)nx * ny;
+    const int64_t n = plane * nz * 2;
+    double* nxt = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    static const int off[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};
+    for (int s = 0; s < steps; ++s) {
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    const int64_t v = z * plane + (int64_t)y * nx + x;
+                    for (int c = 0; c < 2; ++c) {
+                        double sum = 0.0;
+                        int cnt = 0;
+                        for (int j = 0; j < 4; ++j) {
+                            const int sx = x + off[j][0], sy = y + off[j][1];
+                            if (sx < 0 || sx >= nx || sy < 0 || sy >= ny) continue;
+                            sum += state[(z * plane + (int64_t)sy * nx + sx) * 2 + c];
+                            ++cnt;
+                        }
+                        nxt[v * 2 + c] = 0.5 * state[v * 2 + c] + 0.5 * (cnt ? sum / cnt : 0.0);
+                    }
+                }
+        memcpy(state, nxt, sizeof(double) * (size_t)n);
+    }
+    free(nxt);
+}

@@ -83,6 +83,12 @@ int64_t vo_mres_run(int kind, int nx, int ny, int nz, int levels, const int* lev
 /* Band level map of run_multires (proj/src/solver.cpp:319-335). */
 void vo_band_level_map(int nx, int ny, int nz, int levels, int axis, int* map);
 
+/* `steps` x the five-point Jacobi of proj/tests/partition_test.cpp:234-247 on a
+ * 2-component field (canonical, x fastest, component innermost), each z plane
+ * independently. step_occ is partition-invariant for it (the same test), so the
+ * single-grid restatement is the oracle for every partitioning. In place. */
+void vo_jacobi2_run(int nx, int ny, int nz, int steps, double* state);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,7 +47,7 @@ class DenseDesc(C.Structure):
     _fields_ = [("lattice", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("tau", C.c_double),
                 ("scenario", C.c_int), ("velocity", C.c_double * 3), ("layout", C.c_int), ("partitions", C.c_int),
                 ("precision", C.c_int), ("halo_mode", C.c_int), ("first_partition", C.c_int),
-                ("local_partitions", C.c_int)]
+                ("local_partitions", C.c_int), ("op", C.c_int)]
 
 
 class Diag(C.Structure):
@@ -131,6 +131,7 @@ def _load():
         "voxl_sparse_set_state": ([vp, vp], C.c_int),
         "voxl_sparse_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
         "voxl_sparse_step": ([vp, C.c_int], C.c_int),
+        "voxl_sparse_step_identity": ([vp, C.c_int], C.c_int),
         "voxl_sparse_timed_steps": ([vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double)], C.c_int),
         "voxl_sparse_probe": ([vp, C.POINTER(Diag)], C.c_int),

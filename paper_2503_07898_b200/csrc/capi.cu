@@ -153,26 +153,35 @@ int voxl_classify_voxels(int nx, int ny, int nz, int parts, int axis, int period
     });
 }
 
+namespace {
+DenseConfig config_of(const voxl_dense_desc* desc) {
+    require(desc != nullptr, "null descriptor");
+    DenseConfig c;
+    c.lattice = desc->lattice;
+    c.domain = {desc->nx, desc->ny, desc->nz};
+    c.tau = desc->tau;
+    require(desc->scenario >= 0 && desc->scenario <= 2, "unknown scenario");
+    c.scenario = Scenario(desc->scenario);
+    c.velocity = {desc->velocity[0], desc->velocity[1], desc->velocity[2]};
+    require(desc->layout >= 0 && desc->layout <= 2, "unknown layout scheme");
+    c.layout = LayoutScheme(desc->layout);
+    c.partitions = desc->partitions;
+    require(desc->precision == VOXL_F32 || desc->precision == VOXL_F64, "unknown precision");
+    c.precision = Precision(desc->precision);
+    require(desc->halo_mode == 0 || desc->halo_mode == 1, "unknown halo mode");
+    c.halo = HaloMode(desc->halo_mode);
+    c.first_partition = desc->first_partition;
+    c.local_partitions = desc->local_partitions;
+    require(desc->op >= VOXL_OP_LBM && desc->op <= VOXL_OP_JACOBI2, "unknown operator");
+    c.op = Operator(desc->op);
+    return c;
+}
+} // namespace
+
 int voxl_dense_create(const voxl_dense_desc* desc, voxl_dense** out) {
     return guarded([&] {
         require(desc && out, "voxl_dense_create: null argument");
-        DenseConfig c;
-        c.lattice = desc->lattice;
-        c.domain = {desc->nx, desc->ny, desc->nz};
-        c.tau = desc->tau;
-        require(desc->scenario >= 0 && desc->scenario <= 2, "unknown scenario");
-        c.scenario = Scenario(desc->scenario);
-        c.velocity = {desc->velocity[0], desc->velocity[1], desc->velocity[2]};
-        require(desc->layout >= 0 && desc->layout <= 2, "unknown layout scheme");
-        c.layout = LayoutScheme(desc->layout);
-        c.partitions = desc->partitions;
-        require(desc->precision == VOXL_F32 || desc->precision == VOXL_F64, "unknown precision");
-        c.precision = Precision(desc->precision);
-        require(desc->halo_mode == 0 || desc->halo_mode == 1, "unknown halo mode");
-        c.halo = HaloMode(desc->halo_mode);
-        c.first_partition = desc->first_partition;
-        c.local_partitions = desc->local_partitions;
-        *out = new voxl_dense{new DenseEngine(c)};
+        *out = new voxl_dense{new DenseEngine(config_of(desc))};
     });
 }
 
@@ -255,19 +264,14 @@ int voxl_dense_ledger(voxl_dense* h, int step, voxl_transfer_record* out, int ca
 int voxl_dense_plan_ledger(const voxl_dense_desc* desc, int step, voxl_transfer_record* out, int cap,
                            int* count) {
     return guarded([&] {
-        require(desc != nullptr, "null descriptor");
-        require(desc->lattice >= 0 && desc->lattice <= 2, "unknown lattice kind");
-        require(desc->layout >= 0 && desc->layout <= 2, "unknown layout scheme");
-        const LatticeTable t = make_lattice(desc->lattice);
-        const int axis = t.dim == 2 ? 1 : 2;
-        const Decomposition d =
-            decompose({desc->nx, desc->ny, desc->nz}, desc->partitions, axis, desc->scenario == VOXL_PERIODIC);
+        const DenseConfig c = config_of(desc);
+        const OperatorShape os = operator_shape(c);
+        const Decomposition d = decompose(c.domain, c.partitions, os.axis, c.scenario == Scenario::PeriodicBox);
         std::vector<LayoutMap> maps;
-        const TransferSets ts = TransferSets::for_lattice(desc->lattice, axis);
-        for (int p = 0; p < desc->partitions; ++p) {
-            std::array<int, 3> shape{desc->nx, desc->ny, desc->nz};
-            shape[axis] = d.thickness(p);
-            maps.push_back(LayoutMap::build(LayoutScheme(desc->layout), shape, t.q, axis, ts));
+        for (int p = 0; p < c.partitions; ++p) {
+            std::array<int, 3> shape = c.domain;
+            shape[os.axis] = d.thickness(p);
+            maps.push_back(LayoutMap::build(c.layout, shape, os.q, os.axis, os.transfer));
         }
         const auto recs = halo_records(d, maps, step);
         if (count) *count = int(recs.size());
@@ -470,6 +474,13 @@ int voxl_sparse_set_equilibrium(voxl_sparse* h, double rho, const double* u) {
 
 int voxl_sparse_step(voxl_sparse* h, int n) {
     return guarded([&] { SP(h)->step(n); });
+}
+
+int voxl_sparse_step_identity(voxl_sparse* h, int n) {
+    return guarded([&] {
+        require(n >= 0, "step_identity: n must be >= 0");
+        SP(h)->step_identity(n);
+    });
 }
 
 int voxl_sparse_timed_steps(voxl_sparse* h, int n, double* total, double* bms, double* lms) {

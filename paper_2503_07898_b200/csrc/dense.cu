@@ -239,6 +239,67 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
     }
 }
 
+constexpr int kOpIdentity = int(Operator::Identity);
+constexpr int kOpJacobi2 = int(Operator::Jacobi2);
+
+/// The generic step_occ kernels (see Operator): one thread per voxel, same
+/// geometry, plane tables and zero-copy halo stores as dense_step_kernel.
+///   identity: out(v, c) = in(v, c)                      (partition_test.cpp:189-191)
+///   jacobi2:  out(v, c) = 0.5 in(v, c) + 0.5 (n ? sum / n : 0), sum over the
+///             in-domain neighbours +x, -x, +y, -y in that order
+///                                                      (partition_test.cpp:234-247)
+/// The y neighbours are k +- 1 (halo groups at the slab faces) when the
+/// partition axis is y, else the b +- 1 rows of the same plane.
+template <int OP, int Q, class R, bool Exact, bool AOS, int AXIS>
+__global__ void __launch_bounds__(kBlock) dense_operator_kernel(const __grid_constant__ StepArgs<Q, R> A) {
+    using Ar = Arith<R, Exact>;
+    const int a = blockIdx.x * kBlock + threadIdx.x;
+    if (a >= A.na) return;
+    const int b = blockIdx.y;
+    const int k = A.k_first + int(blockIdx.z) * A.k_step;
+    const int kg = A.kg0 + k;
+    const int na = A.na, s = A.s;
+    const int cross = b * na + a;
+    const long long lin = (long long)(k + 1) * s + cross;
+    const int gm = group_of(k - 1, A.n), g0 = group_of(k, A.n), gp = group_of(k + 1, A.n);
+    constexpr long long VS = AOS ? Q : 1;
+    R f[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) {
+        const R v = ld_ro(A.in + A.plane[g0][c] + lin * VS);
+        if constexpr (OP == kOpIdentity) {
+            f[c] = v;
+        } else {
+            R sum = R(0);
+            int cnt = 0;
+            if (a + 1 < na) { sum = Ar::add(sum, ld_ro(A.in + A.plane[g0][c] + (lin + 1) * VS)); ++cnt; }
+            if (a - 1 >= 0) { sum = Ar::add(sum, ld_ro(A.in + A.plane[g0][c] + (lin - 1) * VS)); ++cnt; }
+            if constexpr (AXIS == 1) {
+                if (kg + 1 < A.nk) { sum = Ar::add(sum, ld_ro(A.in + A.plane[gp][c] + (lin + s) * VS)); ++cnt; }
+                if (kg - 1 >= 0) { sum = Ar::add(sum, ld_ro(A.in + A.plane[gm][c] + (lin - s) * VS)); ++cnt; }
+            } else {
+                if (b + 1 < A.nb) { sum = Ar::add(sum, ld_ro(A.in + A.plane[g0][c] + (lin + na) * VS)); ++cnt; }
+                if (b - 1 >= 0) { sum = Ar::add(sum, ld_ro(A.in + A.plane[g0][c] + (lin - na) * VS)); ++cnt; }
+            }
+            const R mean = cnt ? sum / R(cnt) : R(0);
+            f[c] = Ar::add(Ar::mul(R(0.5), v), Ar::mul(R(0.5), mean));
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < Q; ++c) A.out[A.plane[g0][c] + lin * VS] = f[c];
+    if (k == 0 && A.up_out) {
+#pragma unroll
+        for (int c = 0; c < Q; ++c)
+            if ((A.up_mask >> c) & 1u) A.up_out[A.up_plane[c] + (long long)cross * VS] = f[c];
+    }
+    if (k == A.n - 1 && A.low_out) {
+#pragma unroll
+        for (int c = 0; c < Q; ++c)
+            if ((A.low_mask >> c) & 1u) A.low_out[A.low_plane[c] + (long long)cross * VS] = f[c];
+    }
+    if (A.remote_fence && ((k == 0 && A.up_out) || (k == A.n - 1 && A.low_out))) __threadfence_system();
+}
+
 /// Fixed-order reduction of the per-CTA diagnostics partials (stage 1 of 2).
 __global__ void diag_reduce_kernel(const double* partial, long long n, double* out) {
     __shared__ double sm[256], sv[256];
@@ -436,6 +497,54 @@ PartGeom geom_of(const Decomposition& d, int p) {
     return g;
 }
 
+/// Per-(group, component) plane tables, the neighbours' halo targets of the
+/// zero-copy stores, and the slab geometry of one step launch.
+template <int Q, class R>
+PartGeom fill_geometry(StepArgs<Q, R>& A, const Decomposition& d, const std::vector<LayoutMap>& maps, int p,
+                       const void* in, void* out, void* up_out, void* low_out, int k_first, int k_step,
+                       bool remote_fence) {
+    const PartGeom g = geom_of(d, p);
+    A.remote_fence = remote_fence;
+    A.in = static_cast<const R*>(in);
+    A.out = static_cast<R*>(out);
+    for (int gr = 0; gr < kGroupCount; ++gr)
+        for (int c = 0; c < Q; ++c) A.plane[gr][c] = maps[p].plane_offset(gr, c);
+    const bool aos = maps[p].scheme() == LayoutScheme::AoS;
+    const int up = d.upper_neighbor(p), low = d.lower_neighbor(p);
+    A.up_out = static_cast<R*>(up_out);
+    A.low_out = static_cast<R*>(low_out);
+    A.up_mask = A.low_mask = 0;
+    if (up >= 0 && up_out) {
+        const LayoutMap& nm = maps[up];
+        const std::vector<int>& comps = nm.transfer().down;
+        for (int c = 0; c < Q; ++c) {
+            const bool send = aos || std::find(comps.begin(), comps.end(), c) != comps.end();
+            if (send) A.up_mask |= 1u << c;
+            // neighbour's LowerHalo, k = n_up: lin = (n_up + 1) * s + cross
+            A.up_plane[c] = nm.plane_offset(int(GroupTag::LowerHalo), c) +
+                            (long long)(nm.shape()[d.axis] + 1) * g.s * nm.voxel_stride();
+        }
+    }
+    if (low >= 0 && low_out) {
+        const LayoutMap& nm = maps[low];
+        const std::vector<int>& comps = nm.transfer().up;
+        for (int c = 0; c < Q; ++c) {
+            const bool send = aos || std::find(comps.begin(), comps.end(), c) != comps.end();
+            if (send) A.low_mask |= 1u << c;
+            A.low_plane[c] = nm.plane_offset(int(GroupTag::UpperHalo), c);  // k = -1: lin = cross
+        }
+    }
+    A.na = g.na;
+    A.nb = g.nb;
+    A.n = g.n;
+    A.s = g.s;
+    A.k_first = k_first;
+    A.k_step = k_step;
+    A.kg0 = g.kg0;
+    A.nk = g.nk;
+    return g;
+}
+
 template <class L, class R, bool Exact>
 struct DenseOps {
     static constexpr int Q = L::Q;
@@ -457,36 +566,8 @@ struct DenseOps {
                             bool remote_fence = false, DiagTarget* diag = nullptr) {
         if (k_count <= 0) return;
         StepArgs<Q, R> A{};
-        A.remote_fence = remote_fence;
-        const PartGeom g = geom_of(d, p);
-        A.in = static_cast<const R*>(in);
-        A.out = static_cast<R*>(out);
-        fill_planes(maps[p], A.plane);
+        const PartGeom g = fill_geometry(A, d, maps, p, in, out, up_out, low_out, k_first, k_step, remote_fence);
         const bool aos = maps[p].scheme() == LayoutScheme::AoS;
-        const int up = d.upper_neighbor(p), low = d.lower_neighbor(p);
-        A.up_out = static_cast<R*>(up_out);
-        A.low_out = static_cast<R*>(low_out);
-        A.up_mask = A.low_mask = 0;
-        if (up >= 0 && up_out) {
-            const LayoutMap& nm = maps[up];
-            const std::vector<int>& comps = nm.transfer().down;
-            for (int c = 0; c < Q; ++c) {
-                const bool send = aos || std::find(comps.begin(), comps.end(), c) != comps.end();
-                if (send) A.up_mask |= 1u << c;
-                // neighbour's LowerHalo, k = n_up: lin = (n_up + 1) * s + cross
-                A.up_plane[c] = nm.plane_offset(int(GroupTag::LowerHalo), c) +
-                                (long long)(nm.shape()[d.axis] + 1) * g.s * nm.voxel_stride();
-            }
-        }
-        if (low >= 0 && low_out) {
-            const LayoutMap& nm = maps[low];
-            const std::vector<int>& comps = nm.transfer().up;
-            for (int c = 0; c < Q; ++c) {
-                const bool send = aos || std::find(comps.begin(), comps.end(), c) != comps.end();
-                if (send) A.low_mask |= 1u << c;
-                A.low_plane[c] = nm.plane_offset(int(GroupTag::UpperHalo), c);  // k = -1: lin = cross
-            }
-        }
         const bool lid = cfg.scenario == Scenario::LidDrivenCavity;
         for (int i = 0; i < Q; ++i) {
             // (((2.0 * w_i) * 1.0) * 3.0) * eu, eu = (ex*u0 + ey*u1) + ez*u2 (lbm.hpp:66-69)
@@ -502,14 +583,6 @@ struct DenseOps {
             A.omega = R(inv_tau);
             A.keep = R(1.0) - R(inv_tau);
         }
-        A.na = g.na;
-        A.nb = g.nb;
-        A.n = g.n;
-        A.s = g.s;
-        A.k_first = k_first;
-        A.k_step = k_step;
-        A.kg0 = g.kg0;
-        A.nk = g.nk;
         const bool periodic = cfg.scenario == Scenario::PeriodicBox;
         A.wall_a = !periodic;
         A.wall_b = !periodic && L::dim == 3;
@@ -611,14 +684,94 @@ struct DenseOps {
     }
 };
 
+/// Launch plumbing of the generic operators (same interface as DenseOps).
+/// Values are stored unshifted in both precisions.
+template <int OP, int Q, class R, bool Exact>
+struct OperatorOps {
+    static void launch_step(const DenseConfig&, const Decomposition& d, const std::vector<LayoutMap>& maps, int p,
+                            const void* in, void* out, void* up_out, void* low_out, bool, int, int*, int k_first,
+                            int k_step, int k_count, cudaStream_t st, bool remote_fence = false,
+                            DiagTarget* diag = nullptr) {
+        if (diag) throw std::invalid_argument("probe_field requires the lbm operator");
+        if (k_count <= 0) return;
+        StepArgs<Q, R> A{};
+        const PartGeom g = fill_geometry(A, d, maps, p, in, out, up_out, low_out, k_first, k_step, remote_fence);
+        const dim3 grid((g.na + kBlock - 1) / kBlock, g.nb, k_count);
+        auto go = [&](auto aos_c, auto axis_c) {
+            dense_operator_kernel<OP, Q, R, Exact, decltype(aos_c)::value, decltype(axis_c)::value>
+                <<<grid, kBlock, 0, st>>>(A);
+        };
+        using T = std::true_type;
+        using F = std::false_type;
+        using Y = std::integral_constant<int, 1>;
+        using Z = std::integral_constant<int, 2>;
+        const bool aos = maps[p].scheme() == LayoutScheme::AoS;
+        if (d.axis == 1) aos ? go(T{}, Y{}) : go(F{}, Y{});
+        else aos ? go(T{}, Z{}) : go(F{}, Z{});
+        VOXL_CUDA(cudaGetLastError());
+    }
+
+    static long long launch_ctas(const Decomposition& d, int p, int k_count) {
+        const PartGeom g = geom_of(d, p);
+        return (long long)((g.na + kBlock - 1) / kBlock) * g.nb * k_count;
+    }
+
+    static void canon(const Decomposition& d, const LayoutMap& m, int p, void* buf, double* staging, int k_lo,
+                      int k_hi, int kg_stage0, bool to_device, cudaStream_t st) {
+        CanonArgs<Q> A{};
+        for (int gr = 0; gr < kGroupCount; ++gr)
+            for (int c = 0; c < Q; ++c) A.plane[gr][c] = m.plane_offset(gr, c);
+        const PartGeom g = geom_of(d, p);
+        A.vs = m.voxel_stride();
+        A.na = g.na;
+        A.s = g.s;
+        A.n = g.n;
+        A.k_lo = k_lo;
+        A.k_hi = k_hi;
+        A.kg_stage0 = kg_stage0;
+        A.kg0 = g.kg0;
+        const long long count = (long long)(k_hi - k_lo) * g.s;
+        if (count <= 0) return;
+        const unsigned blocks = unsigned((count + 255) / 256);
+        if (to_device) canon_kernel<Q, R, true><<<blocks, 256, 0, st>>>(static_cast<R*>(buf), staging, A);
+        else canon_kernel<Q, R, false><<<blocks, 256, 0, st>>>(static_cast<R*>(buf), staging, A);
+        VOXL_CUDA(cudaGetLastError());
+    }
+
+    static void fill(const Decomposition&, const LayoutMap&, int, void*, const double*, cudaStream_t) {
+        throw std::invalid_argument("set_equilibrium requires the lbm operator");
+    }
+
+    static void probe(const Decomposition&, const LayoutMap&, int, const void*, double*, unsigned long long*, double*,
+                      cudaStream_t) {
+        throw std::invalid_argument("probe_field requires the lbm operator");
+    }
+};
+
 template <class F>
-void dispatch(int lattice, Precision prec, F&& f) {
+void dispatch(const DenseConfig& cfg, F&& f) {
+    const Precision prec = cfg.precision;
     auto by_prec = [&](auto lat) {
         using L = decltype(lat);
-        if (prec == Precision::F64) f(DenseOps<L, double, true>{});
-        else f(DenseOps<L, float, false>{});
+        constexpr int Q = L::Q;
+        switch (cfg.op) {
+            case Operator::Lbm:
+                if (prec == Precision::F64) f(DenseOps<L, double, true>{});
+                else f(DenseOps<L, float, false>{});
+                break;
+            case Operator::Identity:
+                if (prec == Precision::F64) f(OperatorOps<kOpIdentity, Q, double, true>{});
+                else f(OperatorOps<kOpIdentity, Q, float, false>{});
+                break;
+            default: throw std::invalid_argument("unknown operator");
+        }
     };
-    switch (lattice) {
+    if (cfg.op == Operator::Jacobi2) {
+        if (prec == Precision::F64) f(OperatorOps<kOpJacobi2, 2, double, true>{});
+        else f(OperatorOps<kOpJacobi2, 2, float, false>{});
+        return;
+    }
+    switch (cfg.lattice) {
         case kD2Q9: by_prec(D2Q9{}); break;
         case kD3Q19: by_prec(D3Q19{}); break;
         case kD3Q27: by_prec(D3Q27{}); break;
@@ -628,17 +781,42 @@ void dispatch(int lattice, Precision prec, F&& f) {
 
 } // namespace
 
+OperatorShape operator_shape(const DenseConfig& cfg) {
+    OperatorShape o;
+    if (cfg.op == Operator::Jacobi2) {
+        o.q = 2;
+        o.axis = cfg.domain[2] == 1 ? 1 : 2;
+        o.transfer = TransferSets::all(2);
+        return o;
+    }
+    if (cfg.op != Operator::Lbm && cfg.op != Operator::Identity) throw std::invalid_argument("unknown operator");
+    if (cfg.lattice < 0 || cfg.lattice > 2) throw std::invalid_argument("unknown lattice kind");
+    const LatticeTable t = make_lattice(cfg.lattice);
+    o.q = t.q;
+    o.axis = t.dim == 2 ? 1 : 2;
+    o.transfer = TransferSets::for_lattice(cfg.lattice, o.axis);
+    return o;
+}
+
+namespace {
+
+} // namespace
+
 // ---- engine ------------------------------------------------------------------------
 
 DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg) {
-    if (cfg_.lattice < 0 || cfg_.lattice > 2) throw std::invalid_argument("unknown lattice kind");
-    const LatticeTable t = make_lattice(cfg_.lattice);
-    q_ = t.q;
-    axis_ = t.dim == 2 ? 1 : 2;
-    if (!(cfg_.tau > 0.5)) throw std::invalid_argument("invalid configuration: tau must be > 0.5; ");
-    if (t.dim == 2 && cfg_.domain[2] != 1) throw std::invalid_argument("invalid configuration: D2Q9 requires nz == 1; ");
-    if (t.dim == 3 && cfg_.domain[2] < 2)
-        throw std::invalid_argument("invalid configuration: 3D lattices require nz >= 2; ");
+    const OperatorShape shape = operator_shape(cfg_);
+    q_ = shape.q;
+    axis_ = shape.axis;
+    if (cfg_.op != Operator::Jacobi2) {
+        const LatticeTable t = make_lattice(cfg_.lattice);
+        if (t.dim == 2 && cfg_.domain[2] != 1)
+            throw std::invalid_argument("invalid configuration: D2Q9 requires nz == 1; ");
+        if (t.dim == 3 && cfg_.domain[2] < 2)
+            throw std::invalid_argument("invalid configuration: 3D lattices require nz >= 2; ");
+    }
+    if (cfg_.op == Operator::Lbm && !(cfg_.tau > 0.5))
+        throw std::invalid_argument("invalid configuration: tau must be > 0.5; ");
     if (cfg_.domain[0] < 2 || cfg_.domain[1] < 2)
         throw std::invalid_argument("invalid configuration: domain extents must be >= 2; ");
     if (cfg_.scenario == Scenario::FlowOverObstacle)
@@ -651,11 +829,10 @@ DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg) {
     }
     if (cfg_.first_partition < 0 || cfg_.first_partition + cfg_.local_partitions > cfg_.partitions)
         throw std::invalid_argument("dense engine: bad local partition range");
-    const TransferSets ts = TransferSets::for_lattice(cfg_.lattice, axis_);
     for (int p = 0; p < cfg_.partitions; ++p) {
-        std::array<int, 3> shape = cfg_.domain;
-        shape[axis_] = decomp_.thickness(p);
-        maps_.push_back(LayoutMap::build(cfg_.layout, shape, q_, axis_, ts));
+        std::array<int, 3> owned = cfg_.domain;
+        owned[axis_] = decomp_.thickness(p);
+        maps_.push_back(LayoutMap::build(cfg_.layout, owned, q_, axis_, shape.transfer));
     }
     parts_.resize(cfg_.partitions);
     VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -739,7 +916,7 @@ void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_d
             if (!local(p)) continue;
             const int lo = std::max(k0, decomp_.slabs[p].first), hi = std::min(k1, decomp_.slabs[p].second);
             if (lo >= hi) continue;
-            dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+            dispatch(cfg_, [&](auto ops) {
                 decltype(ops)::canon(decomp_, maps_[p], p, parts_[p].buf[cur_], static_cast<double*>(staging_),
                                      lo - decomp_.slabs[p].first, hi - decomp_.slabs[p].first, k0, to_device,
                                      stream_);
@@ -777,6 +954,7 @@ void DenseEngine::set_canonical(const double* host) {
 void DenseEngine::set_equilibrium(double rho, const double u[3]) {
     // equilibrium (lattice.cpp:104-113) evaluated on the host in the reference's
     // double op order, then broadcast to every voxel of both parities.
+    if (cfg_.op != Operator::Lbm) throw std::invalid_argument("set_equilibrium requires the lbm operator");
     const LatticeTable t = make_lattice(cfg_.lattice);
     double feq[27];
     const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
@@ -788,7 +966,7 @@ void DenseEngine::set_equilibrium(double rho, const double u[3]) {
     for (int p = 0; p < cfg_.partitions; ++p) {
         if (!local(p)) continue;
         for (int w = 0; w < 2; ++w)
-            dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+            dispatch(cfg_, [&](auto ops) {
                 decltype(ops)::fill(decomp_, maps_[p], p, parts_[p].buf[w], feq, stream_);
             });
     }
@@ -886,7 +1064,7 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     const int n = decomp_.thickness(p);
     // I: interior(t)
     VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_shared_[prev], 0));
-    dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+    dispatch(cfg_, [&](auto ops) {
         using Ops = decltype(ops);
         Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr, wrap,
                          steps_done_, error_flag_, 1, 1, n - 2, stream_, false, diag);
@@ -900,7 +1078,7 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     }
     void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
     void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
-    dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+    dispatch(cfg_, [&](auto ops) {
         using Ops = decltype(ops);
         Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out, wrap,
                          steps_done_, error_flag_, 0, n - 1, 2, shared_stream_, true, diag);
@@ -937,7 +1115,7 @@ void DenseEngine::launch_step(DiagTarget* diag) {
         void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
         void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
         const int n = decomp_.thickness(p);
-        dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        dispatch(cfg_, [&](auto ops) {
             decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out,
                                        low_out, wrap, steps_done_, error_flag_, 0, 1, n, stream_, false, diag);
         });
@@ -997,7 +1175,7 @@ DenseDiag DenseEngine::step_probe() {
     long long ctas = 0;
     for (int p = 0; p < cfg_.partitions; ++p)
         if (local(p))
-            dispatch(cfg_.lattice, cfg_.precision,
+            dispatch(cfg_,
                      [&](auto ops) { ctas += decltype(ops)::launch_ctas(decomp_, p, decomp_.thickness(p)); });
     if (diag_partials_len_ < std::size_t(2 * ctas)) {
         if (diag_partials_) VOXL_CUDA(cudaFree(diag_partials_));
@@ -1045,7 +1223,7 @@ DenseDiag DenseEngine::probe() {
     VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
     for (int p = 0; p < cfg_.partitions; ++p) {
         if (!local(p)) continue;
-        dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        dispatch(cfg_, [&](auto ops) {
             decltype(ops)::probe(decomp_, maps_[p], p, parts_[p].buf[cur_], partial, bad, out, stream_);
         });
     }

@@ -29,6 +29,14 @@ enum class Precision : int { F32 = 0, F64 = 1 };
 enum class HaloMode : int { ZeroCopy = 0, Copy = 1 };
 enum class Scenario : int { LidDrivenCavity = 0, FlowOverObstacle = 1, PeriodicBox = 2 };
 
+/// The closed operator set behind the step_occ plugin point
+/// (partition.hpp:169-174 takes any `kernel(view, v, out)`; device code needs
+/// a closed set): the LBM GatherKernel (lbm.hpp:123-133), and the two generic
+/// kernels the reference's partition tests drive through step_occ -- the
+/// identity copy (partition_test.cpp:189-191) and the five-point Jacobi on a
+/// 2-component vector field (partition_test.cpp:234-247).
+enum class Operator : int { Lbm = 0, Identity = 1, Jacobi2 = 2 };
+
 struct DenseConfig {
     int lattice = 1;  // LatticeKind
     std::array<int, 3> domain{32, 32, 32};
@@ -43,7 +51,20 @@ struct DenseConfig {
     // The default (-1) owns all of them (single process).
     int first_partition = 0;
     int local_partitions = -1;
+    Operator op = Operator::Lbm;
 };
+
+/// Field geometry an operator implies: cardinality, partition axis and the
+/// face-crossing component sets. LBM / identity: the lattice's Q and
+/// TransferSets::for_lattice along z (y in 2D). Jacobi2: 2 components, every
+/// component crosses (TransferSets::all(2)), partitioned along y when nz == 1
+/// (the reference test's decompose(domain, parts, 1)) else along z.
+struct OperatorShape {
+    int q = 19;
+    int axis = 2;
+    TransferSets transfer;
+};
+OperatorShape operator_shape(const DenseConfig& cfg);
 
 struct DenseDiag {
     double mass = 0.0;

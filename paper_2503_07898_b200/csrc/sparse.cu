@@ -639,6 +639,19 @@ void SparseEngine::step(int n) {
     check_errors();
 }
 
+void SparseEngine::step_identity(int n) {
+    // step_identity (sparse.cpp:396-404): the sweeps copy every active voxel
+    // cur -> nxt. Inactive slots are never observable (canonical_state reads
+    // active voxels only), so one device copy of the field is the same step.
+    const std::size_t bytes = std::size_t(grid_.num_blocks()) * q_ * grid_.block_volume() * esize_;
+    for (int i = 0; i < n; ++i) {
+        VOXL_CUDA(cudaMemcpyAsync(buf_[cur_ ^ 1], buf_[cur_], bytes, cudaMemcpyDeviceToDevice, stream_));
+        cur_ ^= 1;
+        ++steps_done_;
+    }
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
 double SparseEngine::timed_steps(int n, double* boundary_ms, double* light_ms) {
     std::vector<cudaEvent_t> ev(4 * std::size_t(n) + 2);
     for (auto& e : ev) VOXL_CUDA(cudaEventCreate(&e));

@@ -57,6 +57,8 @@ public:
     void set_state(const double* canonical);
     void get_state(double* canonical);
     void step(int n);
+    /// Identity sweeps (sparse.cpp:396-404): state unchanged, report unchanged.
+    void step_identity(int n);
     /// n steps timed with CUDA events per launch: returns total ms, and the
     /// summed boundary-kernel and non-boundary-kernel ms.
     double timed_steps(int n, double* boundary_ms, double* light_ms);

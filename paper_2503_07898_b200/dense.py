@@ -23,6 +23,9 @@ LAYOUTS = {"AoS": 0, "SoA": 1, "DisagSoA": 2}
 SCENARIOS = {"lid_driven_cavity": 0, "flow_over_obstacle": 1, "periodic_box": 2}
 PRECISIONS = {"fp32": 0, "fp64": 1}
 HALO_MODES = {"zero_copy": 0, "copy": 1}
+# closed step_occ operator set (partition.hpp:173): the LBM GatherKernel and the
+# reference tests' identity / five-point Jacobi kernels (partition_test.cpp:189, :234)
+OPERATORS = {"lbm": 0, "identity": 1, "jacobi2": 2}
 
 
 def _kind(lattice):
@@ -79,7 +82,7 @@ class TransferRecord:
 
 def make_desc(lattice="D3Q19", domain=(32, 32, 32), tau=0.56, scenario="lid_driven_cavity",
               velocity=(0.05, 0.0, 0.0), layout="DisagSoA", partitions=1, precision="fp32",
-              halo_mode="zero_copy", first_partition=0, local_partitions=-1) -> _capi.DenseDesc:
+              halo_mode="zero_copy", first_partition=0, local_partitions=-1, op="lbm") -> _capi.DenseDesc:
     d = _capi.DenseDesc()
     d.lattice = _kind(lattice)
     dom = tuple(domain) if len(domain) == 3 else (domain[0], domain[1], 1)
@@ -93,6 +96,7 @@ def make_desc(lattice="D3Q19", domain=(32, 32, 32), tau=0.56, scenario="lid_driv
     d.halo_mode = HALO_MODES[halo_mode] if isinstance(halo_mode, str) else int(halo_mode)
     d.first_partition = first_partition
     d.local_partitions = local_partitions
+    d.op = OPERATORS[op] if isinstance(op, str) else int(op)
     return d
 
 
@@ -120,12 +124,13 @@ class DenseEngine:
 
     def __init__(self, lattice="D3Q19", domain=(32, 32, 32), tau=0.56, scenario="lid_driven_cavity",
                  velocity=(0.05, 0.0, 0.0), layout="DisagSoA", partitions=1, precision="fp32",
-                 halo_mode="zero_copy", first_partition=0, local_partitions=-1):
+                 halo_mode="zero_copy", first_partition=0, local_partitions=-1, op="lbm"):
         d = make_desc(lattice, domain, tau, scenario, velocity, layout, partitions, precision, halo_mode,
-                      first_partition, local_partitions)
+                      first_partition, local_partitions, op)
         dom = (d.nx, d.ny, d.nz)
         self.lattice = lattice if isinstance(lattice, str) else list(LATTICES)[lattice]
-        self.q = Q_OF[self.lattice]
+        self.op = op if isinstance(op, str) else list(OPERATORS)[op]
+        self.q = 2 if self.op == "jacobi2" else Q_OF[self.lattice]
         self.domain = dom
         self.partitions = partitions
         self._h = C.c_void_p()

@@ -167,6 +167,10 @@ class SparseEngine:
     def step(self, n=1):
         check(lib.voxl_sparse_step(self._h, n))
 
+    def step_identity(self, n=1):
+        """SparseLbmEngine::step_identity (sparse.cpp:396-404)."""
+        check(lib.voxl_sparse_step_identity(self._h, n))
+
     def timed_steps(self, n):
         t, b, l_ = C.c_double(), C.c_double(), C.c_double()
         check(lib.voxl_sparse_timed_steps(self._h, n, C.byref(t), C.byref(b), C.byref(l_)))

@@ -237,6 +237,10 @@ typedef struct {
     int precision;        /* VOXL_F32 | VOXL_F64 */
     int block_edge;       /* 8 (production) or 4 (reference granularity) */
     int reference_tables; /* also build the edge-4 ghost / pull / fusion tables */
+    int solid_cells;      /* extension beyond the reference (whose build rejects ids outside
+                             [0, levels), multires.cpp:84-85): level-map value -1 marks solid
+                             bounce-back cells inside the finest level (>= 3 cells from any
+                             coarser cell); 0 = reference semantics */
 } voxl_mres_desc;
 
 /** Band level map of run_multires (solver.cpp:319-335), x fastest int32. */

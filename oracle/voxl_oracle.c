@@ -447,6 +447,7 @@ typedef struct {
     uint8_t* refined;      /* covered by the finer level */
     uint8_t* under_coarse; /* parent active at the coarser level */
     uint8_t* ghost;        /* inactive under_coarse box-neighbour of an active cell */
+    uint8_t* solid;        /* obstacle extension: level-map -1 cells (finest level only) */
     double *cur, *nxt, *post, *ghostv, *coal;
     double inv_tau;
 } vo_level;
@@ -548,6 +549,7 @@ static void mres_stream(vo_mres* M, int l) {
                     } else {
                         const int64_t s = LIN(L, src[0], src[1], src[2]);
                         if (L->active[s]) g = L->post[s * q + i];
+                        else if (L->solid[s]) g = L->post[c * q + M->lat.opp[i]]; /* halfway bounce-back */
                         else if (L->ghost[s]) g = L->ghostv[s * q + i];
                         else g = L->coal[c * q + i];
                     }
@@ -595,7 +597,10 @@ int64_t vo_mres_run(int kind, int nx, int ny, int nz, int levels, const int* lev
         L->refined = (uint8_t*)calloc((size_t)L->vol, 1);
         L->under_coarse = (uint8_t*)calloc((size_t)L->vol, 1);
         L->ghost = (uint8_t*)calloc((size_t)L->vol, 1);
-        L->cur = (double*)calloc((size_t)(L->vol * q), sizeof(double));
+        L->solid = (uint8_t*)calloc((size_t)L->vol, 1);
+        if (l == 0)
+            for (int64_t c = 0; c < L->vol; ++c) L->solid[c] = level_map[c] == -1;
+        L->cur =(double*)calloc((size_t)(L->vol * q), sizeof(double));
         L->nxt = (double*)calloc((size_t)(L->vol * q), sizeof(double));
         L->post = (double*)calloc((size_t)(L->vol * q), sizeof(double));
         L->ghostv = (double*)calloc((size_t)(L->vol * q), sizeof(double));
@@ -682,7 +687,7 @@ int64_t vo_mres_run(int kind, int nx, int ny, int nz, int levels, const int* lev
     }
     for (int l = 0; l < levels; ++l) {
         vo_level* L = &M->lv[l];
-        free(L->active); free(L->refined); free(L->under_coarse); free(L->ghost);
+        free(L->active); free(L->refined); free(L->under_coarse); free(L->ghost); free(L->solid);
         free(L->cur); free(L->nxt); free(L->post); free(L->ghostv); free(L->coal);
     }
     free(M);

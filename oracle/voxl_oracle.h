@@ -76,7 +76,11 @@ int64_t vo_obstacle_mask(int nx, int ny, int nz, double radius, uint8_t* active)
  * dense per-level arrays. level_map: virtual-finest canonical order. The state
  * out is the reference's canonical_state (levels finest->coarsest, cells sorted
  * by pack_coord (x slowest, z fastest), component innermost). Returns the number
- * of doubles written, or -1. */
+ * of doubles written, or -1.
+ * Extension beyond the reference (PARITY UNPINNED for it: the reference's build
+ * rejects such maps, multires.cpp:84-85): level_map value -1 marks solid cells
+ * inside the finest level; a fluid cell pulling from one bounces back (own
+ * post-collision opposite population, as at the domain walls). */
 int64_t vo_mres_run(int kind, int nx, int ny, int nz, int levels, const int* level_map, double tau,
                     const double lid_u[3], int steps, double* out, int64_t cap);
 

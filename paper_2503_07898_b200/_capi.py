@@ -68,7 +68,7 @@ class SparseDesc(C.Structure):
 class MresDesc(C.Structure):
     _fields_ = [("lattice", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("levels", C.c_int),
                 ("tau", C.c_double), ("lid_u", C.c_double * 3), ("fused", C.c_int), ("precision", C.c_int),
-                ("block_edge", C.c_int), ("reference_tables", C.c_int)]
+                ("block_edge", C.c_int), ("reference_tables", C.c_int), ("solid_cells", C.c_int)]
 
 
 def _load():

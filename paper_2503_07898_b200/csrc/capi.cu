@@ -576,6 +576,7 @@ static MresConfig mres_config(const voxl_mres_desc* d) {
     c.precision = Precision(d->precision);
     c.edge = d->block_edge;
     c.reference_tables = d->reference_tables != 0;
+    c.allow_solid = d->solid_cells != 0;
     return c;
 }
 
@@ -665,7 +666,8 @@ int voxl_mres_plan_create(const voxl_mres_desc* d, const int32_t* map, voxl_mres
         require(d && map && out, "voxl_mres_plan_create: null argument");
         require(d->lattice >= 0 && d->lattice <= 2, "unknown lattice kind");
         *out = reinterpret_cast<voxl_mres_plan*>(
-            new MresGrid(MresGrid::build({d->nx, d->ny, d->nz}, d->levels, d->lattice, map, d->tau, true)));
+            new MresGrid(MresGrid::build({d->nx, d->ny, d->nz}, d->levels, d->lattice, map, d->tau, true,
+                                         d->solid_cells != 0)));
     });
 }
 

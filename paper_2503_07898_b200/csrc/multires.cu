@@ -25,6 +25,8 @@ struct MresArgs {
     const int* org;
     int block_begin;              // first block of this launch (blocks are class-ordered)
     const std::uint8_t* full;     // 1 iff every cell of the block is active
+    const std::uint64_t* smask;   // solid cells per block (obstacle extension), or null
+    const std::uint8_t* nsolid;   // 1 iff some active cell of the block has a solid box neighbour
     int n[3];
     R omega, keep;
     R lid[Q];  // 2 w_j rho0 3 (e_j . u_lid) per pulled direction j (multires.cpp:499-503)
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_cons
 /// true: the fused uniform-block kernel (uniform blocks keep post-collision
 /// storage, so collide-after-pull is the reference's collide-before-pull of
 /// the next step), one pass at 2 Q sizeof(real) bytes per update.
-template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER>
+template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER, bool SOLID>
 __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src);
 
 /// CTAs per block: 8^3 blocks are split over two 256-thread CTAs (6 CTAs / SM
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
     mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W, S = kSplit<E>;
     __shared__ const R* s_src[27];
-    __shared__ int s_inner, s_full;
+    __shared__ int s_inner, s_full, s_solid;
     const int b = A.block_begin + int(blockIdx.x) / S;
     const int tid = threadIdx.x;
     const int t = tid + (int(blockIdx.x) % S) * (BV / S);  // local voxel index in the block
@@ -124,13 +126,15 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
         s_inner = o[0] > 0 && o[1] > 0 && o[2] > 0 && o[0] + E < A.n[0] && o[1] + E < A.n[1] && o[2] + E < A.n[2];
     }
     if (tid == (BV / S > 64 ? 64 : 33)) s_full = A.full[b];
+    if (tid == (BV / S > 64 ? 96 : 34)) s_solid = A.nsolid ? A.nsolid[b] : 0;
     __syncthreads();
     if (!s_full && !((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
-    if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true>(A, b, t, s_src);
-    else mres_pull_body<L, R, Exact, E, COLLIDE, false>(A, b, t, s_src);
+    if (s_solid) mres_pull_body<L, R, Exact, E, COLLIDE, false, true>(A, b, t, s_src);
+    else if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true, false>(A, b, t, s_src);
+    else mres_pull_body<L, R, Exact, E, COLLIDE, false, false>(A, b, t, s_src);
 }
 
-template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER>
+template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER, bool SOLID>
 __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src) {
     constexpr int Q = L::Q, BV = E * E * E;
     using Ar = Arith<R, Exact>;
@@ -158,6 +162,14 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
             if constexpr (ey < 0) oob = oob || dyhi;
             if constexpr (ez > 0) oob = oob || dzlo;
             if constexpr (ez < 0) oob = oob || dzhi;
+            if constexpr (SOLID && (ex != 0 || ey != 0 || ez != 0)) {
+                // obstacle cells bounce back like the walls; a source block
+                // missing from the extended grid can only be all-solid there
+                if (!oob) {
+                    const int nb = A.nbr[(long long)b * 27 + d];
+                    oob = nb < 0 || ((A.smask[(long long)nb * BlockGeom<E>::W + (sl >> 6)] >> (sl & 63)) & 1ull);
+                }
+            }
             const R* p = oob ? own_src + oi * BV : s_src[d] + (i * BV + sl);
             R v = __ldg(p);
             if constexpr (ez < 0) {
@@ -292,6 +304,8 @@ struct MultiResEngine::Level {
     std::uint64_t* amask = nullptr;
     std::uint8_t* cls = nullptr;
     std::uint8_t* full = nullptr;
+    std::uint64_t* smask = nullptr;  // obstacle extension: solid cells per block
+    std::uint8_t* nsolid = nullptr;  // per block: an active cell has a solid box neighbour
     int* org = nullptr;
     int* all_blocks = nullptr;
     int* uni_blocks = nullptr;
@@ -322,7 +336,8 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
     const LatticeTable lat = make_lattice(cfg_.lattice);
     q_ = lat.q;
     esize_ = cfg_.precision == Precision::F64 ? 8 : 4;
-    grid_ = MresGrid::build(cfg_.domain, cfg_.levels, cfg_.lattice, level_map, cfg_.tau, cfg_.reference_tables);
+    grid_ = MresGrid::build(cfg_.domain, cfg_.levels, cfg_.lattice, level_map, cfg_.tau, cfg_.reference_tables,
+                            cfg_.allow_solid);
     const int L = grid_.num_levels();
     const int E = cfg_.edge;
     for (int l = 0; l < L; ++l) {
@@ -341,7 +356,7 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
         std::vector<std::uint8_t> other(vol, 0);
         for (std::size_t i = 0; i < vol; ++i) {
             other[i] = !G.active[i] && (G.refined[i] || G.under_coarse[i]);
-            if (!near[i] || G.active[i]) continue;
+            if (!near[i] || G.active[i] || (!G.solid.empty() && G.solid[i])) continue;
             if (G.under_coarse[i]) ghost[l][i] = 1;
             else if (!G.refined[i])
                 throw std::invalid_argument("multires: active region has an uncovered neighbor");
@@ -421,6 +436,27 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
         }
         VOXL_CUDA(cudaMalloc(&V->full, std::max(1, nb)));
         VOXL_CUDA(cudaMemcpy(V->full, full.data(), nb, cudaMemcpyHostToDevice));
+        if (!G.solid.empty()) {
+            // obstacle extension: solid bits per ext block, and the blocks whose
+            // active cells can pull from a solid cell (box neighbourhood)
+            const auto near_solid = box_dilate(G.solid, d);
+            std::vector<std::uint64_t> sm(std::size_t(nb) * W, 0);
+            std::vector<std::uint8_t> ns(nb, 0);
+            for (int b = 0; b < nb; ++b) {
+                const auto& o = bg.blocks()[b].origin;
+                for (int local = 0; local < BV; ++local) {
+                    const int x = o[0] + local % E, y = o[1] + (local / E) % E, z = o[2] + local / (E * E);
+                    if (x >= d[0] || y >= d[1] || z >= d[2]) continue;
+                    const std::int64_t i = lin3(d, x, y, z);
+                    if (G.solid[i]) sm[std::size_t(b) * W + (local >> 6)] |= 1ull << (local & 63);
+                    if (G.active[i] && near_solid[i]) ns[b] = 1;
+                }
+            }
+            VOXL_CUDA(cudaMalloc(&V->smask, sm.size() * sizeof(std::uint64_t)));
+            VOXL_CUDA(cudaMemcpy(V->smask, sm.data(), sm.size() * sizeof(std::uint64_t), cudaMemcpyHostToDevice));
+            VOXL_CUDA(cudaMalloc(&V->nsolid, std::max(1, nb)));
+            VOXL_CUDA(cudaMemcpy(V->nsolid, ns.data(), nb, cudaMemcpyHostToDevice));
+        }
         V->n_all = int(all.size());
         V->n_uni = int(uni.size());
         V->n_jump = int(jmp.size());
@@ -514,6 +550,8 @@ MultiResEngine::~MultiResEngine() {
         cudaFree(V->amask);
         cudaFree(V->cls);
         cudaFree(V->full);
+        cudaFree(V->smask);
+        cudaFree(V->nsolid);
         cudaFree(V->org);
         cudaFree(V->all_blocks);
         cudaFree(V->uni_blocks);
@@ -652,6 +690,8 @@ MresArgs<L::Q, R> level_args(const MresConfig& cfg, MultiResEngine::Level* V, in
     A.cls = V->cls;
     A.org = V->org;
     A.full = V->full;
+    A.smask = V->smask;
+    A.nsolid = V->nsolid;
     for (int a = 0; a < 3; ++a) A.n[a] = V->n[a];
     const double inv_tau = V->inv_tau;
     A.omega = R(inv_tau);

@@ -39,6 +39,9 @@ struct MresConfig {
     Precision precision = Precision::F32;
     int edge = 8;
     bool reference_tables = false;
+    /// Obstacle extension (not in the reference): level-map entries of
+    /// MresGrid::kSolidCell are solid, bounce-back cells inside the finest level.
+    bool allow_solid = false;
 };
 
 struct MresTimes {

@@ -67,7 +67,7 @@ int MresGrid::jump_distance(int l, int x, int y, int z) const {
 }
 
 MresGrid MresGrid::build(std::array<int, 3> vdom, int levels, int lattice, const std::int32_t* map, double tau,
-                         bool reference_tables) {
+                         bool reference_tables, bool allow_solid) {
     // multires.cpp:54-192
     const LatticeTable lat = make_lattice(lattice);
     const int dim = lat.dim;
@@ -84,18 +84,42 @@ MresGrid MresGrid::build(std::array<int, 3> vdom, int levels, int lattice, const
     g.lattice_ = lattice;
     g.levels_.resize(levels);
     const auto offsets = box_offsets(dim);
+    std::int64_t n_solid = 0;
     for (int z = 0; z < vdom[2]; ++z)
         for (int y = 0; y < vdom[1]; ++y)
             for (int x = 0; x < vdom[0]; ++x) {
                 const int l = map[lin3(vdom, x, y, z)];
+                if (allow_solid && l == kSolidCell) {
+                    ++n_solid;
+                    continue;
+                }
                 if (l < 0 || l >= levels) throw std::invalid_argument("multires: level id out of range");
                 for (const auto& d : offsets) {
                     const int a = x + d[0], b = y + d[1], c = z + d[2];
                     if (!inside(vdom, a, b, c)) continue;
-                    if (std::abs(map[lin3(vdom, a, b, c)] - l) > 1)
-                        throw std::invalid_argument("multires: resolution jump skips a level");
+                    const int ln = map[lin3(vdom, a, b, c)];
+                    if (allow_solid && ln == kSolidCell) continue;
+                    if (std::abs(ln - l) > 1) throw std::invalid_argument("multires: resolution jump skips a level");
                 }
             }
+    if (n_solid) {
+        // every cell within kSolidMargin of a solid cell is finest-level or solid
+        const int m = kSolidMargin, mz = dim == 3 ? m : 0;
+        for (int z = 0; z < vdom[2]; ++z)
+            for (int y = 0; y < vdom[1]; ++y)
+                for (int x = 0; x < vdom[0]; ++x) {
+                    if (map[lin3(vdom, x, y, z)] != kSolidCell) continue;
+                    for (int c = std::max(0, z - mz); c <= std::min(vdom[2] - 1, z + mz); ++c)
+                        for (int b = std::max(0, y - m); b <= std::min(vdom[1] - 1, y + m); ++b)
+                            for (int a = std::max(0, x - m); a <= std::min(vdom[0] - 1, x + m); ++a) {
+                                const int ln = map[lin3(vdom, a, b, c)];
+                                if (ln != 0 && ln != kSolidCell)
+                                    throw std::invalid_argument(
+                                        "multires: solid cells must lie inside the finest level, 3 cells from any "
+                                        "coarser cell");
+                            }
+                }
+    }
     for (int l = 0; l < levels; ++l) {
         MresLevel& L = g.levels_[l];
         const int s = 1 << l;
@@ -123,6 +147,11 @@ MresGrid MresGrid::build(std::array<int, 3> vdom, int levels, int lattice, const
                 }
         if (L.num_active == 0) throw std::invalid_argument("multires: every level must have active cells");
         L.ref_blocks = BlockGrid::build(L.domain, L.active.data(), 4);
+        if (l == 0 && n_solid) {
+            L.solid.assign(vol, 0);
+            for (std::size_t i = 0; i < vol; ++i) L.solid[i] = map[i] == kSolidCell;
+            L.num_solid = n_solid;
+        }
     }
     g.levels_[levels - 1].tau = tau;
     for (int l = levels - 2; l >= 0; --l) g.levels_[l].tau = 2.0 * g.levels_[l + 1].tau - 0.5;
@@ -167,7 +196,7 @@ MresGrid MresGrid::build(std::array<int, 3> vdom, int levels, int lattice, const
                         const int a = x + d[0], bb = y + d[1], c = z + d[2];
                         if (!inside(L.domain, a, bb, c)) continue;
                         const std::size_t i = std::size_t(lin3(L.domain, a, bb, c));
-                        if (L.active[i]) continue;
+                        if (L.active[i] || (!L.solid.empty() && L.solid[i])) continue;
                         if (L.under_coarse[i]) {
                             if (seen[i]) continue;
                             seen[i] = 1;

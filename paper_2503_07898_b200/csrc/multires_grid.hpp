@@ -37,7 +37,9 @@ struct MresLevel {
     std::vector<std::uint8_t> active;        // level cells, x fastest
     std::vector<std::uint8_t> refined;       // covered by the finer level
     std::vector<std::uint8_t> under_coarse;  // parent active at the coarser level
+    std::vector<std::uint8_t> solid;         // obstacle cells (extension; level 0 only, else empty)
     std::int64_t num_active = 0;
+    std::int64_t num_solid = 0;
     // reference tables (edge-4 block order)
     BlockGrid ref_blocks;                 // edge 4, active cells only
     std::vector<MresGhost> ghosts;        // multires.cpp:350-368
@@ -51,8 +53,16 @@ public:
     /// level_of_cell: virtual finest domain, x fastest, values in [0, levels).
     /// reference_tables: also build the edge-4 ghost / pull / fusion tables in
     /// the reference's scan order (O(active x 26); off for large grids).
+    /// allow_solid (extension beyond the reference, whose build rejects any id
+    /// outside [0, levels), multires.cpp:84-85): kSolidCell marks obstacle
+    /// cells. They must sit inside the finest level with a margin of
+    /// kSolidMargin finest cells to every coarser cell, so no coarse cell,
+    /// ghost or coalesced pull ever covers one; fluid cells pulling from a
+    /// solid cell bounce back (halfway, like the domain walls).
+    static constexpr int kSolidCell = -1;
+    static constexpr int kSolidMargin = 3;
     static MresGrid build(std::array<int, 3> virtual_domain, int levels, int lattice, const std::int32_t* level_of_cell,
-                          double tau_coarsest, bool reference_tables = true);
+                          double tau_coarsest, bool reference_tables = true, bool allow_solid = false);
     bool has_reference_tables() const { return ref_tables_; }
 
     int num_levels() const { return int(levels_.size()); }

@@ -27,7 +27,7 @@ def band_level_map(domain, levels, axis=2) -> np.ndarray:
     return out
 
 
-def _desc(domain, levels, tau, lid_u, fused, precision, block_edge, lattice, reference_tables):
+def _desc(domain, levels, tau, lid_u, fused, precision, block_edge, lattice, reference_tables, solid_cells=False):
     d = _capi.MresDesc()
     d.lattice = LATTICES[lattice]
     d.nx, d.ny = domain[0], domain[1]
@@ -39,17 +39,38 @@ def _desc(domain, levels, tau, lid_u, fused, precision, block_edge, lattice, ref
     d.precision = {"fp32": 0, "fp64": 1}[precision] if isinstance(precision, str) else int(precision)
     d.block_edge = block_edge
     d.reference_tables = int(reference_tables)
+    d.solid_cells = int(solid_cells)
     return d
+
+
+SOLID = -1  # level-map value of an obstacle cell (voxl_mres_desc::solid_cells)
+
+
+def obstacle_band_level_map(domain, levels, radius=None, center=None):
+    """The band cavity of run_multires with a solid sphere in the finest band
+    (extension: the reference's multires has no obstacle cells). Default
+    sphere: centre (nx/2, ny/2, 3 nz/4) - 1/2, radius nz/10; cells with
+    |x - c| <= r become SOLID."""
+    nx, ny, nz = domain
+    m = band_level_map(domain, levels, 2).reshape(nz, ny, nx)
+    r = nz / 10.0 if radius is None else float(radius)
+    c = (nx / 2 - 0.5, ny / 2 - 0.5, 0.75 * nz - 0.5) if center is None else center
+    z = np.arange(nz)[:, None, None]
+    y = np.arange(ny)[None, :, None]
+    x = np.arange(nx)[None, None, :]
+    solid = (x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2 <= r * r
+    m[solid] = SOLID
+    return m.reshape(-1)
 
 
 class MultiResPlan:
     """Host tables at the reference's edge-4 granularity (no device)."""
 
-    def __init__(self, domain=(32, 32, 32), levels=3, level_map=None, tau=0.56, lattice="D3Q19"):
+    def __init__(self, domain=(32, 32, 32), levels=3, level_map=None, tau=0.56, lattice="D3Q19", solid_cells=False):
         if level_map is None:
             level_map = band_level_map(domain, levels, 2 if len(domain) == 3 else 1)
         lm = np.ascontiguousarray(level_map, np.int32)
-        d = _desc(domain, levels, tau, (0.05, 0, 0), True, "fp64", 4, lattice, True)
+        d = _desc(domain, levels, tau, (0.05, 0, 0), True, "fp64", 4, lattice, True, solid_cells)
         self._h = C.c_void_p()
         check(lib.voxl_mres_plan_create(C.byref(d), lm.ctypes.data, C.byref(self._h)))
         self.levels = levels
@@ -105,11 +126,12 @@ class MultiResPlan:
 
 class MultiResEngine:
     def __init__(self, domain=(32, 32, 32), levels=3, level_map=None, tau=0.56, lid_u=(0.05, 0.0, 0.0),
-                 fused=True, precision="fp32", block_edge=8, lattice="D3Q19", reference_tables=False):
+                 fused=True, precision="fp32", block_edge=8, lattice="D3Q19", reference_tables=False,
+                 solid_cells=False):
         if level_map is None:
             level_map = band_level_map(domain, levels, 2)
         lm = np.ascontiguousarray(level_map, np.int32)
-        d = _desc(domain, levels, tau, lid_u, fused, precision, block_edge, lattice, reference_tables)
+        d = _desc(domain, levels, tau, lid_u, fused, precision, block_edge, lattice, reference_tables, solid_cells)
         self.q = Q_OF[lattice]
         self.levels = levels
         self._h = C.c_void_p()

@@ -204,3 +204,57 @@ def test_total_mass_and_probe_vs_reference():
     m, s = O.port_probe("D3Q19", ref.state())
     d = e.probe()
     assert abs(d.mass - m) <= 1e-12 * m and abs(d.max_speed - s) <= 1e-14
+
+
+# ---- obstacle extension (solid cells in the finest level; PARITY UNPINNED vs the
+# reference, whose MultiResGrid::build rejects them -- checked against the oracle's
+# restatement with the same halfway bounce-back rule as the domain walls) ----------
+
+from paper_2503_07898_b200.multires import SOLID, obstacle_band_level_map  # noqa: E402
+
+
+def test_obstacle_map_validation():
+    dom = (32, 32, 32)
+    lm = obstacle_band_level_map(dom, 3)
+    assert (lm == SOLID).sum() > 0
+    # without the extension flag the map is rejected exactly like the reference
+    with pytest.raises(V.VoxlInvalidArgument, match="level id out of range"):
+        V.MultiResPlan(dom, 3, level_map=lm)
+    p = V.MultiResPlan(dom, 3, level_map=lm, solid_cells=True)
+    assert p.level(0)["num_active"] == 32 * 32 * 16 - int((lm == SOLID).sum())
+    # a solid cell closer than 3 cells to a coarser cell is rejected
+    near = obstacle_band_level_map(dom, 3, radius=2.0, center=(15.5, 15.5, 17.0))
+    with pytest.raises(V.VoxlInvalidArgument, match="solid cells must lie inside the finest level"):
+        V.MultiResPlan(dom, 3, level_map=near, solid_cells=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("levels", [2, 3])
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("edge", [4, 8])
+def test_obstacle_fp64_bitwise_vs_oracle(levels, fused, edge):
+    dom = (32, 32, 32)
+    lm = obstacle_band_level_map(dom, levels)
+    ref = _oracle(dom, levels, 3, level_map=lm)
+    e = V.MultiResEngine(dom, levels, level_map=lm, fused=fused, precision="fp64", block_edge=edge,
+                         solid_cells=True)
+    e.step(3)
+    out = e.get_state()
+    assert out.size == ref.size
+    assert np.array_equal(out, ref), np.abs(out - ref).max()
+
+
+@pytest.mark.gpu
+def test_obstacle_off_centre_sphere_and_fp32():
+    dom = (64, 64, 64)
+    lm = obstacle_band_level_map(dom, 3, radius=7.3, center=(21.2, 40.7, 47.1))
+    ref = _oracle(dom, 3, 2, level_map=lm)
+    e = V.MultiResEngine(dom, 3, level_map=lm, fused=True, precision="fp64", solid_cells=True)
+    e.step(2)
+    assert np.array_equal(e.get_state(), ref)
+    e32 = V.MultiResEngine(dom, 3, level_map=lm, fused=True, precision="fp32", solid_cells=True)
+    e64 = V.MultiResEngine(dom, 3, level_map=lm, fused=True, precision="fp64", solid_cells=True)
+    e32.step(20)
+    e64.step(20)
+    a, b = e64.get_state(), e32.get_state()
+    assert (np.abs(a - b) / np.abs(a)).max() <= 1e-5

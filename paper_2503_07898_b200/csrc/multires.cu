@@ -105,7 +105,9 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
 template <int E>
 constexpr int kSplit = E == 8 ? 2 : 1;
 
-template <class L, class R, bool Exact, int E, bool COLLIDE>
+/// SOLID: the level has obstacle cells (a separate instantiation, so grids
+/// without them keep the register budget of the plain kernel).
+template <class L, class R, bool Exact, int E, bool COLLIDE, bool SOLID>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4) ? 6 : 1)
     mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W, S = kSplit<E>;
@@ -126,12 +128,40 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
         s_inner = o[0] > 0 && o[1] > 0 && o[2] > 0 && o[0] + E < A.n[0] && o[1] + E < A.n[1] && o[2] + E < A.n[2];
     }
     if (tid == (BV / S > 64 ? 64 : 33)) s_full = A.full[b];
-    if (tid == (BV / S > 64 ? 96 : 34)) s_solid = A.nsolid ? A.nsolid[b] : 0;
+    if constexpr (SOLID) {
+        if (tid == (BV / S > 64 ? 96 : 34)) s_solid = A.nsolid[b];
+    }
     __syncthreads();
     if (!s_full && !((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
-    if (s_solid) mres_pull_body<L, R, Exact, E, COLLIDE, false, true>(A, b, t, s_src);
-    else if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true, false>(A, b, t, s_src);
+    if constexpr (SOLID) {
+        if (s_solid) {
+            mres_pull_body<L, R, Exact, E, COLLIDE, false, true>(A, b, t, s_src);
+            return;
+        }
+    }
+    if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true, false>(A, b, t, s_src);
     else mres_pull_body<L, R, Exact, E, COLLIDE, false, false>(A, b, t, s_src);
+}
+
+/// Pull over blocks [begin, begin + count): the part below `n_plain` (blocks
+/// that cannot see a solid cell) runs the plain kernel, the rest the
+/// solid-aware one when the level has obstacle cells.
+template <class L, class R, bool Exact, int E, bool COLLIDE>
+void launch_pull(MresArgs<L::Q, R> A, int begin, int count, int n_plain, cudaStream_t st) {
+    const dim3 block(E * E * E / kSplit<E>);
+    const int split = std::min(begin + count, std::max(begin, n_plain));
+    const std::uint8_t* ns = A.nsolid;
+    if (split > begin) {
+        A.block_begin = begin;
+        A.nsolid = nullptr;
+        mres_pull_kernel<L, R, Exact, E, COLLIDE, false><<<(split - begin) * kSplit<E>, block, 0, st>>>(A);
+    }
+    if (begin + count > split) {
+        A.block_begin = split;
+        A.nsolid = ns;
+        if (ns) mres_pull_kernel<L, R, Exact, E, COLLIDE, true><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
+        else mres_pull_kernel<L, R, Exact, E, COLLIDE, false><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
+    }
 }
 
 template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER, bool SOLID>
@@ -311,6 +341,7 @@ struct MultiResEngine::Level {
     int* uni_blocks = nullptr;
     int* jump_blocks = nullptr;
     int n_all = 0, n_uni = 0, n_jump = 0;
+    int n_plain = 0;  // blocks [0, n_plain) are uniform and never pull from a solid cell
     std::int64_t* explode_dst = nullptr;  // ghost cells of this level
     std::int64_t* explode_src = nullptr;  // parent slots at level + 1
     int n_ghost = 0;
@@ -408,15 +439,31 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
             if (full_out) *full_out = full;
             return any ? (cross ? kJump : kUniform) : kNone;
         };
+        // obstacle extension: does an active cell of the block have a solid box
+        // neighbour (the only blocks that need the solid-aware pull)?
+        const std::vector<std::uint8_t> near_solid =
+            G.solid.empty() ? std::vector<std::uint8_t>() : box_dilate(G.solid, d);
+        auto touches_solid = [&](const BlockGrid& bg, int b) {
+            if (near_solid.empty()) return false;
+            const auto& o = bg.blocks()[b].origin;
+            for (int local = 0; local < BV; ++local) {
+                const int x = o[0] + local % E, y = o[1] + (local / E) % E, z = o[2] + local / (E * E);
+                if (x >= d[0] || y >= d[1] || z >= d[2]) continue;
+                const std::int64_t i = lin3(d, x, y, z);
+                if (G.active[i] && near_solid[i]) return true;
+            }
+            return false;
+        };
         {
-            std::vector<int> perm(nb);
-            std::vector<std::uint8_t> c0(nb);
+            // order: uniform, uniform next to a solid, jump, ghost/ring-only
+            std::vector<int> perm(nb), rk(nb);
             for (int b = 0; b < nb; ++b) {
                 perm[b] = b;
-                c0[b] = classify(V->ext, b, nullptr, nullptr);
+                const auto c = classify(V->ext, b, nullptr, nullptr);
+                rk[b] = c == kUniform ? (touches_solid(V->ext, b) ? 1 : 0) : (c == kJump ? 2 : 3);
             }
-            auto rank = [&](int b) { return c0[b] == kUniform ? 0 : (c0[b] == kJump ? 1 : 2); };
-            std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return rank(x) < rank(y); });
+            std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return rk[x] < rk[y]; });
+            V->n_plain = int(std::count(rk.begin(), rk.end(), 0));
             V->ext.permute(perm);
         }
         const BlockGrid& bg = V->ext;
@@ -437,19 +484,17 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
         VOXL_CUDA(cudaMalloc(&V->full, std::max(1, nb)));
         VOXL_CUDA(cudaMemcpy(V->full, full.data(), nb, cudaMemcpyHostToDevice));
         if (!G.solid.empty()) {
-            // obstacle extension: solid bits per ext block, and the blocks whose
-            // active cells can pull from a solid cell (box neighbourhood)
-            const auto near_solid = box_dilate(G.solid, d);
+            // obstacle extension: solid bits per ext block, and the per-block
+            // flag of the solid-aware pull
             std::vector<std::uint64_t> sm(std::size_t(nb) * W, 0);
             std::vector<std::uint8_t> ns(nb, 0);
             for (int b = 0; b < nb; ++b) {
                 const auto& o = bg.blocks()[b].origin;
+                ns[b] = touches_solid(bg, b);
                 for (int local = 0; local < BV; ++local) {
                     const int x = o[0] + local % E, y = o[1] + (local / E) % E, z = o[2] + local / (E * E);
                     if (x >= d[0] || y >= d[1] || z >= d[2]) continue;
-                    const std::int64_t i = lin3(d, x, y, z);
-                    if (G.solid[i]) sm[std::size_t(b) * W + (local >> 6)] |= 1ull << (local & 63);
-                    if (G.active[i] && near_solid[i]) ns[b] = 1;
+                    if (G.solid[lin3(d, x, y, z)]) sm[std::size_t(b) * W + (local >> 6)] |= 1ull << (local & 63);
                 }
             }
             VOXL_CUDA(cudaMalloc(&V->smask, sm.size() * sizeof(std::uint64_t)));
@@ -740,8 +785,7 @@ void MultiResEngine::launch_stream(int l, bool jump_only) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        A.block_begin = jump_only ? V->n_uni : 0;
-        mres_pull_kernel<L, R, X, E, false><<<nb * kSplit<E>, E * E * E / kSplit<E>, 0, stream_>>>(A);  // post -> nxt
+        launch_pull<L, R, X, E, false>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, stream_);  // post -> nxt
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTStream, b);
@@ -761,10 +805,9 @@ void MultiResEngine::gather_uniform(int l) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        A.block_begin = 0;
         A.post = static_cast<R*>(V->post[V->parity ^ 1]);
         A.nxt = static_cast<R*>(V->cur);
-        mres_pull_kernel<L, R, X, E, false><<<V->n_uni * kSplit<E>, E * E * E / kSplit<E>, 0, stream_>>>(A);
+        launch_pull<L, R, X, E, false>(A, 0, V->n_uni, V->n_plain, stream_);
     });
     VOXL_CUDA(cudaGetLastError());
 }
@@ -809,9 +852,8 @@ void MultiResEngine::launch_fused(int l) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        A.block_begin = 0;
         A.nxt = static_cast<R*>(V->post[V->parity ^ 1]);  // post[p] -> post[p^1]
-        mres_pull_kernel<L, R, X, E, true><<<V->n_uni * kSplit<E>, E * E * E / kSplit<E>, 0, stream_>>>(A);
+        launch_pull<L, R, X, E, true>(A, 0, V->n_uni, V->n_plain, stream_);
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTFused, b);

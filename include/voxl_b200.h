@@ -126,6 +126,11 @@ int voxl_dense_get_canonical(voxl_dense* h, double* host);
 /** Planes [k_begin, k_end) of the partition axis only (chunked I/O). */
 int voxl_dense_set_planes(voxl_dense* h, const double* host, int k_begin, int k_end);
 int voxl_dense_get_planes(voxl_dense* h, double* host, int k_begin, int k_end);
+/** Digest of to_canonical() computed on the device (no host copy of the field):
+ *  out[0] = sum_i h(i, bits(x_i)) mod 2^64, out[1] = xor_i rotl(h, 29),
+ *  h(i, b) = splitmix64(b ^ splitmix64(i)), i = canonical element index.
+ *  Equal digests <=> bitwise-equal canonical states (full-size parity checks). */
+int voxl_dense_digest(voxl_dense* h, uint64_t* out2);
 /** n x step_occ(a, b, GatherKernel) (partition.hpp:173) then error check. */
 int voxl_dense_step(voxl_dense* h, int n);
 /** Enqueue n steps on the engine stream; no host synchronisation. */
@@ -211,6 +216,8 @@ int voxl_sparse_report_json(voxl_sparse* h, char* out, int64_t cap, int64_t* len
 /** canonical_state / set_state (sparse.cpp:416-453): pack_coord order, q per voxel. */
 int voxl_sparse_get_state(voxl_sparse* h, double* canonical);
 int voxl_sparse_set_state(voxl_sparse* h, const double* canonical);
+/** Digest of canonical_state() on the device (see voxl_dense_digest). */
+int voxl_sparse_digest(voxl_sparse* h, uint64_t* out2);
 int voxl_sparse_set_equilibrium(voxl_sparse* h, double rho, const double* u);
 /** n x SparseLbmEngine::step (sparse.cpp:386-394). */
 int voxl_sparse_step(voxl_sparse* h, int n);
@@ -257,6 +264,8 @@ int voxl_mres_state_len(voxl_mres* h, int64_t* len);
  *  first, cells sorted by pack_coord, q populations each. */
 int voxl_mres_get_state(voxl_mres* h, double* canonical);
 int voxl_mres_set_state(voxl_mres* h, const double* canonical);
+/** Digest of canonical_state() on the device (see voxl_dense_digest). */
+int voxl_mres_digest(voxl_mres* h, uint64_t* out2);
 int voxl_mres_set_equilibrium(voxl_mres* h, double rho, const double* u);
 /** probe_field over canonical_state (solver.cpp:345). */
 int voxl_mres_probe(voxl_mres* h, voxl_diag* out);

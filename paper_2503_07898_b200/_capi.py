@@ -90,6 +90,7 @@ def _load():
         "voxl_dense_destroy": ([vp], C.c_int),
         "voxl_dense_set_canonical": ([vp, vp], C.c_int),
         "voxl_dense_get_canonical": ([vp, vp], C.c_int),
+        "voxl_dense_digest": ([vp, vp], C.c_int),
         "voxl_dense_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
         "voxl_dense_set_planes": ([vp, vp, C.c_int, C.c_int], C.c_int),
         "voxl_dense_get_planes": ([vp, vp, C.c_int, C.c_int], C.c_int),
@@ -128,6 +129,7 @@ def _load():
         "voxl_sparse_arrangement": ([vp, vp, vp, vp, C.POINTER(i64)], C.c_int),
         "voxl_sparse_report_json": ([vp, cp, i64, C.POINTER(i64)], C.c_int),
         "voxl_sparse_get_state": ([vp, vp], C.c_int),
+        "voxl_sparse_digest": ([vp, vp], C.c_int),
         "voxl_sparse_set_state": ([vp, vp], C.c_int),
         "voxl_sparse_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
         "voxl_sparse_step": ([vp, C.c_int], C.c_int),
@@ -145,6 +147,7 @@ def _load():
         "voxl_mres_timed_steps": ([vp, C.c_int, vp], C.c_int),
         "voxl_mres_state_len": ([vp, C.POINTER(i64)], C.c_int),
         "voxl_mres_get_state": ([vp, vp], C.c_int),
+        "voxl_mres_digest": ([vp, vp], C.c_int),
         "voxl_mres_set_state": ([vp, vp], C.c_int),
         "voxl_mres_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
         "voxl_mres_probe": ([vp, C.POINTER(Diag)], C.c_int),

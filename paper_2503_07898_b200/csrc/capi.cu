@@ -205,6 +205,15 @@ int voxl_dense_get_canonical(voxl_dense* h, double* host) {
     return guarded([&] { h->eng->get_canonical(host); });
 }
 
+int voxl_dense_digest(voxl_dense* h, uint64_t* out2) {
+    return guarded([&] {
+        unsigned long long d[2];
+        h->eng->digest(d);
+        out2[0] = d[0];
+        out2[1] = d[1];
+    });
+}
+
 int voxl_dense_set_planes(voxl_dense* h, const double* host, int k0, int k1) {
     return guarded([&] { h->eng->set_canonical_planes(host, k0, k1); });
 }
@@ -464,6 +473,15 @@ int voxl_sparse_get_state(voxl_sparse* h, double* canonical) {
     return guarded([&] { SP(h)->get_state(canonical); });
 }
 
+int voxl_sparse_digest(voxl_sparse* h, uint64_t* out2) {
+    return guarded([&] {
+        unsigned long long d[2];
+        SP(h)->digest(d);
+        out2[0] = d[0];
+        out2[1] = d[1];
+    });
+}
+
 int voxl_sparse_set_state(voxl_sparse* h, const double* canonical) {
     return guarded([&] { SP(h)->set_state(canonical); });
 }
@@ -615,6 +633,15 @@ int voxl_mres_state_len(voxl_mres* h, int64_t* len) {
 
 int voxl_mres_get_state(voxl_mres* h, double* c) {
     return guarded([&] { MR(h)->get_state(c); });
+}
+
+int voxl_mres_digest(voxl_mres* h, uint64_t* out2) {
+    return guarded([&] {
+        unsigned long long d[2];
+        MR(h)->digest(d);
+        out2[0] = d[0];
+        out2[1] = d[1];
+    });
 }
 
 int voxl_mres_set_state(voxl_mres* h, const double* c) {

@@ -8,6 +8,7 @@
 // algorithmic traffic is 2*Q*sizeof(real) bytes per lattice update (152 B for
 // D3Q19 fp32), the HBM roofline of this operator.
 #include "dense.cuh"
+#include "digest.cuh"
 #include "lattice.cuh"
 
 #include <algorithm>
@@ -196,15 +197,36 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
         if (live) {
             double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
             bool bad = false;
-            static_for<Q>([&](auto I) {
-                constexpr int i = decltype(I)::value;
-                const double fi = double(f[i]) + (Exact ? 0.0 : L::w(i));
-                bad = bad || !(fabs(fi) <= 1e3);
-                r += fi;
-                mx = acc_term<double, false, L::ex(i)>(mx, fi);
-                my = acc_term<double, false, L::ey(i)>(my, fi);
-                mz = acc_term<double, false, L::ez(i)>(mz, fi);
-            });
+            if constexpr (Exact || sizeof(R) == 8) {
+                static_for<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    const double fi = double(f[i]) + (Exact ? 0.0 : L::w(i));
+                    bad = bad || !(fabs(fi) <= 1e3);
+                    r += fi;
+                    mx = acc_term<double, false, L::ex(i)>(mx, fi);
+                    my = acc_term<double, false, L::ey(i)>(my, fi);
+                    mz = acc_term<double, false, L::ez(i)>(mz, fi);
+                });
+            } else {
+                // fp32 shifted storage g = f - w: moments of the O(u) values in
+                // fp32 (sum w_i = 1, sum w_i e_i = 0), promoted once per voxel.
+                // 19 fp32 adds instead of 19 F2F.F64 conversions + fp64 adds,
+                // which made the fused probe 36 % slower than the plain step.
+                R dr = R(0), px = R(0), py = R(0), pz = R(0);
+                static_for<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    constexpr float hi = float(1e3 - L::w(i)), lo = float(-1e3 - L::w(i));
+                    bad = bad || !(f[i] <= R(hi) && f[i] >= R(lo));  // |g + w| <= 1e3, NaN-safe
+                    dr += f[i];
+                    px = acc_term<R, false, L::ex(i)>(px, f[i]);
+                    py = acc_term<R, false, L::ey(i)>(py, f[i]);
+                    pz = acc_term<R, false, L::ez(i)>(pz, f[i]);
+                });
+                r = 1.0 + double(dr);
+                mx = double(px);
+                my = double(py);
+                mz = double(pz);
+            }
             mass = r;
             if (bad || !(r > 0.0)) {
                 const unsigned long long canon =
@@ -460,16 +482,53 @@ __global__ void __launch_bounds__(kProbeThreads) probe_kernel(const R* buf, cons
     }
 }
 
-__global__ void probe_final_kernel(const double* partial, int n, double* out) {
-    // fixed-order reduction: deterministic run to run
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double m = 0.0, v = 0.0;
-        for (int i = 0; i < n; ++i) {
-            m += partial[2 * i];
-            v = fmax(v, partial[2 * i + 1]);
+/// Fixed-order reduction of n (mass, max) partials by one 256-thread block:
+/// thread j sums the contiguous slice j, then a fixed pairwise tree. (A single
+/// thread walking the partials serialises one L2 round trip per element:
+/// ~0.35 ms for 592 partials.) Deterministic run to run.
+__device__ __forceinline__ void block_reduce_partials(const double* partial, int n, double& m_out, double& v_out) {
+    __shared__ double sm[256], sv[256];
+    const int per = (n + 255) / 256;
+    const int lo = threadIdx.x * per, hi = min(n, lo + per);
+    double m = 0.0, v = 0.0;
+    for (int i = lo; i < hi; ++i) {
+        m += partial[2 * i];
+        v = fmax(v, partial[2 * i + 1]);
+    }
+    sm[threadIdx.x] = m;
+    sv[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sm[threadIdx.x] += sm[threadIdx.x + w];
+            sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + w]);
         }
+        __syncthreads();
+    }
+    m_out = sm[0];
+    v_out = sv[0];
+}
+
+__global__ void __launch_bounds__(256) probe_final_kernel(const double* partial, int n, double* out) {
+    double m, v;
+    block_reduce_partials(partial, n, m, v);
+    if (threadIdx.x == 0) {
         out[0] += m;
         out[1] = fmax(out[1], v);
+    }
+}
+
+/// step_probe's last kernel: the fixed-order final reduction, written with the
+/// device error flag into one 4-word row ({mass, max |u|^2, bad voxel bits,
+/// error step}) so the host reads the whole diagnostics row with one copy.
+__global__ void __launch_bounds__(256) step_probe_final_kernel(const double* partial, int n, double* row,
+                                                               const int* error_flag) {
+    double m, v;
+    block_reduce_partials(partial, n, m, v);
+    if (threadIdx.x == 0) {
+        row[0] = m;
+        row[1] = v;
+        reinterpret_cast<long long*>(row)[3] = *error_flag;
     }
 }
 
@@ -679,7 +738,7 @@ struct DenseOps {
         A.n = g.n;
         A.kg0 = g.kg0;
         probe_kernel<L, R><<<kProbeBlocks, kProbeThreads, 0, st>>>(static_cast<const R*>(buf), A, partial, bad);
-        probe_final_kernel<<<1, 32, 0, st>>>(partial, kProbeBlocks, out);
+        probe_final_kernel<<<1, 256, 0, st>>>(partial, kProbeBlocks, out);
         VOXL_CUDA(cudaGetLastError());
     }
 };
@@ -850,6 +909,7 @@ DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg) {
     VOXL_CUDA(cudaMemcpyAsync(error_flag_, &big, sizeof(int), cudaMemcpyHostToDevice, stream_));
     diag_scratch_len_ = 2 * kProbeBlocks + 4;
     VOXL_CUDA(cudaMalloc(&diag_scratch_, diag_scratch_len_ * sizeof(double)));
+    VOXL_CUDA(cudaMallocHost(&diag_row_host_, 4 * sizeof(double)));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -860,6 +920,7 @@ DenseEngine::~DenseEngine() {
             for (void* b : p.buf) cudaFree(b);
     cudaFree(error_flag_);
     cudaFree(diag_scratch_);
+    if (diag_row_host_) cudaFreeHost(diag_row_host_);
     if (diag_partials_) cudaFree(diag_partials_);
     if (staging_) cudaFree(staging_);
     if (flags_ && distributed_) cudaFree(flags_);
@@ -893,7 +954,7 @@ void DenseEngine::attach_peer(int p, void* b0, void* b1) {
     parts_[p].buf[1] = b1;
 }
 
-void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_device) {
+void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_device, unsigned long long* digest) {
     join_streams();
     const std::int64_t s = maps_[0].cross_section();
     const std::size_t plane_bytes = std::size_t(s) * q_ * sizeof(double);
@@ -908,7 +969,7 @@ void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_d
     }
     for (int k0 = k_begin; k0 < k_end; k0 += chunk) {
         const int k1 = std::min(k_end, k0 + chunk);
-        double* hchunk = host + std::size_t(k0 - k_begin) * s * q_;
+        double* hchunk = host ? host + std::size_t(k0 - k_begin) * s * q_ : nullptr;
         const std::size_t bytes = std::size_t(k1 - k0) * plane_bytes;
         if (to_device)
             VOXL_CUDA(cudaMemcpyAsync(staging_, hchunk, bytes, cudaMemcpyHostToDevice, stream_));
@@ -922,7 +983,10 @@ void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_d
                                      stream_);
             });
         }
-        if (!to_device)
+        if (!to_device && digest)
+            digest_accumulate(static_cast<const double*>(staging_), (long long)(k1 - k0) * s * q_,
+                              (long long)k0 * s * q_, digest, stream_);
+        else if (!to_device)
             VOXL_CUDA(cudaMemcpyAsync(hchunk, staging_, bytes, cudaMemcpyDeviceToHost, stream_));
         VOXL_CUDA(cudaStreamSynchronize(stream_));
     }
@@ -949,6 +1013,22 @@ void DenseEngine::set_canonical(const double* host) {
     // refreshes them. Do the same refresh here for the single-process engine
     // (multi-process engines refresh through their shared-layer stores).
     if (cfg_.local_partitions == cfg_.partitions) halo_copy(0);
+}
+
+void DenseEngine::digest(unsigned long long out[2]) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int p = 0; p < cfg_.partitions; ++p)
+        if (local(p)) {
+            lo = std::min(lo, decomp_.slabs[p].first);
+            hi = std::max(hi, decomp_.slabs[p].second);
+        }
+    unsigned long long* acc = nullptr;
+    VOXL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&acc), 2 * sizeof(unsigned long long), stream_));
+    VOXL_CUDA(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), stream_));
+    scatter_gather(nullptr, lo, hi, false, acc);
+    VOXL_CUDA(cudaMemcpyAsync(out, acc, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaFreeAsync(acc, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void DenseEngine::set_equilibrium(double rho, const double u[3]) {
@@ -1182,25 +1262,28 @@ DenseDiag DenseEngine::step_probe() {
         VOXL_CUDA(cudaMalloc(&diag_partials_, 2 * ctas * sizeof(double)));
         diag_partials_len_ = std::size_t(2 * ctas);
     }
+    // One memset, the step (with the fused probe partials), two reduction
+    // kernels and one 32-byte copy of the diagnostics row into pinned memory:
+    // a single host round trip per step, as run() needs (solver.cpp:245-255).
     double* stage = diag_scratch_;
-    double* out = diag_scratch_ + 2 * kProbeBlocks;
-    auto* bad = reinterpret_cast<unsigned long long*>(diag_scratch_ + 2 * kProbeBlocks + 2);
-    const double zero[2] = {0.0, 0.0};
-    const unsigned long long none = ~0ull;
-    VOXL_CUDA(cudaMemcpyAsync(out, zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
-    VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
+    double* row = diag_scratch_ + 2 * kProbeBlocks;
+    auto* bad = reinterpret_cast<unsigned long long*>(row + 2);
+    VOXL_CUDA(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), stream_));
     DiagTarget dt;
     dt.partial = diag_partials_;
     dt.bad = bad;
     launch_step(&dt);
     diag_reduce_kernel<<<kProbeBlocks, 256, 0, stream_>>>(diag_partials_, dt.offset, stage);
-    probe_final_kernel<<<1, 32, 0, stream_>>>(stage, kProbeBlocks, out);
+    step_probe_final_kernel<<<1, 256, 0, stream_>>>(stage, kProbeBlocks, row, error_flag_);
     VOXL_CUDA(cudaGetLastError());
-    double res[2];
-    unsigned long long b = 0;
-    VOXL_CUDA(cudaMemcpyAsync(res, out, sizeof res, cudaMemcpyDeviceToHost, stream_));
-    VOXL_CUDA(cudaMemcpyAsync(&b, bad, sizeof b, cudaMemcpyDeviceToHost, stream_));
-    check_errors();
+    VOXL_CUDA(cudaMemcpyAsync(diag_row_host_, row, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    const double* res = diag_row_host_;
+    const unsigned long long b = reinterpret_cast<const unsigned long long*>(res)[2];
+    const long long flag = reinterpret_cast<const long long*>(res)[3];
+    if (flag != INT_MAX)
+        throw InstabilityError("run aborted at step " + std::to_string(flag) +
+                               ": macroscopic: non-positive density");
     DenseDiag d;
     d.mass = res[0];
     d.max_speed = std::sqrt(res[1]);

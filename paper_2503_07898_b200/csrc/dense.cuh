@@ -99,6 +99,9 @@ public:
     /// Same, over global axis planes [k_begin, k_end) only (chunked I/O).
     void set_canonical_planes(const double* host, int k_begin, int k_end);
     void get_canonical_planes(double* host, int k_begin, int k_end);
+    /// Digest (digest.cuh) of the canonical state of the owned slabs,
+    /// computed on the device: full-size parity without a host copy.
+    void digest(unsigned long long out[2]);
 
     /// Advance n steps (step_occ x n). Throws InstabilityError if the device
     /// reported a non-positive density / non-finite moment.
@@ -164,6 +167,7 @@ private:
     cudaStream_t stream_ = nullptr;
     int* error_flag_ = nullptr;
     double* diag_scratch_ = nullptr;
+    double* diag_row_host_ = nullptr;  // pinned: step_probe's diagnostics row
     double* diag_partials_ = nullptr;
     std::size_t diag_partials_len_ = 0;
     std::size_t diag_scratch_len_ = 0;
@@ -186,7 +190,7 @@ private:
     }
     void launch_step(struct DiagTarget* diag = nullptr);
     void launch_step_distributed(struct DiagTarget* diag);
-    void scatter_gather(double* host, int k_begin, int k_end, bool to_device);
+    void scatter_gather(double* host, int k_begin, int k_end, bool to_device, unsigned long long* digest = nullptr);
 };
 
 } // namespace voxl_b200

@@ -1,6 +1,7 @@
 // multires.cu -- multi-resolution kernels and engine (see multires.cuh).
 #include "multires.cuh"
 #include "lattice.cuh"
+#include "digest.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -678,7 +679,19 @@ void MultiResEngine::set_state(const double* canonical) {
     load_uniform_post();
 }
 
-void MultiResEngine::get_state(double* canonical) {
+void MultiResEngine::get_state(double* canonical) { read_state(canonical, nullptr); }
+
+void MultiResEngine::digest(unsigned long long out[2]) {
+    unsigned long long* acc = nullptr;
+    VOXL_CUDA(cudaMalloc(reinterpret_cast<void**>(&acc), 2 * sizeof(unsigned long long)));
+    VOXL_CUDA(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), stream_));
+    read_state(nullptr, acc);
+    VOXL_CUDA(cudaMemcpyAsync(out, acc, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(acc);
+}
+
+void MultiResEngine::read_state(double* canonical, unsigned long long* digest) {
     // canonical_state (multires.cpp:578-598): levels finest first
     sync_state();
     const LatticeTable t = make_lattice(cfg_.lattice);
@@ -700,7 +713,10 @@ void MultiResEngine::get_state(double* canonical) {
             else mres_io_kernel<27, float, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
         }
         VOXL_CUDA(cudaGetLastError());
-        VOXL_CUDA(cudaMemcpyAsync(canonical + off, st, n * q_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        if (digest)
+            digest_accumulate(st, n * q_, off, digest, stream_);
+        else
+            VOXL_CUDA(cudaMemcpyAsync(canonical + off, st, n * q_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         VOXL_CUDA(cudaStreamSynchronize(stream_));
         cudaFree(st);
         off += n * q_;

@@ -62,6 +62,8 @@ public:
     void set_equilibrium(double rho, const double u[3]);
     void set_state(const double* canonical);
     void get_state(double* canonical);
+    /// Device digest (digest.cuh) of the canonical state (levels finest first).
+    void digest(unsigned long long out[2]);
     void coarse_step(int n);
     MresTimes timed_steps(int n);
     DenseDiag probe();
@@ -73,6 +75,7 @@ public:
     void check_errors();
 
     struct Level;
+    void read_state(double* canonical, unsigned long long* digest);
 
 private:
     MresConfig cfg_;

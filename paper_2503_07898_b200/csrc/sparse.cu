@@ -11,6 +11,7 @@
 // bytes per block of metadata (L2-resident, < 0.2 % at E = 8).
 #include "sparse.cuh"
 #include "lattice.cuh"
+#include "digest.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -543,6 +544,24 @@ void SparseEngine::set_state(const double* canonical) {
 }
 
 void SparseEngine::get_state(double* canonical) {
+    const long long n = stage_canonical();
+    VOXL_CUDA(cudaMemcpyAsync(canonical, d_staging_, std::size_t(n) * q_ * sizeof(double), cudaMemcpyDeviceToHost,
+                              stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void SparseEngine::digest(unsigned long long out[2]) {
+    const long long n = stage_canonical();
+    unsigned long long* acc = nullptr;
+    VOXL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&acc), 2 * sizeof(unsigned long long), stream_));
+    VOXL_CUDA(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), stream_));
+    digest_accumulate(d_staging_, n * q_, 0, acc, stream_);
+    VOXL_CUDA(cudaMemcpyAsync(out, acc, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaFreeAsync(acc, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+long long SparseEngine::stage_canonical() {
     ensure_slots();
     const long long n = grid_.num_active();
     const std::size_t len = std::size_t(n) * q_;
@@ -559,8 +578,7 @@ void SparseEngine::get_state(double* canonical) {
             static_cast<R*>(buf_[cur_]), d_staging_, d_slots_, n, grid_.block_volume(), A);
         VOXL_CUDA(cudaGetLastError());
     });
-    VOXL_CUDA(cudaMemcpyAsync(canonical, d_staging_, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
-    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    return n;
 }
 
 void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l) {

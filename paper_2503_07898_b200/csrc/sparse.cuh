@@ -56,6 +56,8 @@ public:
     /// fastest), q populations each (sparse.cpp:416-453).
     void set_state(const double* canonical);
     void get_state(double* canonical);
+    /// Device digest (digest.cuh) of the canonical state.
+    void digest(unsigned long long out[2]);
     void step(int n);
     /// Identity sweeps (sparse.cpp:396-404): state unchanged, report unchanged.
     void step_identity(int n);
@@ -93,6 +95,7 @@ private:
 
     void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l);
     void ensure_slots();
+    long long stage_canonical();  // canonical fp64 state -> d_staging_; returns active voxels
 };
 
 } // namespace voxl_b200

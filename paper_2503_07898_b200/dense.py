@@ -150,11 +150,34 @@ class DenseEngine:
         uu = (C.c_double * 3)(*u)
         check(lib.voxl_dense_set_equilibrium(self._h, rho, uu))
 
+    def digest(self) -> tuple[int, int]:
+        """Device digest of the canonical state (csrc/digest.cuh; host restatement
+        in digest.py): equal iff the canonical states are bitwise equal."""
+        out = (C.c_uint64 * 2)()
+        check(lib.voxl_dense_digest(self._h, out))
+        return int(out[0]), int(out[1])
+
     def get_canonical(self, out: np.ndarray | None = None) -> np.ndarray:
         if out is None:
             out = np.empty(self.voxels * self.q, np.float64)
         check(lib.voxl_dense_get_canonical(self._h, out.ctypes.data))
         return out
+
+    def _plane_elems(self) -> int:
+        axis2d = self.lattice == "D2Q9"
+        return self.domain[0] * (1 if axis2d else self.domain[1]) * self.q
+
+    def get_canonical_planes(self, k_begin: int, k_end: int) -> np.ndarray:
+        """Canonical fp64 values of partition-axis planes [k_begin, k_end)."""
+        out = np.empty((k_end - k_begin) * self._plane_elems(), np.float64)
+        check(lib.voxl_dense_get_planes(self._h, out.ctypes.data, k_begin, k_end))
+        return out
+
+    def set_canonical_planes(self, values: np.ndarray, k_begin: int, k_end: int) -> None:
+        v = np.ascontiguousarray(values, np.float64)
+        if v.size != (k_end - k_begin) * self._plane_elems():
+            raise ValueError("set_canonical_planes: size mismatch")
+        check(lib.voxl_dense_set_planes(self._h, v.ctypes.data, k_begin, k_end))
 
     def step(self, n: int = 1) -> None:
         check(lib.voxl_dense_step(self._h, n))

@@ -150,6 +150,13 @@ class MultiResEngine:
         check(lib.voxl_mres_state_len(self._h, C.byref(n)))
         return n.value
 
+    def digest(self) -> tuple[int, int]:
+        """Device digest of the canonical state (csrc/digest.cuh; host restatement
+        in digest.py): equal iff the canonical states are bitwise equal."""
+        out = (C.c_uint64 * 2)()
+        check(lib.voxl_mres_digest(self._h, out))
+        return int(out[0]), int(out[1])
+
     def get_state(self):
         out = np.empty(self.state_len(), np.float64)
         check(lib.voxl_mres_get_state(self._h, out.ctypes.data))

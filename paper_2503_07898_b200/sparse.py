@@ -152,6 +152,13 @@ class SparseEngine:
     def report_json(self) -> str:
         return self.plan().report_json()
 
+    def digest(self) -> tuple[int, int]:
+        """Device digest of the canonical state (csrc/digest.cuh; host restatement
+        in digest.py): equal iff the canonical states are bitwise equal."""
+        out = (C.c_uint64 * 2)()
+        check(lib.voxl_sparse_digest(self._h, out))
+        return int(out[0]), int(out[1])
+
     def get_state(self) -> np.ndarray:
         out = np.empty(self.num_active * self.q, np.float64)
         check(lib.voxl_sparse_get_state(self._h, out.ctypes.data))

@@ -168,10 +168,15 @@ def test_step_probe_equals_step_plus_probe(precision, parts):
     b = V.DenseEngine(domain=(24, 20, 18), precision=precision, partitions=parts)
     a.set_canonical(init)
     b.set_canonical(init)
+    # fp64: same values, only the summation order differs. fp32: the fused
+    # probe forms each voxel's moments from the shifted fp32 populations in
+    # fp32 (probe() promotes every population to fp64 first), so the
+    # diagnostics row agrees to fp32 moment rounding.
+    tol_m, tol_u = (1e-12, 1e-12) if precision == "fp64" else (1e-9, 1e-6)
     for _ in range(7):
         da = a.step_probe()
         b.step(1)
         db = b.probe()
-        assert abs(da.mass - db.mass) <= 1e-12 * db.mass
-        assert abs(da.max_speed - db.max_speed) <= 1e-12
+        assert abs(da.mass - db.mass) <= tol_m * db.mass
+        assert abs(da.max_speed - db.max_speed) <= tol_u * db.max_speed + 1e-12
     assert np.array_equal(a.get_canonical(), b.get_canonical())

@@ -9,6 +9,7 @@
 // D3Q19 fp32), the HBM roofline of this operator.
 #include "dense.cuh"
 #include "digest.cuh"
+#include "host_pool.hpp"
 #include "lattice.cuh"
 
 #include <algorithm>
@@ -29,6 +30,13 @@ struct DiagTarget {
 namespace {
 
 constexpr int kBlock = 256;  // 256-thread CTAs: +4 % DRAM throughput over 128 on B200 (tools/micro/membw.cu)
+#ifndef VOXL_DIAG_WARP
+#define VOXL_DIAG_WARP 1
+#endif
+#ifndef VOXL_DIAG_MINB
+#define VOXL_DIAG_MINB 6
+#endif
+constexpr int kDiagSlots = VOXL_DIAG_WARP ? kBlock / 32 : 1;  // fused-probe partial slots per CTA
 
 template <int Q, class R>
 struct StepArgs {
@@ -70,18 +78,79 @@ __device__ __forceinline__ R ld_ro(const R* p) {
     return __ldg(p);
 }
 
+/// probe_field's per-voxel terms (lbm.cpp:116-138) for the fused probe, from
+/// the moments the collision just computed: BGK conserves rho and rho*u, so
+/// the post-collision mass and velocity equal the pre-collision ones up to
+/// rounding (<= 1 ulp of the moment sums; the probe's tolerance is 1e-12
+/// relative in fp64). Reusing them keeps the probing step kernel near the
+/// plain kernel's register and instruction budget (a second set of
+/// post-collision moment sums in fp64 cost 16 registers, 6 -> 4 resident CTAs
+/// per SM and 27 % of the step). The instability test |f_i| <= 1e3 still runs
+/// on the post-collision values.
+///   fp64 (P = double): m = rho, v = |u|^2.
+///   fp32 shifted storage (P = float): m = dr = rho - 1 (the caller adds the
+///   live-voxel count in fp64), v = |u|^2 in fp32. A max-|g| screen (one
+///   FMNMX per population) replaces the per-population two-sided bounds; only
+///   a voxel that fails it (|g| > 999, rho <= 0 or a non-finite moment) takes
+///   the exact test, so the verdict is the reference's.
+template <class L, class R, bool Exact, class P>
+__device__ __forceinline__ void probe_voxel(const R (&f)[L::Q], R rho, R dr, const R (&u)[3], P& m, P& v,
+                                            bool& bad) {
+    if constexpr (Exact || sizeof(R) == 8) {
+        bool b = false;
+        static_for<L::Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            const double fi = double(f[i]) + (Exact ? 0.0 : L::w(i));
+            b = b || !(fabs(fi) <= 1e3);
+        });
+        m = Exact ? double(rho) : 1.0 + double(dr);
+        if (b || !(m > 0.0)) {
+            bad = true;
+        } else {
+            const double ux = double(u[0]), uy = double(u[1]), uz = double(u[2]);
+            v = ux * ux + uy * uy + uz * uz;
+        }
+    } else {
+        float mx = 0.0f;
+        static_for<L::Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            mx = fmaxf(mx, fabsf(f[i]));
+        });
+        const float v2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+        m = dr;
+        if (!(mx <= 999.0f) || !(rho > 0.0f) || !(v2 <= 1e30f)) {
+            bool b = !(1.0 + double(dr) > 0.0);
+            static_for<L::Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr float hi = float(1e3 - L::w(i)), lo = float(-1e3 - L::w(i));
+                b = b || !(f[i] <= R(hi) && f[i] >= R(lo));  // |g + w| <= 1e3, NaN-safe
+            });
+            if (b) {
+                bad = true;
+                return;
+            }
+        }
+        v = v2;
+    }
+}
+
 /// Fused pull-stream + bounce-back/lid + BGK for one voxel per thread
 /// (gather_pull lbm.hpp:40-74 then bgk_relax lattice.cpp:131-138).
 /// AXIS is the partition axis (2 in 3D, 1 in 2D); `a` is x, `b` the remaining
 /// cross-section axis, `k` the local coordinate along AXIS.
 template <class L, class R, bool Exact, bool AOS, int AXIS, bool WRAP, bool DIAG>
-__global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constant__ StepArgs<L::Q, R> A) {
+__global__ void __launch_bounds__(kBlock, (DIAG && sizeof(R) == 4) ? VOXL_DIAG_MINB : 0) dense_step_kernel(const __grid_constant__ StepArgs<L::Q, R> A) {
     constexpr int Q = L::Q;
     constexpr int OTHER = AXIS == 2 ? 1 : 2;
     using Ar = Arith<R, Exact>;
     const int a = blockIdx.x * kBlock + threadIdx.x;
     R f[Q];
     const bool live = a < A.na;
+    // fused probe_field (DIAG): per-voxel mass and |u|^2 of this step's
+    // result, and the instability test on the post-collision populations
+    using P = std::conditional_t<Exact || sizeof(R) == 8, double, float>;
+    P dg_mass = P(0), dg_v2 = P(0);
+    bool dg_bad = false;
     if (live) [&] {
     const int b = blockIdx.y;
     const int k = A.k_first + int(blockIdx.z) * A.k_step;
@@ -112,10 +181,11 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
                 f[i] = ld_ro(reinterpret_cast<const R*>(base_in + A.fast_in_off[i]));
             });
             bool ok = true;
-            R rho, u[3];
+            R rho, u[3], dr = R(0);
             if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
-            else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok);
+            else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok, DIAG ? &dr : nullptr);
             if (!ok) atomicMin(A.error_flag, A.step);
+            if constexpr (DIAG) probe_voxel<L, R, Exact, P>(f, rho, dr, u, dg_mass, dg_v2, dg_bad);
             char* base_out = reinterpret_cast<char*>(A.out) + A.fast_base + (long long)lin * (VS * sizeof(R));
             static_for<Q>([&](auto I) {
                 constexpr int i = decltype(I)::value;
@@ -160,10 +230,11 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
     });
 
     bool ok = true;
-    R rho, u[3];
+    R rho, u[3], dr = R(0);
     if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
-    else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok);
+    else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok, DIAG ? &dr : nullptr);
     if (!ok) atomicMin(A.error_flag, A.step);
+    if constexpr (DIAG) probe_voxel<L, R, Exact, P>(f, rho, dr, u, dg_mass, dg_v2, dg_bad);
 
     static_for<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
@@ -189,58 +260,34 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
     if (A.remote_fence && ((k == 0 && A.up_out) || (k == A.n - 1 && A.low_out))) __threadfence_system();
     }();
 
-    // Fused probe_field (lbm.cpp:116-138) on the post-collision values still
-    // in registers: per-CTA mass and max |u| partials (fixed-order reduction
-    // later, so run-to-run deterministic) and the instability flag.
+    // Fused probe_field (lbm.cpp:116-138): the per-voxel terms were taken in
+    // probe_voxel; per-CTA mass and max |u| partials here (fixed-order
+    // reduction later, so run-to-run deterministic) and the instability flag.
     if constexpr (DIAG) {
-        double mass = 0.0, v2 = 0.0;
-        if (live) {
-            double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
-            bool bad = false;
-            if constexpr (Exact || sizeof(R) == 8) {
-                static_for<Q>([&](auto I) {
-                    constexpr int i = decltype(I)::value;
-                    const double fi = double(f[i]) + (Exact ? 0.0 : L::w(i));
-                    bad = bad || !(fabs(fi) <= 1e3);
-                    r += fi;
-                    mx = acc_term<double, false, L::ex(i)>(mx, fi);
-                    my = acc_term<double, false, L::ey(i)>(my, fi);
-                    mz = acc_term<double, false, L::ez(i)>(mz, fi);
-                });
-            } else {
-                // fp32 shifted storage g = f - w: moments of the O(u) values in
-                // fp32 (sum w_i = 1, sum w_i e_i = 0), promoted once per voxel.
-                // 19 fp32 adds instead of 19 F2F.F64 conversions + fp64 adds,
-                // which made the fused probe 36 % slower than the plain step.
-                R dr = R(0), px = R(0), py = R(0), pz = R(0);
-                static_for<Q>([&](auto I) {
-                    constexpr int i = decltype(I)::value;
-                    constexpr float hi = float(1e3 - L::w(i)), lo = float(-1e3 - L::w(i));
-                    bad = bad || !(f[i] <= R(hi) && f[i] >= R(lo));  // |g + w| <= 1e3, NaN-safe
-                    dr += f[i];
-                    px = acc_term<R, false, L::ex(i)>(px, f[i]);
-                    py = acc_term<R, false, L::ey(i)>(py, f[i]);
-                    pz = acc_term<R, false, L::ez(i)>(pz, f[i]);
-                });
-                r = 1.0 + double(dr);
-                mx = double(px);
-                my = double(py);
-                mz = double(pz);
-            }
-            mass = r;
-            if (bad || !(r > 0.0)) {
-                const unsigned long long canon =
-                    (unsigned long long)(A.kg0 + A.k_first + int(blockIdx.z) * A.k_step) * A.s +
-                    (unsigned long long)(blockIdx.y * A.na + a);
-                atomicMin(A.diag_bad, canon << 5);
-            } else {
-                v2 = (mx * mx + my * my + mz * mz) / (r * r);
-            }
+        P pm = dg_mass, pv = dg_v2;
+        if (live && dg_bad) {
+            const unsigned long long canon =
+                (unsigned long long)(A.kg0 + A.k_first + int(blockIdx.z) * A.k_step) * A.s +
+                (unsigned long long)(blockIdx.y * A.na + a);
+            atomicMin(A.diag_bad, canon << 5);
         }
         for (int o = 16; o > 0; o >>= 1) {
-            mass += __shfl_xor_sync(0xffffffffu, mass, o);
-            v2 = fmax(v2, __shfl_xor_sync(0xffffffffu, v2, o));
+            pm += __shfl_xor_sync(0xffffffffu, pm, o);
+            pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
         }
+        double mass = double(pm);
+        const double v2 = double(pv);
+        if constexpr (std::is_same_v<P, float>) mass += double(__popc(__ballot_sync(0xffffffffu, live)));
+        const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#if VOXL_DIAG_WARP
+        // one partial slot per warp: no CTA barrier, so a probing CTA retires
+        // warp by warp like the plain step
+        if ((threadIdx.x & 31) == 0) {
+            const long long slot = (A.diag_offset + blk) * kDiagSlots + (threadIdx.x >> 5);
+            A.diag_partial[2 * slot] = mass;
+            A.diag_partial[2 * slot + 1] = v2;
+        }
+#else
         __shared__ double sm[kBlock / 32], sv[kBlock / 32];
         const int w = threadIdx.x >> 5;
         if ((threadIdx.x & 31) == 0) {
@@ -254,10 +301,10 @@ __global__ void __launch_bounds__(kBlock) dense_step_kernel(const __grid_constan
                 m += sm[j];
                 v = fmax(v, sv[j]);
             }
-            const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
             A.diag_partial[2 * (A.diag_offset + blk)] = m;
             A.diag_partial[2 * (A.diag_offset + blk) + 1] = v;
         }
+#endif
     }
 }
 
@@ -391,8 +438,11 @@ struct CanonArgs {
     int kg0;          // partition's global offset
 };
 
-template <int Q, class R, bool ToDevice>
-__global__ void canon_kernel(R* buf, double* staging, const __grid_constant__ CanonArgs<Q> A) {
+/// S = double: fp64 canonical staging, storage = R(f - shift). S = R (fp32
+/// wire format): the host already applied the same fp64 subtraction and
+/// rounding (HostPool conversion), so the kernel only permutes.
+template <int Q, class R, bool ToDevice, class S = double>
+__global__ void canon_kernel(R* buf, S* staging, const __grid_constant__ CanonArgs<Q> A) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long count = (long long)(A.k_hi - A.k_lo) * A.s;
     if (t >= count) return;
@@ -403,8 +453,13 @@ __global__ void canon_kernel(R* buf, double* staging, const __grid_constant__ Ca
     const long long st = ((long long)(A.kg0 + k - A.kg_stage0) * A.s + cross) * Q;
     for (int c = 0; c < Q; ++c) {
         R* p = buf + A.plane[g][c] + lin * A.vs;
-        if constexpr (ToDevice) *p = R(staging[st + c] - A.shift[c]);
-        else staging[st + c] = double(*p) + A.shift[c];
+        if constexpr (std::is_same_v<S, double>) {
+            if constexpr (ToDevice) *p = R(staging[st + c] - A.shift[c]);
+            else staging[st + c] = double(*p) + A.shift[c];
+        } else {
+            if constexpr (ToDevice) *p = staging[st + c];
+            else staging[st + c] = *p;
+        }
     }
 }
 
@@ -420,6 +475,24 @@ __global__ void fill_kernel(R* buf, const __grid_constant__ CanonArgs<Q> A, cons
     const int g = group_of(k, A.n);
     const long long lin = (long long)(k + 1) * A.s + cross;
     for (int c = 0; c < Q; ++c) buf[A.plane[g][c] + lin * A.vs] = V.lid[c];
+}
+
+template <int Q, class R>
+void launch_canon(unsigned blocks, int threads, R* buf, void* staging, bool wire32, bool to_device,
+                  const CanonArgs<Q>& A, cudaStream_t st) {
+    if (wire32) {
+        if constexpr (sizeof(R) == 4) {
+            if (to_device) canon_kernel<Q, R, true, R><<<blocks, threads, 0, st>>>(buf, static_cast<R*>(staging), A);
+            else canon_kernel<Q, R, false, R><<<blocks, threads, 0, st>>>(buf, static_cast<R*>(staging), A);
+        } else {
+            throw std::logic_error("fp32 wire format on an fp64 engine");
+        }
+    } else {
+        auto* sd = static_cast<double*>(staging);
+        if (to_device) canon_kernel<Q, R, true><<<blocks, threads, 0, st>>>(buf, sd, A);
+        else canon_kernel<Q, R, false><<<blocks, threads, 0, st>>>(buf, sd, A);
+    }
+    VOXL_CUDA(cudaGetLastError());
 }
 
 // ---- diagnostics (probe_field, lbm.cpp:116-138) ------------------------------------
@@ -438,31 +511,31 @@ __global__ void __launch_bounds__(kProbeThreads) probe_kernel(const R* buf, cons
         const int k = int(t / A.s), cross = int(t % A.s);
         const int g = group_of(k, A.n);
         const long long lin = (long long)(k + 1) * A.s + cross;
-        double f[Q];
-        double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
-        bool bad_here = false;
-        int bad_pop = 0;
-        for (int c = 0; c < Q; ++c) {
-            f[c] = double(buf[A.plane[g][c] + lin * A.vs]) + A.shift[c];
-            if (!bad_here && (!isfinite(f[c]) || fabs(f[c]) > 1e3)) {
-                bad_here = true;
-                bad_pop = c;
-            }
-        }
+        // all Q loads issued back to back, then the fp64 moments; |u|^2 with a
+        // single division (max |u| = sqrt(max |u|^2): sqrt is monotone and
+        // correctly rounded, applied once on the host)
+        R raw[Q];
         static_for<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            mass += f[i];
-            r += f[i];
-            mx = acc_term<double, false, L::ex(i)>(mx, f[i]);
-            my = acc_term<double, false, L::ey(i)>(my, f[i]);
-            mz = acc_term<double, false, L::ez(i)>(mz, f[i]);
+            raw[i] = buf[A.plane[g][i] + lin * A.vs];
         });
-        if (bad_here || !(r > 0.0)) {
+        double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+        int bad_pop = -1;
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            const double fi = double(raw[i]) + A.shift[i];
+            if (bad_pop < 0 && !(fabs(fi) <= 1e3)) bad_pop = i;
+            mass += fi;
+            r += fi;
+            mx = acc_term<double, false, L::ex(i)>(mx, fi);
+            my = acc_term<double, false, L::ey(i)>(my, fi);
+            mz = acc_term<double, false, L::ez(i)>(mz, fi);
+        });
+        if (bad_pop >= 0 || !(r > 0.0)) {
             const unsigned long long canon = (unsigned long long)(A.kg0 + k) * A.s + cross;
-            atomicMin(bad, (canon << 5) | (unsigned long long)bad_pop);
+            atomicMin(bad, (canon << 5) | (unsigned long long)(bad_pop < 0 ? 0 : bad_pop));
         } else {
-            const double ux = mx / r, uy = my / r, uz = mz / r;
-            vmax = fmax(vmax, sqrt(ux * ux + uy * uy + uz * uz));
+            vmax = fmax(vmax, (mx * mx + my * my + mz * mz) / (r * r));
         }
     }
     __shared__ double sm[kProbeThreads], sv[kProbeThreads];
@@ -667,7 +740,7 @@ struct DenseOps {
         A.diag_partial = diag ? diag->partial : nullptr;
         A.diag_offset = diag ? diag->offset : 0;
         A.diag_bad = diag ? diag->bad : nullptr;
-        if (diag) diag->offset += (long long)grid.x * grid.y * grid.z;
+        if (diag) diag->offset += (long long)grid.x * grid.y * grid.z;  // CTA index; slots = offset * kDiagSlots
         auto go = [&](auto aos_c, auto wrap_c, auto diag_c) {
             dense_step_kernel<L, R, Exact, decltype(aos_c)::value, AXIS, decltype(wrap_c)::value,
                               decltype(diag_c)::value><<<grid, kBlock, 0, st>>>(A);
@@ -686,8 +759,14 @@ struct DenseOps {
         return (long long)((g.na + kBlock - 1) / kBlock) * g.nb * k_count;
     }
 
-    static void canon(const Decomposition& d, const LayoutMap& m, int p, void* buf, double* staging, int k_lo,
-                      int k_hi, int kg_stage0, bool to_device, cudaStream_t st) {
+    static void host_shift(double* shift) {
+        double sh[Q];
+        fill_shift(sh);
+        for (int c = 0; c < Q; ++c) shift[c] = sh[c];
+    }
+
+    static void canon(const Decomposition& d, const LayoutMap& m, int p, void* buf, void* staging, bool wire32,
+                      int k_lo, int k_hi, int kg_stage0, bool to_device, cudaStream_t st) {
         CanonArgs<Q> A{};
         fill_planes(m, A.plane);
         fill_shift(A.shift);
@@ -704,9 +783,7 @@ struct DenseOps {
         if (count <= 0) return;
         const int threads = 256;
         const unsigned blocks = unsigned((count + threads - 1) / threads);
-        if (to_device) canon_kernel<Q, R, true><<<blocks, threads, 0, st>>>(static_cast<R*>(buf), staging, A);
-        else canon_kernel<Q, R, false><<<blocks, threads, 0, st>>>(static_cast<R*>(buf), staging, A);
-        VOXL_CUDA(cudaGetLastError());
+        launch_canon<Q, R>(blocks, threads, static_cast<R*>(buf), staging, wire32, to_device, A, st);
     }
 
     static void fill(const Decomposition& d, const LayoutMap& m, int p, void* buf, const double* feq,
@@ -775,8 +852,12 @@ struct OperatorOps {
         return (long long)((g.na + kBlock - 1) / kBlock) * g.nb * k_count;
     }
 
-    static void canon(const Decomposition& d, const LayoutMap& m, int p, void* buf, double* staging, int k_lo,
-                      int k_hi, int kg_stage0, bool to_device, cudaStream_t st) {
+    static void host_shift(double* shift) {
+        for (int c = 0; c < Q; ++c) shift[c] = 0.0;
+    }
+
+    static void canon(const Decomposition& d, const LayoutMap& m, int p, void* buf, void* staging, bool wire32,
+                      int k_lo, int k_hi, int kg_stage0, bool to_device, cudaStream_t st) {
         CanonArgs<Q> A{};
         for (int gr = 0; gr < kGroupCount; ++gr)
             for (int c = 0; c < Q; ++c) A.plane[gr][c] = m.plane_offset(gr, c);
@@ -792,9 +873,7 @@ struct OperatorOps {
         const long long count = (long long)(k_hi - k_lo) * g.s;
         if (count <= 0) return;
         const unsigned blocks = unsigned((count + 255) / 256);
-        if (to_device) canon_kernel<Q, R, true><<<blocks, 256, 0, st>>>(static_cast<R*>(buf), staging, A);
-        else canon_kernel<Q, R, false><<<blocks, 256, 0, st>>>(static_cast<R*>(buf), staging, A);
-        VOXL_CUDA(cudaGetLastError());
+        launch_canon<Q, R>(blocks, 256, static_cast<R*>(buf), staging, wire32, to_device, A, st);
     }
 
     static void fill(const Decomposition&, const LayoutMap&, int, void*, const double*, cudaStream_t) {
@@ -923,6 +1002,15 @@ DenseEngine::~DenseEngine() {
     if (diag_row_host_) cudaFreeHost(diag_row_host_);
     if (diag_partials_) cudaFree(diag_partials_);
     if (staging_) cudaFree(staging_);
+    if (host_staging_) cudaFreeHost(host_staging_);
+    if (copy_stream_) {
+        cudaStreamSynchronize(copy_stream_);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(ev_copied_[i]);
+            cudaEventDestroy(ev_laid_[i]);
+        }
+        cudaStreamDestroy(copy_stream_);
+    }
     if (flags_ && distributed_) cudaFree(flags_);
     if (shared_stream_) {
         cudaStreamSynchronize(shared_stream_);
@@ -957,39 +1045,119 @@ void DenseEngine::attach_peer(int p, void* b0, void* b1) {
 void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_device, unsigned long long* digest) {
     join_streams();
     const std::int64_t s = maps_[0].cross_section();
-    const std::size_t plane_bytes = std::size_t(s) * q_ * sizeof(double);
-    // stage at most ~256 MiB of canonical planes at a time
-    int chunk = int(std::max<std::size_t>(1, (std::size_t(256) << 20) / plane_bytes));
+    // fp32 engines move the canonical field over PCIe in the fp32 storage
+    // format: host threads apply the same fp64 shift and rounding the device
+    // would (R(f - w_i) in, double(g) + w_i out), which halves the link bytes.
+    // Bitwise the same field either way.
+    const bool wire32 = esize_ == 4 && host != nullptr && !(digest && !to_device);
+    const std::size_t wsize = wire32 ? sizeof(float) : sizeof(double);
+    const std::size_t plane_bytes = std::size_t(s) * q_ * wsize;
+    // Two staging slots of at most ~64 MiB of canonical planes each: the PCIe
+    // copy of one slot (copy_stream_) overlaps the layout kernel of the other
+    // (stream_) and, on the fp32 wire, the host conversion of the next chunk.
+    int chunk = int(std::max<std::size_t>(1, (std::size_t(64) << 20) / plane_bytes));
     chunk = std::min(chunk, std::max(1, k_end - k_begin));
-    const std::size_t need = std::size_t(chunk) * plane_bytes;
+    const std::size_t slot_elems = std::size_t(chunk) * s * q_;
+    const std::size_t need = 2 * slot_elems * wsize;
     if (staging_bytes_ < need) {
         if (staging_) VOXL_CUDA(cudaFree(staging_));
         VOXL_CUDA(cudaMalloc(&staging_, need));
         staging_bytes_ = need;
     }
-    for (int k0 = k_begin; k0 < k_end; k0 += chunk) {
+    if (wire32 && host_staging_bytes_ < need) {
+        if (host_staging_) VOXL_CUDA(cudaFreeHost(host_staging_));
+        VOXL_CUDA(cudaMallocHost(&host_staging_, need));
+        host_staging_bytes_ = need;
+    }
+    if (!copy_stream_) {
+        VOXL_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            VOXL_CUDA(cudaEventCreateWithFlags(&ev_copied_[i], cudaEventDisableTiming));
+            VOXL_CUDA(cudaEventCreateWithFlags(&ev_laid_[i], cudaEventDisableTiming));
+        }
+    }
+    double shift[27] = {};
+    if (wire32) dispatch(cfg_, [&](auto ops) { decltype(ops)::host_shift(shift); });
+    const int q = q_;
+    // host fp64 canonical <-> pinned fp32 wire slot, on the host pool
+    auto convert = [&](double* h, float* w, std::size_t elems, bool in) {
+        const long long vox = (long long)(elems / q);
+        HostPool::get().parallel_for(vox, [&](long long lo, long long hi) {
+            if (in) io_detail::convert<true>(h, w, lo, hi, shift, q);
+            else io_detail::convert<false>(h, w, lo, hi, shift, q);
+        });
+    };
+    const bool copies = host != nullptr && !(digest && !to_device);
+    if (copies) {  // the copy stream starts after everything already queued on the engine stream
+        VOXL_CUDA(cudaEventRecord(ev_laid_[0], stream_));
+        VOXL_CUDA(cudaStreamWaitEvent(copy_stream_, ev_laid_[0], 0));
+    }
+    auto host_slot = [&](int slot) { return static_cast<float*>(host_staging_) + slot * slot_elems; };
+    int i = 0;
+    int pending_out = -1;  // fp32 wire D2H: chunk whose host conversion is still due
+    double* pending_host = nullptr;
+    std::size_t pending_elems = 0;
+    for (int k0 = k_begin; k0 < k_end; k0 += chunk, ++i) {
         const int k1 = std::min(k_end, k0 + chunk);
+        const int slot = i & 1;
+        char* st = static_cast<char*>(staging_) + slot * slot_elems * wsize;
         double* hchunk = host ? host + std::size_t(k0 - k_begin) * s * q_ : nullptr;
-        const std::size_t bytes = std::size_t(k1 - k0) * plane_bytes;
-        if (to_device)
-            VOXL_CUDA(cudaMemcpyAsync(staging_, hchunk, bytes, cudaMemcpyHostToDevice, stream_));
+        const std::size_t elems = std::size_t(k1 - k0) * s * q_;
+        const std::size_t bytes = elems * wsize;
+        if (to_device) {
+            const void* src = hchunk;
+            if (wire32) {
+                // the slot's previous H2D (chunk i-2) must have left the pinned buffer
+                if (i >= 2) VOXL_CUDA(cudaEventSynchronize(ev_copied_[slot]));
+                convert(hchunk, host_slot(slot), elems, true);
+                src = host_slot(slot);
+            }
+            if (i >= 2) VOXL_CUDA(cudaStreamWaitEvent(copy_stream_, ev_laid_[slot], 0));  // slot consumed
+            VOXL_CUDA(cudaMemcpyAsync(st, src, bytes, cudaMemcpyHostToDevice, copy_stream_));
+            VOXL_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
+            VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_copied_[slot], 0));
+        } else if (copies && i >= 2) {
+            VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_copied_[slot], 0));  // slot drained to the host
+        }
         for (int p = 0; p < cfg_.partitions; ++p) {
             if (!local(p)) continue;
             const int lo = std::max(k0, decomp_.slabs[p].first), hi = std::min(k1, decomp_.slabs[p].second);
             if (lo >= hi) continue;
             dispatch(cfg_, [&](auto ops) {
-                decltype(ops)::canon(decomp_, maps_[p], p, parts_[p].buf[cur_], static_cast<double*>(staging_),
+                decltype(ops)::canon(decomp_, maps_[p], p, parts_[p].buf[cur_], st, wire32,
                                      lo - decomp_.slabs[p].first, hi - decomp_.slabs[p].first, k0, to_device,
                                      stream_);
             });
         }
-        if (!to_device && digest)
-            digest_accumulate(static_cast<const double*>(staging_), (long long)(k1 - k0) * s * q_,
-                              (long long)k0 * s * q_, digest, stream_);
-        else if (!to_device)
-            VOXL_CUDA(cudaMemcpyAsync(hchunk, staging_, bytes, cudaMemcpyDeviceToHost, stream_));
-        VOXL_CUDA(cudaStreamSynchronize(stream_));
+        if (to_device) {
+            VOXL_CUDA(cudaEventRecord(ev_laid_[slot], stream_));
+        } else if (digest) {
+            digest_accumulate(reinterpret_cast<double*>(st), (long long)(k1 - k0) * s * q_, (long long)k0 * s * q_,
+                              digest, stream_);
+        } else {
+            VOXL_CUDA(cudaEventRecord(ev_laid_[slot], stream_));
+            VOXL_CUDA(cudaStreamWaitEvent(copy_stream_, ev_laid_[slot], 0));
+            void* dst = wire32 ? static_cast<void*>(host_slot(slot)) : static_cast<void*>(hchunk);
+            VOXL_CUDA(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyDeviceToHost, copy_stream_));
+            VOXL_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
+            if (wire32) {
+                // widen the previous chunk while this one is gathered and copied
+                if (pending_out >= 0) {
+                    VOXL_CUDA(cudaEventSynchronize(ev_copied_[pending_out]));
+                    convert(pending_host, host_slot(pending_out), pending_elems, false);
+                }
+                pending_out = slot;
+                pending_host = hchunk;
+                pending_elems = elems;
+            }
+        }
     }
+    if (pending_out >= 0) {
+        VOXL_CUDA(cudaEventSynchronize(ev_copied_[pending_out]));
+        convert(pending_host, host_slot(pending_out), pending_elems, false);
+    }
+    if (copies) VOXL_CUDA(cudaStreamSynchronize(copy_stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void DenseEngine::set_canonical_planes(const double* host, int k_begin, int k_end) {
@@ -1257,10 +1425,11 @@ DenseDiag DenseEngine::step_probe() {
         if (local(p))
             dispatch(cfg_,
                      [&](auto ops) { ctas += decltype(ops)::launch_ctas(decomp_, p, decomp_.thickness(p)); });
-    if (diag_partials_len_ < std::size_t(2 * ctas)) {
+    const long long slots = ctas * kDiagSlots;
+    if (diag_partials_len_ < std::size_t(2 * slots)) {
         if (diag_partials_) VOXL_CUDA(cudaFree(diag_partials_));
-        VOXL_CUDA(cudaMalloc(&diag_partials_, 2 * ctas * sizeof(double)));
-        diag_partials_len_ = std::size_t(2 * ctas);
+        VOXL_CUDA(cudaMalloc(&diag_partials_, 2 * slots * sizeof(double)));
+        diag_partials_len_ = std::size_t(2 * slots);
     }
     // One memset, the step (with the fused probe partials), two reduction
     // kernels and one 32-byte copy of the diagnostics row into pinned memory:
@@ -1273,7 +1442,7 @@ DenseDiag DenseEngine::step_probe() {
     dt.partial = diag_partials_;
     dt.bad = bad;
     launch_step(&dt);
-    diag_reduce_kernel<<<kProbeBlocks, 256, 0, stream_>>>(diag_partials_, dt.offset, stage);
+    diag_reduce_kernel<<<kProbeBlocks, 256, 0, stream_>>>(diag_partials_, dt.offset * kDiagSlots, stage);
     step_probe_final_kernel<<<1, 256, 0, stream_>>>(stage, kProbeBlocks, row, error_flag_);
     VOXL_CUDA(cudaGetLastError());
     VOXL_CUDA(cudaMemcpyAsync(diag_row_host_, row, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
@@ -1317,7 +1486,7 @@ DenseDiag DenseEngine::probe() {
     VOXL_CUDA(cudaStreamSynchronize(stream_));
     DenseDiag d;
     d.mass = res[0];
-    d.max_speed = res[1];
+    d.max_speed = std::sqrt(res[1]);  // the kernels reduce |u|^2
     if (b != ~0ull) {
         d.unstable = 1;
         d.bad_voxel = std::int64_t(b >> 5);

@@ -173,6 +173,11 @@ private:
     std::size_t diag_scratch_len_ = 0;
     void* staging_ = nullptr;  // fp64 canonical staging (device)
     std::size_t staging_bytes_ = 0;
+    void* host_staging_ = nullptr;  // pinned fp32 wire slots (scatter_gather, fp32 engines)
+    std::size_t host_staging_bytes_ = 0;
+    cudaStream_t copy_stream_ = nullptr;  // host <-> staging transfers (scatter_gather)
+    cudaEvent_t ev_copied_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_laid_[2] = {nullptr, nullptr};
     std::uint32_t* flags_ = nullptr;
     std::uint32_t* remote_flag_up_ = nullptr;
     std::uint32_t* remote_flag_low_ = nullptr;

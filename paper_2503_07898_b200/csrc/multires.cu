@@ -269,6 +269,76 @@ __global__ void mres_io_kernel(R* buf, double* staging, const std::int64_t* slot
     }
 }
 
+/// probe_field (lbm.cpp:116-138) and total_mass (multires.cpp:600-609) on
+/// the device, over one level's fp64 canonical cells (the staging array
+/// read_state fills): per-CTA partial sums of the populations and max |u|
+/// (u = m / rho, true division, as macroscopic lattice.cpp:115-129), the
+/// first unstable (cell, population) by atomicMin. Fixed grid and fixed
+/// reduction order, so the result is run-to-run deterministic.
+constexpr int kMresProbeBlocks = 296;
+
+template <class L>
+__global__ void __launch_bounds__(256) mres_canon_probe_kernel(const double* st, long long n, long long cell0,
+                                                               double* partial, unsigned long long* bad) {
+    constexpr int Q = L::Q;
+    double mass = 0.0, vmax = 0.0;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
+        const double* f = st + v * Q;
+        double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+        int bp = -1;
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            const double fi = f[i];
+            if (bp < 0 && !(fabs(fi) <= 1e3)) bp = i;
+            r += fi;
+            mx = acc_term<double, false, L::ex(i)>(mx, fi);
+            my = acc_term<double, false, L::ey(i)>(my, fi);
+            mz = acc_term<double, false, L::ez(i)>(mz, fi);
+        });
+        mass += r;
+        if (bp >= 0 || !(r > 0.0)) {
+            atomicMin(bad, ((unsigned long long)(cell0 + v) << 5) | (unsigned long long)(bp < 0 ? 0 : bp));
+        } else {
+            const double ux = mx / r, uy = my / r, uz = mz / r;
+            vmax = fmax(vmax, sqrt(ux * ux + uy * uy + uz * uz));
+        }
+    }
+    __shared__ double sm[256], sv[256];
+    sm[threadIdx.x] = mass;
+    sv[threadIdx.x] = vmax;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sm[threadIdx.x] += sm[threadIdx.x + w];
+            sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = sm[0];
+        partial[2 * blockIdx.x + 1] = sv[0];
+    }
+}
+
+/// out = {sum of all cells, max |u|, sum_l 8^l * level sum (total_mass)}.
+__global__ void mres_probe_final(const double* partial, int levels, int per, double child, double* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double all = 0.0, v = 0.0, weighted = 0.0, vol = 1.0;
+    for (int l = 0; l < levels; ++l) {
+        double lev = 0.0;
+        for (int i = 0; i < per; ++i) {
+            lev += partial[2 * (l * per + i)];
+            v = fmax(v, partial[2 * (l * per + i) + 1]);
+        }
+        all += lev;
+        weighted += lev * vol;
+        vol *= child;
+    }
+    out[0] = all;
+    out[1] = v;
+    out[2] = weighted;
+}
+
 template <class R>
 __global__ void mres_fill_kernel(R* buf, long long total, int bv, int q, const double* val) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -377,6 +447,13 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
         if (!(G.tau > 0.5)) throw std::invalid_argument("multires: derived tau must stay > 0.5");
     }
     VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    {
+        int lo = 0, hi = 0;
+        VOXL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        VOXL_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, hi));
+        VOXL_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        VOXL_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
     std::vector<std::vector<std::uint8_t>> ghost(L), ring(L);
     for (int l = 0; l < L; ++l) {
         const MresLevel& G = grid_.level(l);
@@ -583,7 +660,6 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
     VOXL_CUDA(cudaMalloc(&d_error_, sizeof(int)));
     const int big = INT_MAX;
     VOXL_CUDA(cudaMemcpy(d_error_, &big, sizeof(int), cudaMemcpyHostToDevice));
-    VOXL_CUDA(cudaMalloc(&d_diag_, (2 * 592 + 64) * sizeof(double)));
     const double u0[3] = {0.0, 0.0, 0.0};
     set_equilibrium(1.0, u0);  // multires.cpp:574-575
 }
@@ -611,6 +687,12 @@ MultiResEngine::~MultiResEngine() {
     }
     cudaFree(d_error_);
     cudaFree(d_diag_);
+    if (side_) {
+        cudaStreamSynchronize(side_);
+        cudaEventDestroy(ev_fork_);
+        cudaEventDestroy(ev_join_);
+        cudaStreamDestroy(side_);
+    }
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -658,7 +740,7 @@ void MultiResEngine::set_state(const double* canonical) {
     VOXL_CUDA(cudaMalloc(&d_shift, q_ * sizeof(double)));
     VOXL_CUDA(cudaMemcpy(d_shift, shift.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
     std::int64_t off = 0;
-    for (Level* V : lv_) {
+    for (Level*& V : lv_) {
         const long long n = V->n_active;
         double* st = nullptr;
         VOXL_CUDA(cudaMalloc(&st, std::max<long long>(1, n * q_) * sizeof(double)));
@@ -691,7 +773,7 @@ void MultiResEngine::digest(unsigned long long out[2]) {
     cudaFree(acc);
 }
 
-void MultiResEngine::read_state(double* canonical, unsigned long long* digest) {
+void MultiResEngine::read_state(double* canonical, unsigned long long* digest, double* probe) {
     // canonical_state (multires.cpp:578-598): levels finest first
     sync_state();
     const LatticeTable t = make_lattice(cfg_.lattice);
@@ -701,7 +783,7 @@ void MultiResEngine::read_state(double* canonical, unsigned long long* digest) {
     VOXL_CUDA(cudaMalloc(&d_shift, q_ * sizeof(double)));
     VOXL_CUDA(cudaMemcpy(d_shift, shift.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
     std::int64_t off = 0;
-    for (Level* V : lv_) {
+    for (Level*& V : lv_) {
         const long long n = V->n_active;
         double* st = nullptr;
         VOXL_CUDA(cudaMalloc(&st, std::max<long long>(1, n * q_) * sizeof(double)));
@@ -713,7 +795,19 @@ void MultiResEngine::read_state(double* canonical, unsigned long long* digest) {
             else mres_io_kernel<27, float, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
         }
         VOXL_CUDA(cudaGetLastError());
-        if (digest)
+        if (probe) {
+            const int l = int(&V - lv_.data());
+            double* part = probe + 2 * std::size_t(l) * kMresProbeBlocks;
+            auto* bad = reinterpret_cast<unsigned long long*>(probe + 2 * lv_.size() * kMresProbeBlocks + 3);
+            if (n == 0) {
+                VOXL_CUDA(cudaMemsetAsync(part, 0, 2 * kMresProbeBlocks * sizeof(double), stream_));
+            } else if (q_ == 19) {
+                mres_canon_probe_kernel<D3Q19><<<kMresProbeBlocks, 256, 0, stream_>>>(st, n, off / q_, part, bad);
+            } else {
+                mres_canon_probe_kernel<D3Q27><<<kMresProbeBlocks, 256, 0, stream_>>>(st, n, off / q_, part, bad);
+            }
+            VOXL_CUDA(cudaGetLastError());
+        } else if (digest)
             digest_accumulate(st, n * q_, off, digest, stream_);
         else
             VOXL_CUDA(cudaMemcpyAsync(canonical + off, st, n * q_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
@@ -724,17 +818,17 @@ void MultiResEngine::read_state(double* canonical, unsigned long long* digest) {
     cudaFree(d_shift);
 }
 
-void MultiResEngine::mark_begin(int, cudaEvent_t* b) {
+void MultiResEngine::mark_begin(int, cudaEvent_t* b, cudaStream_t s) {
     if (!events_) return;
     VOXL_CUDA(cudaEventCreate(b));
-    VOXL_CUDA(cudaEventRecord(*b, stream_));
+    VOXL_CUDA(cudaEventRecord(*b, s ? s : stream_));
 }
 
-void MultiResEngine::mark_end(int cls, cudaEvent_t b) {
+void MultiResEngine::mark_end(int cls, cudaEvent_t b, cudaStream_t s) {
     if (!events_) return;
     cudaEvent_t e;
     VOXL_CUDA(cudaEventCreate(&e));
-    VOXL_CUDA(cudaEventRecord(e, stream_));
+    VOXL_CUDA(cudaEventRecord(e, s ? s : stream_));
     events_->push_back({cls, {b, e}});
 }
 
@@ -789,22 +883,23 @@ void MultiResEngine::launch_collide(int l, bool jump_only) {
     mark_end(kTCollide, b);
 }
 
-void MultiResEngine::launch_stream(int l, bool jump_only) {
+void MultiResEngine::launch_stream(int l, bool jump_only, cudaStream_t s) {
     Level* V = lv_[l];
     const int nb = jump_only ? V->n_jump : V->n_all;
     if (nb == 0) return;
+    cudaStream_t st = s ? s : stream_;
     cudaEvent_t b{};
-    mark_begin(kTStream, &b);
+    mark_begin(kTStream, &b, st);
     mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
         using L = decltype(lat);
         using R = decltype(real);
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        launch_pull<L, R, X, E, false>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, stream_);  // post -> nxt
+        launch_pull<L, R, X, E, false>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st);  // post -> nxt
     });
     VOXL_CUDA(cudaGetLastError());
-    mark_end(kTStream, b);
+    mark_end(kTStream, b, st);
 }
 
 void MultiResEngine::gather_uniform(int l) {
@@ -928,9 +1023,19 @@ void MultiResEngine::advance(int l) {
         advance(l - 1);
         launch_coalesce(l);
     }
-    if (cfg_.fused) launch_fused(l);
-    launch_stream(l, cfg_.fused);
     Level* V = lv_[l];
+    if (cfg_.fused && V->n_uni > 0 && V->n_jump > 0) {
+        // jump stream (side stream, high priority) || fused uniform (engine stream)
+        VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
+        VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+        launch_stream(l, true, side_);
+        launch_fused(l);
+        VOXL_CUDA(cudaEventRecord(ev_join_, side_));
+        VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    } else {
+        if (cfg_.fused) launch_fused(l);
+        launch_stream(l, cfg_.fused);
+    }
     std::swap(V->cur, V->nxt);
     if (cfg_.fused) V->parity ^= 1;
     cur_valid_ = false;
@@ -984,49 +1089,55 @@ MresTimes MultiResEngine::timed_steps(int n) {
     return T;
 }
 
-DenseDiag MultiResEngine::probe() {
-    // probe_field over canonical_state (solver.cpp:345): plain sum over all
-    // levels' cells and max |u|; computed on the host copy of the state.
-    std::vector<double> s(static_cast<std::size_t>(state_len()));
-    get_state(s.data());
-    DenseDiag d;
-    const LatticeTable t = make_lattice(cfg_.lattice);
-    for (std::size_t v = 0; v * q_ < s.size(); ++v) {
-        double r = 0, mx = 0, my = 0, mz = 0;
-        for (int i = 0; i < q_; ++i) {
-            const double f = s[v * q_ + i];
-            if (!std::isfinite(f) || std::fabs(f) > 1e3) {
-                if (!d.unstable) {
-                    d.unstable = 1;
-                    d.bad_voxel = std::int64_t(v);
-                    d.bad_population = i;
-                }
-            }
-            d.mass += f;
-            r += f;
-            mx += f * t.e[i][0];
-            my += f * t.e[i][1];
-            mz += f * t.e[i][2];
-        }
-        if (r > 0) d.max_speed = std::max(d.max_speed, std::sqrt(mx * mx + my * my + mz * mz) / r);
+void MultiResEngine::device_probe(double out[3], DenseDiag* d) {
+    // canonical_state per level into device staging, then the reductions on
+    // the device; only the 4-word result row comes back to the host.
+    const std::size_t per_level = 2 * std::size_t(kMresProbeBlocks);
+    const std::size_t need = per_level * lv_.size() + 4;
+    if (diag_len_ < need) {
+        cudaFree(d_diag_);
+        VOXL_CUDA(cudaMalloc(&d_diag_, need * sizeof(double)));
+        diag_len_ = need;
     }
+    double* row = d_diag_ + per_level * lv_.size();
+    VOXL_CUDA(cudaMemsetAsync(row + 3, 0xFF, sizeof(double), stream_));
+    read_state(nullptr, nullptr, d_diag_);
+    mres_probe_final<<<1, 32, 0, stream_>>>(d_diag_, int(lv_.size()), kMresProbeBlocks,
+                                            double(grid_.dim() == 3 ? 8 : 4), row);
+    VOXL_CUDA(cudaGetLastError());
+    double h[4];
+    VOXL_CUDA(cudaMemcpyAsync(h, row, sizeof h, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    out[0] = h[0];
+    out[1] = h[1];
+    out[2] = h[2];
+    if (d) {
+        unsigned long long b;
+        std::memcpy(&b, &h[3], sizeof b);
+        d->mass = h[0];
+        d->max_speed = h[1];
+        if (b != ~0ull) {
+            d->unstable = 1;
+            d->bad_voxel = std::int64_t(b >> 5);
+            d->bad_population = int(b & 31u);
+        }
+    }
+}
+
+DenseDiag MultiResEngine::probe() {
+    // probe_field over canonical_state (solver.cpp:345): sum over all levels'
+    // cells and max |u|, reduced on the device.
+    DenseDiag d;
+    double o[3];
+    device_probe(o, &d);
     return d;
 }
 
 double MultiResEngine::total_mass() {
     // total_mass (multires.cpp:600-609): per-level sums weighted by 8^l
-    std::vector<double> s(static_cast<std::size_t>(state_len()));
-    get_state(s.data());
-    double mass = 0.0;
-    std::size_t off = 0;
-    for (int l = 0; l < grid_.num_levels(); ++l) {
-        double lev = 0.0;
-        const std::size_t n = std::size_t(lv_[l]->n_active) * q_;
-        for (std::size_t i = 0; i < n; ++i) lev += s[off + i];
-        off += n;
-        mass += lev * std::pow(double(grid_.dim() == 3 ? 8 : 4), l);
-    }
-    return mass;
+    double o[3];
+    device_probe(o, nullptr);
+    return o[2];
 }
 
 std::array<std::int64_t, 2> MultiResEngine::fusion_counts(int l) const { return {lv_[l]->n_uni, lv_[l]->n_jump}; }

@@ -75,7 +75,8 @@ public:
     void check_errors();
 
     struct Level;
-    void read_state(double* canonical, unsigned long long* digest);
+    void read_state(double* canonical, unsigned long long* digest, double* probe = nullptr);
+    void device_probe(double out[3], DenseDiag* d);
 
 private:
     MresConfig cfg_;
@@ -84,8 +85,14 @@ private:
     MresGrid grid_;
     std::vector<Level*> lv_;
     cudaStream_t stream_ = nullptr;
+    // fused mode: the jump-block stream runs on a high-priority side stream
+    // concurrently with the fused uniform kernel (both read post[parity]; they
+    // write disjoint buffers: nxt of jump blocks vs post[parity ^ 1]).
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     int* d_error_ = nullptr;
     double* d_diag_ = nullptr;
+    std::size_t diag_len_ = 0;
     int steps_done_ = 0;
     // timing (events around each launch class) when non-null
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* events_ = nullptr;
@@ -97,12 +104,12 @@ private:
     void sync_state();         // cur of every cell valid (fused mode gathers uniform cells)
     void load_uniform_post();  // uniform cells' post = BGK(cur) after a host-side state change
     void launch_collide(int l, bool jump_only);
-    void launch_stream(int l, bool jump_only);
+    void launch_stream(int l, bool jump_only, cudaStream_t s = nullptr);
     void launch_fused(int l);
     void launch_explode(int coarse);
     void launch_coalesce(int coarse);
-    void mark_begin(int cls, cudaEvent_t* b);
-    void mark_end(int cls, cudaEvent_t b);
+    void mark_begin(int cls, cudaEvent_t* b, cudaStream_t s = nullptr);
+    void mark_end(int cls, cudaEvent_t b, cudaStream_t s = nullptr);
 };
 
 } // namespace voxl_b200

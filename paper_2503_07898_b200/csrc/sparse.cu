@@ -394,6 +394,13 @@ SparseEngine::SparseEngine(const SparseConfig& cfg, const std::uint8_t* active) 
     T_ = SparseTables::build(cfg_.domain, active, cfg_.edge, cfg_.strategy, q_);
 
     VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    {
+        int lo = 0, hi = 0;
+        VOXL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        VOXL_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, hi));
+        VOXL_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        VOXL_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
     const std::size_t nb = std::size_t(grid_.num_blocks());
     const std::size_t bytes = nb * q_ * grid_.block_volume() * esize_;
     for (auto& b : buf_) {
@@ -487,6 +494,12 @@ SparseEngine::~SparseEngine() {
     cudaFree(d_staging_);
     cudaFree(d_error_);
     cudaFree(d_diag_);
+    if (side_) {
+        cudaStreamSynchronize(side_);
+        cudaEventDestroy(ev_fork_);
+        cudaEventDestroy(ev_join_);
+        cudaStreamDestroy(side_);
+    }
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -627,15 +640,28 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l) {
                 break;
             case Strategy::DisagMem: {
                 A.vel_source = kVelConst;
+                // boundary blocks [0, n_b) with the heavy kernel on the side
+                // stream, blocks [n_b, nb) with the light kernel on the engine
+                // stream, concurrently; joined before the next step.
                 const int n_b = int(classes_.n_boundary);
+                const bool split = n_b > 0 && n_b < nb;
+                cudaStream_t hs = split ? side_ : stream_;
+                if (split) {
+                    VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
+                    VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+                }
                 A.block_begin = 0;
-                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], stream_));
-                Ops::launch(edge, A, kHeavy, n_b, stream_);
-                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], stream_));
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], hs));
+                if (n_b > 0) Ops::launch(edge, A, kHeavy, n_b, hs);
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], hs));
                 A.block_begin = n_b;
                 if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
-                Ops::launch(edge, A, kLight, nb - n_b, stream_);
+                if (nb > n_b) Ops::launch(edge, A, kLight, nb - n_b, stream_);
                 if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
+                if (split) {
+                    VOXL_CUDA(cudaEventRecord(ev_join_, side_));
+                    VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+                }
                 break;
             }
         }

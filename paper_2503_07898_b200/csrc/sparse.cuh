@@ -92,6 +92,11 @@ private:
     int* d_error_ = nullptr;
     double* d_diag_ = nullptr;
     cudaStream_t stream_ = nullptr;
+    // DisagMem: the boundary (regularized) kernel runs on a high-priority side
+    // stream concurrently with the light kernel (disjoint output blocks, shared
+    // read-only input), so its low-occupancy tail hides under the light sweep.
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
 
     void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l);
     void ensure_slots();

@@ -72,3 +72,17 @@ def test_cpp_dropin_driver_bitwise(tmp_path):
     got = np.fromfile(out, np.float64)
     ref = O.port_dense_run("D3Q19", (16, 16, 16), 0.56, "lid_driven_cavity", (0.05, 0, 0), 20)
     assert np.array_equal(got, ref)
+
+
+def test_host_io_conversion_exact(tmp_path):
+    """fp32 wire-format conversions (host pool + AVX2 streaming stores) equal
+    the scalar fp64 subtract / round / add for all widths and alignments."""
+    import subprocess
+
+    exe = str(tmp_path / "host_io_convert")
+    src = os.path.join(ROOT, "tests", "cpp", "host_io_convert.cpp")
+    inc = os.path.join(ROOT, "paper_2503_07898_b200", "csrc")
+    subprocess.run(["g++", "-O3", "-std=c++17", "-pthread", "-ffp-contract=off", "-I" + inc, src, "-o", exe],
+                   check=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -135,3 +135,25 @@ def test_engine_ledger_equals_plan():
     e = V.DenseEngine(domain=(16, 16, 16), partitions=4, layout="SoA")
     assert [r.__dict__ for r in e.ledger(3)] == [r.__dict__ for r in V.plan_ledger(3, domain=(16, 16, 16),
                                                                                     partitions=4, layout="SoA")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("parts,layout", [(1, "DisagSoA"), (3, "DisagSoA"), (2, "AoS")])
+def test_canonical_io_multichunk_roundtrip(precision, parts, layout):
+    """set_canonical / get_canonical over several pipelined 64 MiB staging
+    chunks (two slots, copy stream, host fp32 wire conversion for fp32): the
+    stored field is exactly R(f - w_i) and reads back as double(g) + w_i."""
+    dom = (256, 256, 40)
+    rng = np.random.default_rng(7)
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    f = (w[None, :] * (1.0 + 0.05 * rng.standard_normal((np.prod(dom), 19)))).reshape(-1)
+    e = V.DenseEngine(domain=dom, precision=precision, partitions=parts, layout=layout)
+    e.set_canonical(f)
+    out = e.get_canonical()
+    e.close()
+    if precision == "fp64":
+        assert np.array_equal(out, f)
+    else:
+        ww = np.tile(w, np.prod(dom))
+        assert np.array_equal(out, (f - ww).astype(np.float32).astype(np.float64) + ww)

@@ -1,6 +1,7 @@
 """Multi-resolution path: host tables vs the reference (CPU) and the CUDA
 engine vs the oracle (GPU; fp64 bitwise for fused and staged schedules)."""
 import json
+import math
 import os
 
 import numpy as np
@@ -201,9 +202,17 @@ def test_total_mass_and_probe_vs_reference():
     e = V.MultiResEngine((32, 32, 32), 3, precision="fp64")
     e.step(3)
     assert abs(e.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
-    m, s = O.port_probe("D3Q19", ref.state())
+    st = ref.state()
+    m, s = O.port_probe("D3Q19", st)
     d = e.probe()
-    assert abs(d.mass - m) <= 1e-12 * m and abs(d.max_speed - s) <= 1e-14
+    # probe_field sums ~3e5 populations sequentially (lbm.cpp:121-130); that
+    # order is itself 2.4e-12 off the exactly rounded sum here. The device
+    # reduces in a fixed tree order: check it against the exact sum, and the
+    # reference's sequential sum within its own rounding.
+    exact = math.fsum(st.tolist())
+    assert abs(d.mass - exact) <= 1e-13 * exact
+    assert abs(d.mass - m) <= 1e-11 * m
+    assert abs(d.max_speed - s) <= 1e-14
 
 
 # ---- obstacle extension (solid cells in the finest level; PARITY UNPINNED vs the
@@ -258,3 +267,18 @@ def test_obstacle_off_centre_sphere_and_fp32():
     e64.step(20)
     a, b = e64.get_state(), e32.get_state()
     assert (np.abs(a - b) / np.abs(a)).max() <= 1e-5
+
+
+@pytest.mark.gpu
+def test_fp32_tolerance_1000_fine_steps():
+    """BASELINE tolerance at its stated horizon: 250 coarse steps of the 3-level
+    band cavity = 1000 finest-level steps, fp32 vs the fp64 engine."""
+    dom = (32, 32, 32)
+    e64 = V.MultiResEngine(dom, 3, fused=True, precision="fp64")
+    e32 = V.MultiResEngine(dom, 3, fused=True, precision="fp32")
+    e64.step(250)
+    e32.step(250)
+    a, b = e64.get_state(), e32.get_state()
+    rel = np.abs(a - b) / np.abs(a)
+    print("multires fp32 max rel err after 1000 finest steps:", rel.max())
+    assert rel.max() <= 1e-5

@@ -210,3 +210,20 @@ def test_probe_matches_oracle():
     d = e.probe()
     assert d.unstable == 0
     assert abs(d.mass - m_ref) <= 1e-12 * m_ref and abs(d.max_speed - s_ref) <= 1e-14
+
+
+@pytest.mark.gpu
+def test_fp32_tolerance_1000_steps():
+    """BASELINE tolerance at its stated horizon: fp32 (shifted storage) vs the
+    fp64 engine (bitwise = reference) after 1000 steps, regularized x-faces and
+    sphere, kernel split."""
+    dom = (48, 32, 32)
+    kw = dict(block_edge=8, strategy="disag_mem")
+    e64 = V.SparseEngine(dom, precision="fp64", **kw)
+    e32 = V.SparseEngine(dom, precision="fp32", **kw)
+    e64.step(1000)
+    e32.step(1000)
+    a, b = e64.get_state(), e32.get_state()
+    rel = np.abs(a - b) / np.abs(a)
+    print("sparse fp32 max rel err after 1000 steps:", rel.max())
+    assert rel.max() <= 1e-5

@@ -3,6 +3,7 @@
 
     python tools/bench_paths.py sparse [--n 256] [--steps 50]
     python tools/bench_paths.py multires [--n 512] [--steps 5]
+    python tools/bench_paths.py dense [--n 512] [--steps 50]
 
 Prints one JSON line per variant: MLUPS (active voxels for sparse; LUP =
 sum_l N_l * 2^(L-1-l) per coarse step for multires) and the fraction of the
@@ -79,11 +80,38 @@ def multires(args):
         e.close()
 
 
+def dense(args):
+    """The dense step across lattice, precision, layout and partition count
+    (the paper's layout study: AoS vs SoA vs DisagSoA; D3Q27 and fp64 at the
+    same size). Bytes/LUP = 2 * Q * sizeof(real)."""
+    import paper_2503_07898_b200 as V
+
+    n = args.n
+    cases = [("D3Q19", "fp32", "DisagSoA", 1), ("D3Q19", "fp32", "SoA", 1), ("D3Q19", "fp32", "AoS", 1),
+             ("D3Q19", "fp32", "DisagSoA", 8), ("D3Q27", "fp32", "DisagSoA", 1), ("D3Q19", "fp64", "DisagSoA", 1)]
+    for lat, prec, layout, parts in cases:
+        q = 19 if lat == "D3Q19" else 27
+        bpl = 2 * q * (4 if prec == "fp32" else 8)
+        e = V.DenseEngine(lattice=lat, domain=(n, n, n), precision=prec, layout=layout, partitions=parts)
+        e.set_equilibrium(1.0, (0.0, 0.0, 0.0))
+        e.timed_steps(args.warmup)
+        total, kern = e.timed_steps(args.steps)
+        vox = n ** 3
+        mlups = vox * args.steps / (total / 1e3) / 1e6
+        gbs = bpl * vox * args.steps / (total / 1e3) / 1e9
+        line = {"path": "dense", "lattice": lat, "precision": prec, "layout": layout, "partitions": parts,
+                "domain": [n] * 3, "bytes_per_lup": bpl, "steps": args.steps,
+                "ms_per_step": round(total / args.steps, 4), "MLUPS": round(mlups, 1), "achieved_GBs": round(gbs, 1),
+                "frac_of_measured_peak": round(gbs / peak(), 4), "frac_of_8TBs": round(gbs / 8000, 4)}
+        print(json.dumps(line), flush=True)
+        e.close()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("path", choices=["sparse", "multires"])
+    ap.add_argument("path", choices=["sparse", "multires", "dense"])
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     a = ap.parse_args()
-    sparse(a) if a.path == "sparse" else multires(a)
+    {"sparse": sparse, "multires": multires, "dense": dense}[a.path](a)

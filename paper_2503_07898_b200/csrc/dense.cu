@@ -9,7 +9,7 @@
 // D3Q19 fp32), the HBM roofline of this operator.
 #include "dense.cuh"
 #include "digest.cuh"
-#include "host_pool.hpp"
+#include "canon_io.cuh"
 #include "lattice.cuh"
 
 #include <algorithm>
@@ -942,7 +942,7 @@ namespace {
 
 // ---- engine ------------------------------------------------------------------------
 
-DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg) {
+DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg), io_(std::make_unique<CanonPipe>()) {
     const OperatorShape shape = operator_shape(cfg_);
     q_ = shape.q;
     axis_ = shape.axis;
@@ -1001,16 +1001,6 @@ DenseEngine::~DenseEngine() {
     cudaFree(diag_scratch_);
     if (diag_row_host_) cudaFreeHost(diag_row_host_);
     if (diag_partials_) cudaFree(diag_partials_);
-    if (staging_) cudaFree(staging_);
-    if (host_staging_) cudaFreeHost(host_staging_);
-    if (copy_stream_) {
-        cudaStreamSynchronize(copy_stream_);
-        for (int i = 0; i < 2; ++i) {
-            cudaEventDestroy(ev_copied_[i]);
-            cudaEventDestroy(ev_laid_[i]);
-        }
-        cudaStreamDestroy(copy_stream_);
-    }
     if (flags_ && distributed_) cudaFree(flags_);
     if (shared_stream_) {
         cudaStreamSynchronize(shared_stream_);
@@ -1045,119 +1035,28 @@ void DenseEngine::attach_peer(int p, void* b0, void* b1) {
 void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_device, unsigned long long* digest) {
     join_streams();
     const std::int64_t s = maps_[0].cross_section();
-    // fp32 engines move the canonical field over PCIe in the fp32 storage
-    // format: host threads apply the same fp64 shift and rounding the device
-    // would (R(f - w_i) in, double(g) + w_i out), which halves the link bytes.
-    // Bitwise the same field either way.
-    const bool wire32 = esize_ == 4 && host != nullptr && !(digest && !to_device);
-    const std::size_t wsize = wire32 ? sizeof(float) : sizeof(double);
-    const std::size_t plane_bytes = std::size_t(s) * q_ * wsize;
-    // Two staging slots of at most ~64 MiB of canonical planes each: the PCIe
-    // copy of one slot (copy_stream_) overlaps the layout kernel of the other
-    // (stream_) and, on the fp32 wire, the host conversion of the next chunk.
-    int chunk = int(std::max<std::size_t>(1, (std::size_t(64) << 20) / plane_bytes));
-    chunk = std::min(chunk, std::max(1, k_end - k_begin));
-    const std::size_t slot_elems = std::size_t(chunk) * s * q_;
-    const std::size_t need = 2 * slot_elems * wsize;
-    if (staging_bytes_ < need) {
-        if (staging_) VOXL_CUDA(cudaFree(staging_));
-        VOXL_CUDA(cudaMalloc(&staging_, need));
-        staging_bytes_ = need;
-    }
-    if (wire32 && host_staging_bytes_ < need) {
-        if (host_staging_) VOXL_CUDA(cudaFreeHost(host_staging_));
-        VOXL_CUDA(cudaMallocHost(&host_staging_, need));
-        host_staging_bytes_ = need;
-    }
-    if (!copy_stream_) {
-        VOXL_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
-        for (int i = 0; i < 2; ++i) {
-            VOXL_CUDA(cudaEventCreateWithFlags(&ev_copied_[i], cudaEventDisableTiming));
-            VOXL_CUDA(cudaEventCreateWithFlags(&ev_laid_[i], cudaEventDisableTiming));
-        }
-    }
+    // rows = canonical planes; fp32 engines use the fp32 wire format (canon_io.cuh)
+    const bool wire32 = esize_ == 4 && host != nullptr;
     double shift[27] = {};
     if (wire32) dispatch(cfg_, [&](auto ops) { decltype(ops)::host_shift(shift); });
-    const int q = q_;
-    // host fp64 canonical <-> pinned fp32 wire slot, on the host pool
-    auto convert = [&](double* h, float* w, std::size_t elems, bool in) {
-        const long long vox = (long long)(elems / q);
-        HostPool::get().parallel_for(vox, [&](long long lo, long long hi) {
-            if (in) io_detail::convert<true>(h, w, lo, hi, shift, q);
-            else io_detail::convert<false>(h, w, lo, hi, shift, q);
-        });
-    };
-    const bool copies = host != nullptr && !(digest && !to_device);
-    if (copies) {  // the copy stream starts after everything already queued on the engine stream
-        VOXL_CUDA(cudaEventRecord(ev_laid_[0], stream_));
-        VOXL_CUDA(cudaStreamWaitEvent(copy_stream_, ev_laid_[0], 0));
-    }
-    auto host_slot = [&](int slot) { return static_cast<float*>(host_staging_) + slot * slot_elems; };
-    int i = 0;
-    int pending_out = -1;  // fp32 wire D2H: chunk whose host conversion is still due
-    double* pending_host = nullptr;
-    std::size_t pending_elems = 0;
-    for (int k0 = k_begin; k0 < k_end; k0 += chunk, ++i) {
-        const int k1 = std::min(k_end, k0 + chunk);
-        const int slot = i & 1;
-        char* st = static_cast<char*>(staging_) + slot * slot_elems * wsize;
-        double* hchunk = host ? host + std::size_t(k0 - k_begin) * s * q_ : nullptr;
-        const std::size_t elems = std::size_t(k1 - k0) * s * q_;
-        const std::size_t bytes = elems * wsize;
-        if (to_device) {
-            const void* src = hchunk;
-            if (wire32) {
-                // the slot's previous H2D (chunk i-2) must have left the pinned buffer
-                if (i >= 2) VOXL_CUDA(cudaEventSynchronize(ev_copied_[slot]));
-                convert(hchunk, host_slot(slot), elems, true);
-                src = host_slot(slot);
-            }
-            if (i >= 2) VOXL_CUDA(cudaStreamWaitEvent(copy_stream_, ev_laid_[slot], 0));  // slot consumed
-            VOXL_CUDA(cudaMemcpyAsync(st, src, bytes, cudaMemcpyHostToDevice, copy_stream_));
-            VOXL_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
-            VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_copied_[slot], 0));
-        } else if (copies && i >= 2) {
-            VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_copied_[slot], 0));  // slot drained to the host
-        }
+    auto layout = [&](long long r0, long long r1, void* slot, bool w32) {
+        const int k0 = k_begin + int(r0), k1 = k_begin + int(r1);
         for (int p = 0; p < cfg_.partitions; ++p) {
             if (!local(p)) continue;
             const int lo = std::max(k0, decomp_.slabs[p].first), hi = std::min(k1, decomp_.slabs[p].second);
             if (lo >= hi) continue;
             dispatch(cfg_, [&](auto ops) {
-                decltype(ops)::canon(decomp_, maps_[p], p, parts_[p].buf[cur_], st, wire32,
+                decltype(ops)::canon(decomp_, maps_[p], p, parts_[p].buf[cur_], slot, w32,
                                      lo - decomp_.slabs[p].first, hi - decomp_.slabs[p].first, k0, to_device,
                                      stream_);
             });
         }
-        if (to_device) {
-            VOXL_CUDA(cudaEventRecord(ev_laid_[slot], stream_));
-        } else if (digest) {
-            digest_accumulate(reinterpret_cast<double*>(st), (long long)(k1 - k0) * s * q_, (long long)k0 * s * q_,
-                              digest, stream_);
-        } else {
-            VOXL_CUDA(cudaEventRecord(ev_laid_[slot], stream_));
-            VOXL_CUDA(cudaStreamWaitEvent(copy_stream_, ev_laid_[slot], 0));
-            void* dst = wire32 ? static_cast<void*>(host_slot(slot)) : static_cast<void*>(hchunk);
-            VOXL_CUDA(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyDeviceToHost, copy_stream_));
-            VOXL_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
-            if (wire32) {
-                // widen the previous chunk while this one is gathered and copied
-                if (pending_out >= 0) {
-                    VOXL_CUDA(cudaEventSynchronize(ev_copied_[pending_out]));
-                    convert(pending_host, host_slot(pending_out), pending_elems, false);
-                }
-                pending_out = slot;
-                pending_host = hchunk;
-                pending_elems = elems;
-            }
-        }
-    }
-    if (pending_out >= 0) {
-        VOXL_CUDA(cudaEventSynchronize(ev_copied_[pending_out]));
-        convert(pending_host, host_slot(pending_out), pending_elems, false);
-    }
-    if (copies) VOXL_CUDA(cudaStreamSynchronize(copy_stream_));
-    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    };
+    auto consume = [&](long long r0, long long r1, void* slot) {
+        digest_accumulate(static_cast<const double*>(slot), (r1 - r0) * s * q_, (k_begin + r0) * s * q_, digest,
+                          stream_);
+    };
+    io_->run(host, k_end - k_begin, s, q_, to_device, wire32, shift, stream_, layout, consume, digest != nullptr);
 }
 
 void DenseEngine::set_canonical_planes(const double* host, int k_begin, int k_end) {

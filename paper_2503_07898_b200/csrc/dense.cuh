@@ -24,6 +24,8 @@
 
 namespace voxl_b200 {
 
+class CanonPipe;
+
 struct DiagTarget;
 enum class Precision : int { F32 = 0, F64 = 1 };
 enum class HaloMode : int { ZeroCopy = 0, Copy = 1 };
@@ -171,13 +173,7 @@ private:
     double* diag_partials_ = nullptr;
     std::size_t diag_partials_len_ = 0;
     std::size_t diag_scratch_len_ = 0;
-    void* staging_ = nullptr;  // fp64 canonical staging (device)
-    std::size_t staging_bytes_ = 0;
-    void* host_staging_ = nullptr;  // pinned fp32 wire slots (scatter_gather, fp32 engines)
-    std::size_t host_staging_bytes_ = 0;
-    cudaStream_t copy_stream_ = nullptr;  // host <-> staging transfers (scatter_gather)
-    cudaEvent_t ev_copied_[2] = {nullptr, nullptr};
-    cudaEvent_t ev_laid_[2] = {nullptr, nullptr};
+    std::unique_ptr<CanonPipe> io_;  // canonical host <-> device pipeline (canon_io.cuh)
     std::uint32_t* flags_ = nullptr;
     std::uint32_t* remote_flag_up_ = nullptr;
     std::uint32_t* remote_flag_low_ = nullptr;

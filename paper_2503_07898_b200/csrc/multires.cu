@@ -2,6 +2,7 @@
 #include "multires.cuh"
 #include "lattice.cuh"
 #include "digest.cuh"
+#include "canon_io.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -255,20 +256,6 @@ __global__ void mres_coalesce_kernel(R* coarse_post, const R* fine_cur, const st
     }
 }
 
-template <int Q, class R, bool ToDevice>
-__global__ void mres_io_kernel(R* buf, double* staging, const std::int64_t* slots, long long n, int bv,
-                               const double* shift) {
-    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    const long long slot = slots[v];
-    const long long b = slot / bv, local = slot % bv;
-    for (int c = 0; c < Q; ++c) {
-        R* p = buf + (b * Q + c) * bv + local;
-        if constexpr (ToDevice) *p = R(staging[v * Q + c] - shift[c]);
-        else staging[v * Q + c] = double(*p) + shift[c];
-    }
-}
-
 /// probe_field (lbm.cpp:116-138) and total_mass (multires.cpp:600-609) on
 /// the device, over one level's fp64 canonical cells (the staging array
 /// read_state fills): per-CTA partial sums of the populations and max |u|
@@ -314,9 +301,9 @@ __global__ void __launch_bounds__(256) mres_canon_probe_kernel(const double* st,
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        partial[2 * blockIdx.x] = sm[0];
-        partial[2 * blockIdx.x + 1] = sv[0];
+    if (threadIdx.x == 0) {  // accumulated over the staging chunks of a level, in chunk order
+        partial[2 * blockIdx.x] += sm[0];
+        partial[2 * blockIdx.x + 1] = fmax(partial[2 * blockIdx.x + 1], sv[0]);
     }
 }
 
@@ -431,7 +418,8 @@ struct MultiResEngine::Level {
     }
 };
 
-MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_map) : cfg_(cfg) {
+MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_map)
+    : cfg_(cfg), io_(std::make_unique<CanonPipe>()) {
     if (cfg_.lattice != kD3Q19 && cfg_.lattice != kD3Q27)
         throw std::invalid_argument("multires engine: D3Q19 or D3Q27 (3D cavity)");
     if (cfg_.edge != 4 && cfg_.edge != 8) throw std::invalid_argument("multires engine: block edge must be 4 or 8");
@@ -733,31 +721,7 @@ void MultiResEngine::set_equilibrium(double rho, const double u[3]) {
 }
 
 void MultiResEngine::set_state(const double* canonical) {
-    const LatticeTable t = make_lattice(cfg_.lattice);
-    std::vector<double> shift(q_);
-    for (int i = 0; i < q_; ++i) shift[i] = esize_ == 8 ? 0.0 : double(t.wnum[i]) / double(t.wden[i]);
-    double* d_shift = nullptr;
-    VOXL_CUDA(cudaMalloc(&d_shift, q_ * sizeof(double)));
-    VOXL_CUDA(cudaMemcpy(d_shift, shift.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
-    std::int64_t off = 0;
-    for (Level*& V : lv_) {
-        const long long n = V->n_active;
-        double* st = nullptr;
-        VOXL_CUDA(cudaMalloc(&st, std::max<long long>(1, n * q_) * sizeof(double)));
-        VOXL_CUDA(cudaMemcpy(st, canonical + off, n * q_ * sizeof(double), cudaMemcpyHostToDevice));
-        if (esize_ == 8) {
-            if (q_ == 19) mres_io_kernel<19, double, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-            else mres_io_kernel<27, double, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-        } else {
-            if (q_ == 19) mres_io_kernel<19, float, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-            else mres_io_kernel<27, float, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-        }
-        VOXL_CUDA(cudaGetLastError());
-        VOXL_CUDA(cudaStreamSynchronize(stream_));
-        cudaFree(st);
-        off += n * q_;
-    }
-    cudaFree(d_shift);
+    transfer(const_cast<double*>(canonical), true, nullptr, nullptr);
     load_uniform_post();
 }
 
@@ -776,46 +740,51 @@ void MultiResEngine::digest(unsigned long long out[2]) {
 void MultiResEngine::read_state(double* canonical, unsigned long long* digest, double* probe) {
     // canonical_state (multires.cpp:578-598): levels finest first
     sync_state();
+    transfer(canonical, false, digest, probe);
+}
+
+void MultiResEngine::transfer(double* host, bool to_device, unsigned long long* digest, double* probe) {
+    // per level, the level's cells through the shared pipeline (canon_io.cuh);
+    // device-only gathers feed the digest or the probe reduction chunk by chunk
     const LatticeTable t = make_lattice(cfg_.lattice);
-    std::vector<double> shift(q_);
+    double shift[27] = {};
     for (int i = 0; i < q_; ++i) shift[i] = esize_ == 8 ? 0.0 : double(t.wnum[i]) / double(t.wden[i]);
-    double* d_shift = nullptr;
-    VOXL_CUDA(cudaMalloc(&d_shift, q_ * sizeof(double)));
-    VOXL_CUDA(cudaMemcpy(d_shift, shift.data(), q_ * sizeof(double), cudaMemcpyHostToDevice));
-    std::int64_t off = 0;
-    for (Level*& V : lv_) {
+    const bool wire32 = esize_ == 4 && host != nullptr;
+    std::int64_t off = 0;  // canonical element offset of the level
+    for (std::size_t l = 0; l < lv_.size(); ++l) {
+        Level* V = lv_[l];
         const long long n = V->n_active;
-        double* st = nullptr;
-        VOXL_CUDA(cudaMalloc(&st, std::max<long long>(1, n * q_) * sizeof(double)));
-        if (esize_ == 8) {
-            if (q_ == 19) mres_io_kernel<19, double, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-            else mres_io_kernel<27, double, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<double*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-        } else {
-            if (q_ == 19) mres_io_kernel<19, float, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-            else mres_io_kernel<27, float, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(static_cast<float*>(V->cur), st, V->slots, n, V->ext.block_volume(), d_shift);
-        }
-        VOXL_CUDA(cudaGetLastError());
-        if (probe) {
-            const int l = int(&V - lv_.data());
-            double* part = probe + 2 * std::size_t(l) * kMresProbeBlocks;
-            auto* bad = reinterpret_cast<unsigned long long*>(probe + 2 * lv_.size() * kMresProbeBlocks + 3);
-            if (n == 0) {
-                VOXL_CUDA(cudaMemsetAsync(part, 0, 2 * kMresProbeBlocks * sizeof(double), stream_));
-            } else if (q_ == 19) {
-                mres_canon_probe_kernel<D3Q19><<<kMresProbeBlocks, 256, 0, stream_>>>(st, n, off / q_, part, bad);
+        const int bv = V->ext.block_volume();
+        double* part = probe ? probe + 2 * l * kMresProbeBlocks : nullptr;
+        auto* bad = probe ? reinterpret_cast<unsigned long long*>(probe + 2 * lv_.size() * kMresProbeBlocks + 3)
+                          : nullptr;
+        if (part) VOXL_CUDA(cudaMemsetAsync(part, 0, 2 * kMresProbeBlocks * sizeof(double), stream_));
+        auto layout = [&](long long r0, long long r1, void* slot, bool w32) {
+            if (esize_ == 8) {
+                if (q_ == 19) launch_slot_io<19, double>(static_cast<double*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
+                else launch_slot_io<27, double>(static_cast<double*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
             } else {
-                mres_canon_probe_kernel<D3Q27><<<kMresProbeBlocks, 256, 0, stream_>>>(st, n, off / q_, part, bad);
+                if (q_ == 19) launch_slot_io<19, float>(static_cast<float*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
+                else launch_slot_io<27, float>(static_cast<float*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
             }
-            VOXL_CUDA(cudaGetLastError());
-        } else if (digest)
-            digest_accumulate(st, n * q_, off, digest, stream_);
-        else
-            VOXL_CUDA(cudaMemcpyAsync(canonical + off, st, n * q_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
-        VOXL_CUDA(cudaStreamSynchronize(stream_));
-        cudaFree(st);
+        };
+        auto consume = [&](long long r0, long long r1, void* slot) {
+            const double* st = static_cast<const double*>(slot);
+            if (part) {
+                if (q_ == 19)
+                    mres_canon_probe_kernel<D3Q19><<<kMresProbeBlocks, 256, 0, stream_>>>(st, r1 - r0, off / q_ + r0, part, bad);
+                else
+                    mres_canon_probe_kernel<D3Q27><<<kMresProbeBlocks, 256, 0, stream_>>>(st, r1 - r0, off / q_ + r0, part, bad);
+                VOXL_CUDA(cudaGetLastError());
+            } else {
+                digest_accumulate(st, (r1 - r0) * q_, off + r0 * q_, digest, stream_);
+            }
+        };
+        io_->run(host ? host + off : nullptr, n, 1, q_, to_device, wire32, shift, stream_, layout, consume,
+                 digest != nullptr || part != nullptr);
         off += n * q_;
     }
-    cudaFree(d_shift);
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void MultiResEngine::mark_begin(int, cudaEvent_t* b, cudaStream_t s) {

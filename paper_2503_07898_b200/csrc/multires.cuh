@@ -77,9 +77,11 @@ public:
     struct Level;
     void read_state(double* canonical, unsigned long long* digest, double* probe = nullptr);
     void device_probe(double out[3], DenseDiag* d);
+    void transfer(double* host, bool to_device, unsigned long long* digest, double* probe);
 
 private:
     MresConfig cfg_;
+    std::unique_ptr<CanonPipe> io_;  // canonical host <-> device pipeline (canon_io.cuh)
     int q_ = 19;
     int esize_ = 4;
     MresGrid grid_;

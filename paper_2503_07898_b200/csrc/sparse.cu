@@ -12,6 +12,7 @@
 #include "sparse.cuh"
 #include "lattice.cuh"
 #include "digest.cuh"
+#include "canon_io.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -247,20 +248,6 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && si
     });
 }
 
-template <int Q, class R, bool ToDevice>
-__global__ void sparse_io_kernel(R* buf, double* staging, const std::int64_t* slots, long long n, int bv,
-                                 const __grid_constant__ SparseArgs<Q, R> A) {
-    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    const long long slot = slots[v];
-    const long long b = slot / bv, local = slot % bv;
-    for (int c = 0; c < Q; ++c) {
-        R* p = buf + (b * Q + c) * bv + local;
-        if constexpr (ToDevice) *p = R(staging[v * Q + c] - A.shift[c]);
-        else staging[v * Q + c] = double(*p) + A.shift[c];
-    }
-}
-
 template <int Q, class R>
 __global__ void sparse_fill_kernel(R* buf, long long total, int bv, const __grid_constant__ SparseArgs<Q, R> A) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -384,7 +371,8 @@ void sparse_dispatch(int lattice, Precision prec, F&& f) {
 
 } // namespace
 
-SparseEngine::SparseEngine(const SparseConfig& cfg, const std::uint8_t* active) : cfg_(cfg) {
+SparseEngine::SparseEngine(const SparseConfig& cfg, const std::uint8_t* active)
+    : cfg_(cfg), io_(std::make_unique<CanonPipe>()) {
     if (!(cfg_.tau > 0.5)) throw std::invalid_argument("sparse engine: tau must be > 0.5");
     if (cfg_.lattice != kD3Q19 && cfg_.lattice != kD3Q27)
         throw std::invalid_argument("sparse engine: D3Q19 or D3Q27 only (3D wind tunnel)");
@@ -491,7 +479,6 @@ SparseEngine::~SparseEngine() {
     cudaFree(d_compact_meta_);
     cudaFree(d_naive_meta_);
     cudaFree(d_slots_);
-    cudaFree(d_staging_);
     cudaFree(d_error_);
     cudaFree(d_diag_);
     if (side_) {
@@ -535,63 +522,41 @@ void SparseEngine::ensure_slots() {
     VOXL_CUDA(cudaMemcpy(d_slots_, slots.data(), slots.size() * sizeof(std::int64_t), cudaMemcpyHostToDevice));
 }
 
-void SparseEngine::set_state(const double* canonical) {
+void SparseEngine::transfer(double* host, bool to_device, unsigned long long* digest) {
+    // canonical_state / set_state (sparse.cpp:416-453) through the shared
+    // pipeline (canon_io.cuh): rows = canonical cells, fp32 wire format for
+    // fp32 engines
     ensure_slots();
     const long long n = grid_.num_active();
-    const std::size_t len = std::size_t(n) * q_;
-    if (staging_len_ < len) {
-        cudaFree(d_staging_);
-        VOXL_CUDA(cudaMalloc(&d_staging_, len * sizeof(double)));
-        staging_len_ = len;
-    }
-    VOXL_CUDA(cudaMemcpyAsync(d_staging_, canonical, len * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    const bool wire32 = esize_ == 4 && host != nullptr;
     sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
         using Ops = decltype(ops);
         auto A = Ops::base_args(cfg_);
         using R = std::remove_pointer_t<decltype(A.nxt)>;
-        sparse_io_kernel<Ops::Q, R, true><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(
-            static_cast<R*>(buf_[cur_]), d_staging_, d_slots_, n, grid_.block_volume(), A);
-        VOXL_CUDA(cudaGetLastError());
+        R* buf = static_cast<R*>(buf_[cur_]);
+        const int bv = grid_.block_volume();
+        auto layout = [&](long long r0, long long r1, void* slot, bool w32) {
+            launch_slot_io<Ops::Q, R>(buf, slot, w32, d_slots_ + r0, r1 - r0, bv, A.shift, to_device, stream_);
+        };
+        auto consume = [&](long long r0, long long r1, void* slot) {
+            digest_accumulate(static_cast<const double*>(slot), (r1 - r0) * Ops::Q, r0 * Ops::Q, digest, stream_);
+        };
+        io_->run(host, n, 1, Ops::Q, to_device, wire32, A.shift, stream_, layout, consume, digest != nullptr);
     });
-    VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void SparseEngine::get_state(double* canonical) {
-    const long long n = stage_canonical();
-    VOXL_CUDA(cudaMemcpyAsync(canonical, d_staging_, std::size_t(n) * q_ * sizeof(double), cudaMemcpyDeviceToHost,
-                              stream_));
-    VOXL_CUDA(cudaStreamSynchronize(stream_));
-}
+void SparseEngine::set_state(const double* canonical) { transfer(const_cast<double*>(canonical), true, nullptr); }
+
+void SparseEngine::get_state(double* canonical) { transfer(canonical, false, nullptr); }
 
 void SparseEngine::digest(unsigned long long out[2]) {
-    const long long n = stage_canonical();
     unsigned long long* acc = nullptr;
     VOXL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&acc), 2 * sizeof(unsigned long long), stream_));
     VOXL_CUDA(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), stream_));
-    digest_accumulate(d_staging_, n * q_, 0, acc, stream_);
+    transfer(nullptr, false, acc);
     VOXL_CUDA(cudaMemcpyAsync(out, acc, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaFreeAsync(acc, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
-}
-
-long long SparseEngine::stage_canonical() {
-    ensure_slots();
-    const long long n = grid_.num_active();
-    const std::size_t len = std::size_t(n) * q_;
-    if (staging_len_ < len) {
-        cudaFree(d_staging_);
-        VOXL_CUDA(cudaMalloc(&d_staging_, len * sizeof(double)));
-        staging_len_ = len;
-    }
-    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
-        using Ops = decltype(ops);
-        auto A = Ops::base_args(cfg_);
-        using R = std::remove_pointer_t<decltype(A.nxt)>;
-        sparse_io_kernel<Ops::Q, R, false><<<unsigned((n + 255) / 256), 256, 0, stream_>>>(
-            static_cast<R*>(buf_[cur_]), d_staging_, d_slots_, n, grid_.block_volume(), A);
-        VOXL_CUDA(cudaGetLastError());
-    });
-    return n;
 }
 
 void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l) {

@@ -87,8 +87,7 @@ private:
     void* d_compact_meta_ = nullptr;
     void* d_naive_meta_ = nullptr;
     std::int64_t* d_slots_ = nullptr;
-    double* d_staging_ = nullptr;
-    std::size_t staging_len_ = 0;
+    std::unique_ptr<CanonPipe> io_;  // canonical host <-> device pipeline (canon_io.cuh)
     int* d_error_ = nullptr;
     double* d_diag_ = nullptr;
     cudaStream_t stream_ = nullptr;
@@ -100,7 +99,7 @@ private:
 
     void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l);
     void ensure_slots();
-    long long stage_canonical();  // canonical fp64 state -> d_staging_; returns active voxels
+    void transfer(double* host, bool to_device, unsigned long long* digest);
 };
 
 } // namespace voxl_b200

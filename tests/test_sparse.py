@@ -227,3 +227,25 @@ def test_fp32_tolerance_1000_steps():
     rel = np.abs(a - b) / np.abs(a)
     print("sparse fp32 max rel err after 1000 steps:", rel.max())
     assert rel.max() <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_state_io_multichunk_roundtrip(precision):
+    """set_state / get_state of 2.0 M active voxels through the pipelined
+    staging (several 64 MiB chunks; fp32 wire format for fp32): stored values
+    are exactly R(f - w_i) and read back as double(g) + w_i."""
+    dom = (128, 128, 128)
+    e = V.SparseEngine(dom, block_edge=8, strategy="disag_mem", precision=precision)
+    n = e.num_active
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    rng = np.random.default_rng(3)
+    f = (w[None, :] * (1.0 + 0.05 * rng.standard_normal((n, 19)))).reshape(-1)
+    e.set_state(f)
+    out = e.get_state()
+    e.close()
+    if precision == "fp64":
+        assert np.array_equal(out, f)
+    else:
+        ww = np.tile(w, n)
+        assert np.array_equal(out, (f - ww).astype(np.float32).astype(np.float64) + ww)

@@ -31,14 +31,14 @@ struct ShiftQ {
 /// slot slots[v] = b*bv + local. S = double: fp64 staging (shift applied
 /// here); S = R: fp32 wire staging (shift applied on the host).
 template <int Q, class R, bool ToDevice, class S>
-__global__ void slot_io_kernel(R* buf, S* staging, const std::int64_t* slots, long long n, int bv,
+__global__ void slot_io_kernel(R* buf, S* staging, const std::int64_t* slots, long long n, int lb,
                                const __grid_constant__ ShiftQ<Q> sh) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    const long long slot = slots[v];
-    const long long b = slot / bv, local = slot % bv;
+    const long long slot = slots[v], bv = 1ll << lb;
+    const long long base = ((slot >> lb) * Q << lb) + (slot & (bv - 1));
     for (int c = 0; c < Q; ++c) {
-        R* p = buf + (b * Q + c) * bv + local;
+        R* p = buf + base + c * bv;
         if constexpr (std::is_same_v<S, double>) {
             if constexpr (ToDevice) *p = R(staging[v * Q + c] - sh.v[c]);
             else staging[v * Q + c] = double(*p) + sh.v[c];
@@ -55,19 +55,20 @@ void launch_slot_io(R* buf, void* staging, bool wire32, const std::int64_t* slot
     if (n <= 0) return;
     ShiftQ<Q> sh{};
     for (int c = 0; c < Q; ++c) sh.v[c] = shift[c];
+    const int lb = log2_exact(bv);
     const unsigned blocks = unsigned((n + 255) / 256);
     if (wire32) {
         if constexpr (sizeof(R) == 4) {
             auto* s = static_cast<R*>(staging);
-            if (to_device) slot_io_kernel<Q, R, true, R><<<blocks, 256, 0, st>>>(buf, s, slots, n, bv, sh);
-            else slot_io_kernel<Q, R, false, R><<<blocks, 256, 0, st>>>(buf, s, slots, n, bv, sh);
+            if (to_device) slot_io_kernel<Q, R, true, R><<<blocks, 256, 0, st>>>(buf, s, slots, n, lb, sh);
+            else slot_io_kernel<Q, R, false, R><<<blocks, 256, 0, st>>>(buf, s, slots, n, lb, sh);
         } else {
             throw std::logic_error("fp32 wire format on an fp64 engine");
         }
     } else {
         auto* s = static_cast<double*>(staging);
-        if (to_device) slot_io_kernel<Q, R, true, double><<<blocks, 256, 0, st>>>(buf, s, slots, n, bv, sh);
-        else slot_io_kernel<Q, R, false, double><<<blocks, 256, 0, st>>>(buf, s, slots, n, bv, sh);
+        if (to_device) slot_io_kernel<Q, R, true, double><<<blocks, 256, 0, st>>>(buf, s, slots, n, lb, sh);
+        else slot_io_kernel<Q, R, false, double><<<blocks, 256, 0, st>>>(buf, s, slots, n, lb, sh);
     }
     VOXL_CUDA(cudaGetLastError());
 }

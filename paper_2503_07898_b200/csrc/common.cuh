@@ -33,4 +33,13 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 #define VOXL_CUDA(call) ::voxl_b200::cuda_check((call), #call)
 
+/// log2 of a power of two (block volumes E^3, E in {1, 2, 4, 8}): device
+/// slot arithmetic uses shifts instead of 64-bit division.
+inline int log2_exact(long long v) {
+    int l = 0;
+    while ((1ll << l) < v) ++l;
+    if ((1ll << l) != v) throw std::invalid_argument("block volume is not a power of two");
+    return l;
+}
+
 } // namespace voxl_b200

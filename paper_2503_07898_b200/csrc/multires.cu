@@ -224,58 +224,81 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
     });
 }
 
-/// explode (multires.cpp:458-467): ghost(l) <- parent(l+1) post-collision.
+/// explode (multires.cpp:458-467): ghost cells of the fine level <- the
+/// post-collision populations of their parent, a plain copy. One launch fills
+/// both fine post parities in fused mode (one explosion serves both fine
+/// sub-steps, multires.cpp:563-570). Slot -> element offsets use shifts: the
+/// block volume E^3 is a power of two (64-bit division is ~100 instructions).
 template <int Q, class R>
-__global__ void mres_explode_kernel(R* fine_post, const R* coarse_post, const std::int64_t* dst,
-                                    const std::int64_t* src, int n, int bv) {
+__global__ void mres_explode_kernel(R* fine_a, R* fine_b, const R* coarse_post, const std::int64_t* dst,
+                                    const std::int64_t* src, int n, int lb) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    const long long ds = dst[g], ss = src[g];
-    const long long db = ds / bv, dl = ds % bv, sb = ss / bv, sl = ss % bv;
-    for (int c = 0; c < Q; ++c) fine_post[(db * Q + c) * bv + dl] = coarse_post[(sb * Q + c) * bv + sl];
+    const long long bv = 1ll << lb, ds = dst[g], ss = src[g];
+    const long long dbase = ((ds >> lb) * Q << lb) + (ds & (bv - 1));
+    const long long sbase = ((ss >> lb) * Q << lb) + (ss & (bv - 1));
+    for (int c = 0; c < Q; ++c) {
+        const R v = coarse_post[sbase + c * bv];
+        fine_a[dbase + c * bv] = v;
+        if (fine_b) fine_b[dbase + c * bv] = v;
+    }
 }
 
 /// coalesce (multires.cpp:469-483): ring(l) <- mean of the 8 children's
 /// current (post-stream) populations, children_of order, sum * (1/8).
 template <int Q, class R, bool Exact>
 __global__ void mres_coalesce_kernel(R* coarse_post, const R* fine_cur, const std::int64_t* dst,
-                                     const std::int64_t* child, int n, int bv_c, int bv_f, int nchild) {
+                                     const std::int64_t* child, int n, int lbc, int lbf, int nchild) {
     using A = Arith<R, Exact>;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    const long long ds = dst[g];
-    const long long db = ds / bv_c, dl = ds % bv_c;
+    const long long bvc = 1ll << lbc, bvf = 1ll << lbf, ds = dst[g];
+    const long long dbase = ((ds >> lbc) * Q << lbc) + (ds & (bvc - 1));
+    long long cb[8];
+    for (int k = 0; k < 8; ++k) {
+        if (k < nchild) {
+            const long long cs = child[(long long)g * 8 + k];
+            cb[k] = ((cs >> lbf) * Q << lbf) + (cs & (bvf - 1));
+        }
+    }
     const R scale = R(1.0 / double(nchild));
     for (int c = 0; c < Q; ++c) {
         R sum = R(0);
-        for (int k = 0; k < nchild; ++k) {
-            const long long cs = child[(long long)g * 8 + k];
-            sum = A::add(sum, fine_cur[((cs / bv_f) * Q + c) * bv_f + cs % bv_f]);
-        }
-        coarse_post[(db * Q + c) * bv_c + dl] = A::mul(sum, scale);
+        for (int k = 0; k < nchild; ++k) sum = A::add(sum, fine_cur[cb[k] + c * bvf]);
+        coarse_post[dbase + c * bvc] = A::mul(sum, scale);
     }
 }
 
 /// probe_field (lbm.cpp:116-138) and total_mass (multires.cpp:600-609) on
-/// the device, over one level's fp64 canonical cells (the staging array
-/// read_state fills): per-CTA partial sums of the populations and max |u|
+/// the device, over one level's cells in canonical order (slots[v]), read
+/// straight from the state buffer (fp64 value = storage + shift, exactly the
+/// canonical_state value): per-CTA partial sums of the populations and max |u|
 /// (u = m / rho, true division, as macroscopic lattice.cpp:115-129), the
 /// first unstable (cell, population) by atomicMin. Fixed grid and fixed
 /// reduction order, so the result is run-to-run deterministic.
 constexpr int kMresProbeBlocks = 296;
 
-template <class L>
-__global__ void __launch_bounds__(256) mres_canon_probe_kernel(const double* st, long long n, long long cell0,
-                                                               double* partial, unsigned long long* bad) {
+template <class L, class R>
+__global__ void __launch_bounds__(256) mres_slot_probe_kernel(const R* cur, const std::int64_t* slots, long long n,
+                                                              int lb, const __grid_constant__ ShiftQ<L::Q> sh,
+                                                              long long cell0, double* partial,
+                                                              unsigned long long* bad) {
     constexpr int Q = L::Q;
     double mass = 0.0, vmax = 0.0;
+    const long long bv = 1ll << lb;
     for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
-        const double* f = st + v * Q;
+        const long long slot = slots[v];
+        const R* f = cur + ((slot >> lb) * Q << lb) + (slot & (bv - 1));
+        R raw[Q];
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            raw[i] = f[i * bv];
+        });
         double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
         int bp = -1;
         static_for<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            const double fi = f[i];
+            const double fi = double(raw[i]) + sh.v[i];
             if (bp < 0 && !(fabs(fi) <= 1e3)) bp = i;
             r += fi;
             mx = acc_term<double, false, L::ex(i)>(mx, fi);
@@ -721,7 +744,7 @@ void MultiResEngine::set_equilibrium(double rho, const double u[3]) {
 }
 
 void MultiResEngine::set_state(const double* canonical) {
-    transfer(const_cast<double*>(canonical), true, nullptr, nullptr);
+    transfer(const_cast<double*>(canonical), true, nullptr);
     load_uniform_post();
 }
 
@@ -737,15 +760,15 @@ void MultiResEngine::digest(unsigned long long out[2]) {
     cudaFree(acc);
 }
 
-void MultiResEngine::read_state(double* canonical, unsigned long long* digest, double* probe) {
+void MultiResEngine::read_state(double* canonical, unsigned long long* digest) {
     // canonical_state (multires.cpp:578-598): levels finest first
     sync_state();
-    transfer(canonical, false, digest, probe);
+    transfer(canonical, false, digest);
 }
 
-void MultiResEngine::transfer(double* host, bool to_device, unsigned long long* digest, double* probe) {
+void MultiResEngine::transfer(double* host, bool to_device, unsigned long long* digest) {
     // per level, the level's cells through the shared pipeline (canon_io.cuh);
-    // device-only gathers feed the digest or the probe reduction chunk by chunk
+    // device-only gathers feed the digest chunk by chunk
     const LatticeTable t = make_lattice(cfg_.lattice);
     double shift[27] = {};
     for (int i = 0; i < q_; ++i) shift[i] = esize_ == 8 ? 0.0 : double(t.wnum[i]) / double(t.wden[i]);
@@ -755,10 +778,6 @@ void MultiResEngine::transfer(double* host, bool to_device, unsigned long long* 
         Level* V = lv_[l];
         const long long n = V->n_active;
         const int bv = V->ext.block_volume();
-        double* part = probe ? probe + 2 * l * kMresProbeBlocks : nullptr;
-        auto* bad = probe ? reinterpret_cast<unsigned long long*>(probe + 2 * lv_.size() * kMresProbeBlocks + 3)
-                          : nullptr;
-        if (part) VOXL_CUDA(cudaMemsetAsync(part, 0, 2 * kMresProbeBlocks * sizeof(double), stream_));
         auto layout = [&](long long r0, long long r1, void* slot, bool w32) {
             if (esize_ == 8) {
                 if (q_ == 19) launch_slot_io<19, double>(static_cast<double*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
@@ -769,19 +788,10 @@ void MultiResEngine::transfer(double* host, bool to_device, unsigned long long* 
             }
         };
         auto consume = [&](long long r0, long long r1, void* slot) {
-            const double* st = static_cast<const double*>(slot);
-            if (part) {
-                if (q_ == 19)
-                    mres_canon_probe_kernel<D3Q19><<<kMresProbeBlocks, 256, 0, stream_>>>(st, r1 - r0, off / q_ + r0, part, bad);
-                else
-                    mres_canon_probe_kernel<D3Q27><<<kMresProbeBlocks, 256, 0, stream_>>>(st, r1 - r0, off / q_ + r0, part, bad);
-                VOXL_CUDA(cudaGetLastError());
-            } else {
-                digest_accumulate(st, (r1 - r0) * q_, off + r0 * q_, digest, stream_);
-            }
+            digest_accumulate(static_cast<const double*>(slot), (r1 - r0) * q_, off + r0 * q_, digest, stream_);
         };
         io_->run(host ? host + off : nullptr, n, 1, q_, to_device, wire32, shift, stream_, layout, consume,
-                 digest != nullptr || part != nullptr);
+                 digest != nullptr);
         off += n * q_;
     }
     VOXL_CUDA(cudaStreamSynchronize(stream_));
@@ -948,16 +958,16 @@ void MultiResEngine::launch_explode(int coarse) {
     const unsigned grid = unsigned((F->n_ghost + 127) / 128);
     // One explosion serves both fine sub-steps (multires.cpp:563-570); the
     // fine level flips its post parity between them, so fill both copies.
-    for (int w = 0; w < (cfg_.fused ? 2 : 1); ++w) {
-        void* dst = F->post[cfg_.fused ? w : F->parity];
-        const void* src = Cc->post[Cc->parity];
-        if (esize_ == 8) {
-            if (q_ == 19) mres_explode_kernel<19, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(dst), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
-            else mres_explode_kernel<27, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(dst), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
-        } else {
-            if (q_ == 19) mres_explode_kernel<19, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(dst), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
-            else mres_explode_kernel<27, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(dst), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, F->ext.block_volume());
-        }
+    void* da = F->post[cfg_.fused ? 0 : F->parity];
+    void* db = cfg_.fused ? F->post[1] : nullptr;
+    const void* src = Cc->post[Cc->parity];
+    const int lb = log2_exact(F->ext.block_volume());
+    if (esize_ == 8) {
+        if (q_ == 19) mres_explode_kernel<19, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        else mres_explode_kernel<27, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+    } else {
+        if (q_ == 19) mres_explode_kernel<19, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        else mres_explode_kernel<27, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
     }
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTTransition, b);
@@ -971,7 +981,7 @@ void MultiResEngine::launch_coalesce(int coarse) {
     mark_begin(kTTransition, &b);
     const unsigned grid = unsigned((Cc->n_ring + 127) / 128);
     const int nchild = grid_.dim() == 3 ? 8 : 4;
-    const int bvc = Cc->ext.block_volume(), bvf = F->ext.block_volume();
+    const int bvc = log2_exact(Cc->ext.block_volume()), bvf = log2_exact(F->ext.block_volume());
     if (esize_ == 8) {
         if (q_ == 19) mres_coalesce_kernel<19, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
         else mres_coalesce_kernel<27, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
@@ -1070,7 +1080,28 @@ void MultiResEngine::device_probe(double out[3], DenseDiag* d) {
     }
     double* row = d_diag_ + per_level * lv_.size();
     VOXL_CUDA(cudaMemsetAsync(row + 3, 0xFF, sizeof(double), stream_));
-    read_state(nullptr, nullptr, d_diag_);
+    sync_state();  // uniform cells' pre-collision state (fused mode)
+    auto* bad = reinterpret_cast<unsigned long long*>(row + 3);
+    long long cell0 = 0;
+    for (std::size_t l = 0; l < lv_.size(); ++l) {
+        Level* V = lv_[l];
+        double* part = d_diag_ + per_level * l;
+        VOXL_CUDA(cudaMemsetAsync(part, 0, per_level * sizeof(double), stream_));
+        const long long n = V->n_active;
+        const int lb = log2_exact(V->ext.block_volume());
+        if (n > 0) {
+            mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto, auto) {
+                using L = decltype(lat);
+                using R = decltype(real);
+                ShiftQ<L::Q> sh{};
+                for (int i = 0; i < L::Q; ++i) sh.v[i] = esize_ == 8 ? 0.0 : L::w(i);
+                mres_slot_probe_kernel<L, R><<<kMresProbeBlocks, 256, 0, stream_>>>(
+                    static_cast<const R*>(V->cur), V->slots, n, lb, sh, cell0, part, bad);
+            });
+            VOXL_CUDA(cudaGetLastError());
+        }
+        cell0 += n;
+    }
     mres_probe_final<<<1, 32, 0, stream_>>>(d_diag_, int(lv_.size()), kMresProbeBlocks,
                                             double(grid_.dim() == 3 ? 8 : 4), row);
     VOXL_CUDA(cudaGetLastError());

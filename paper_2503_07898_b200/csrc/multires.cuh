@@ -75,9 +75,9 @@ public:
     void check_errors();
 
     struct Level;
-    void read_state(double* canonical, unsigned long long* digest, double* probe = nullptr);
+    void read_state(double* canonical, unsigned long long* digest);
     void device_probe(double out[3], DenseDiag* d);
-    void transfer(double* host, bool to_device, unsigned long long* digest, double* probe);
+    void transfer(double* host, bool to_device, unsigned long long* digest);
 
 private:
     MresConfig cfg_;

@@ -41,19 +41,21 @@ def test_error_status_and_message():
         V.lattice_json(7)
 
 
-def _build_dropin(tmp_path):
-    exe = os.path.join(str(tmp_path), "dropin_dense")
+def _build_dropin(tmp_path, name="dropin_dense"):
+    exe = os.path.join(str(tmp_path), name)
     libdir = os.path.dirname(V.LIB_PATH)
-    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
-           os.path.join(ROOT, "tests", "cpp", "dropin_dense.cpp"), "-L", libdir, "-lvoxl_b200",
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", name + ".cpp"), "-L", libdir, "-lvoxl_b200",
            "-Wl,-rpath," + libdir, "-o", exe]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     return exe
 
 
 def test_cpp_binding_compiles_and_links(tmp_path):
-    """include/voxl_b200.hpp: the reference-named C++ wrapper builds against the .so."""
+    """include/voxl_b200.hpp: the reference-named C++ wrapper (engines and
+    run()) builds against the .so."""
     assert os.path.exists(_build_dropin(tmp_path))
+    assert os.path.exists(_build_dropin(tmp_path, "dropin_run"))
 
 
 import pytest as _pytest  # noqa: E402
@@ -86,3 +88,45 @@ def test_host_io_conversion_exact(tmp_path):
                    check=True)
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@_pytest.mark.gpu
+def test_cpp_run_dropin_matches_oracle_and_python(tmp_path):
+    """voxl::b200::run (C++, solver.cpp:369-375 shape) on the three engines:
+    fields bitwise equal to the oracle, diagnostics equal to the Python
+    front-end's run(), and the reference's abort text on an unstable run."""
+    import numpy as np
+
+    import oracle as O
+    from paper_2503_07898_b200 import solver as S
+
+    exe = _build_dropin(tmp_path, "dropin_run")
+    prefix = os.path.join(str(tmp_path), "run")
+    r = subprocess.run([exe, prefix], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "run aborted at step" in r.stdout
+    field = lambda n: np.fromfile(f"{prefix}_{n}.bin", np.float64)  # noqa: E731
+    diag = lambda n: np.loadtxt(f"{prefix}_{n}.csv", delimiter=",", ndmin=2)  # noqa: E731
+    dom = (16, 16, 16)
+    assert np.array_equal(field("dense"), O.port_dense_run("D3Q19", dom, 0.56, "lid_driven_cavity", (0.05, 0, 0), 12))
+    act = O.obstacle_mask(dom)
+    sref = O.sparse_canonical(dom, act, O.port_sparse_run("D3Q19", dom, 0.7, (0.04, 0, 0), 5, act), 19)
+    assert np.array_equal(field("sparse"), sref)
+    assert np.array_equal(field("multires"), O.port_mres_run("D3Q19", dom, 2, 0.56, (0.05, 0.0, 0.0), 2))
+    cfgs = {"dense": dict(steps=12, partitions=2),
+            "sparse": dict(scenario="flow_over_obstacle", tau=0.7, velocity=[0.04, 0, 0], steps=5,
+                           strategy="disag_mem"),
+            "multires": dict(levels=2, steps=2)}
+    for name, kw in cfgs.items():
+        base = dict(lattice="D3Q19", domain=[16, 16, 16], tau=0.56, scenario="lid_driven_cavity",
+                    velocity=[0.05, 0, 0])
+        base.update(kw)
+        c = S.SolverConfig(**base)
+        c.domain = tuple(c.domain)
+        c.velocity = tuple(c.velocity)
+        c.precision = "fp64"
+        py = S.run(c)
+        got = diag(name)
+        assert got.shape[0] == len(py.diagnostics)
+        for (st, m, u), row in zip(py.diagnostics, got):
+            assert int(row[0]) == st and row[1] == m and row[2] == u, name

@@ -225,6 +225,9 @@ int voxl_sparse_step(voxl_sparse* h, int n);
 int voxl_sparse_step_identity(voxl_sparse* h, int n);
 int voxl_sparse_timed_steps(voxl_sparse* h, int n, double* total_ms, double* boundary_ms, double* light_ms);
 int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out);
+/** One SparseLbmEngine::step with probe_field fused into the step kernels:
+ *  run_sparse's per-step diagnostics row (solver.cpp:287-291). */
+int voxl_sparse_step_probe(voxl_sparse* h, voxl_diag* out);
 /** dispatch_plan(...).to_json() (sparse.cpp:199-225; Table 2). */
 int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int block_size, int s_w, int s_i,
                             int naive_full_domain_storage, char* out, int64_t cap, int64_t* len);

@@ -289,9 +289,8 @@ inline RunResult run_sparse(const SolverConfig& c) {
     d.precision = c.precision;
     SparseLbmEngine e(d, mask);
     for (int step = 0; step < c.steps; ++step) {
-        e.step();
         voxl_diag g{};
-        check(voxl_sparse_probe(e.handle(), &g));
+        check(voxl_sparse_step_probe(e.handle(), &g));  // step + probe_field, fused on the device
         abort_if_unstable(g, step);
         r.diagnostics.push_back({step, g.mass, g.max_speed});
     }

@@ -137,6 +137,7 @@ def _load():
         "voxl_sparse_timed_steps": ([vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double)], C.c_int),
         "voxl_sparse_probe": ([vp, C.POINTER(Diag)], C.c_int),
+        "voxl_sparse_step_probe": ([vp, C.POINTER(Diag)], C.c_int),
         "voxl_dispatch_plan_json": ([C.c_int, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, cp, i64,
                                      C.POINTER(i64)], C.c_int),
         "voxl_band_level_map": ([C.c_int] * 5 + [vp], C.c_int),

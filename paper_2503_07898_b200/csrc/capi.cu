@@ -516,6 +516,17 @@ int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out) {
     });
 }
 
+int voxl_sparse_step_probe(voxl_sparse* h, voxl_diag* out) {
+    return guarded([&] {
+        const DenseDiag d = SP(h)->step_probe();
+        out->mass = d.mass;
+        out->max_speed = d.max_speed;
+        out->unstable = d.unstable;
+        out->bad_population = d.bad_population;
+        out->bad_voxel = d.bad_voxel;
+    });
+}
+
 int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int bs, int s_w, int s_i, int full,
                             char* out, int64_t cap, int64_t* len) {
     return guarded([&] {

@@ -78,62 +78,6 @@ __device__ __forceinline__ R ld_ro(const R* p) {
     return __ldg(p);
 }
 
-/// probe_field's per-voxel terms (lbm.cpp:116-138) for the fused probe, from
-/// the moments the collision just computed: BGK conserves rho and rho*u, so
-/// the post-collision mass and velocity equal the pre-collision ones up to
-/// rounding (<= 1 ulp of the moment sums; the probe's tolerance is 1e-12
-/// relative in fp64). Reusing them keeps the probing step kernel near the
-/// plain kernel's register and instruction budget (a second set of
-/// post-collision moment sums in fp64 cost 16 registers, 6 -> 4 resident CTAs
-/// per SM and 27 % of the step). The instability test |f_i| <= 1e3 still runs
-/// on the post-collision values.
-///   fp64 (P = double): m = rho, v = |u|^2.
-///   fp32 shifted storage (P = float): m = dr = rho - 1 (the caller adds the
-///   live-voxel count in fp64), v = |u|^2 in fp32. A max-|g| screen (one
-///   FMNMX per population) replaces the per-population two-sided bounds; only
-///   a voxel that fails it (|g| > 999, rho <= 0 or a non-finite moment) takes
-///   the exact test, so the verdict is the reference's.
-template <class L, class R, bool Exact, class P>
-__device__ __forceinline__ void probe_voxel(const R (&f)[L::Q], R rho, R dr, const R (&u)[3], P& m, P& v,
-                                            bool& bad) {
-    if constexpr (Exact || sizeof(R) == 8) {
-        bool b = false;
-        static_for<L::Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            const double fi = double(f[i]) + (Exact ? 0.0 : L::w(i));
-            b = b || !(fabs(fi) <= 1e3);
-        });
-        m = Exact ? double(rho) : 1.0 + double(dr);
-        if (b || !(m > 0.0)) {
-            bad = true;
-        } else {
-            const double ux = double(u[0]), uy = double(u[1]), uz = double(u[2]);
-            v = ux * ux + uy * uy + uz * uz;
-        }
-    } else {
-        float mx = 0.0f;
-        static_for<L::Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            mx = fmaxf(mx, fabsf(f[i]));
-        });
-        const float v2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
-        m = dr;
-        if (!(mx <= 999.0f) || !(rho > 0.0f) || !(v2 <= 1e30f)) {
-            bool b = !(1.0 + double(dr) > 0.0);
-            static_for<L::Q>([&](auto I) {
-                constexpr int i = decltype(I)::value;
-                constexpr float hi = float(1e3 - L::w(i)), lo = float(-1e3 - L::w(i));
-                b = b || !(f[i] <= R(hi) && f[i] >= R(lo));  // |g + w| <= 1e3, NaN-safe
-            });
-            if (b) {
-                bad = true;
-                return;
-            }
-        }
-        v = v2;
-    }
-}
-
 /// Fused pull-stream + bounce-back/lid + BGK for one voxel per thread
 /// (gather_pull lbm.hpp:40-74 then bgk_relax lattice.cpp:131-138).
 /// AXIS is the partition axis (2 in 3D, 1 in 2D); `a` is x, `b` the remaining

@@ -3,6 +3,7 @@
 #include "lattice.cuh"
 #include "digest.cuh"
 #include "canon_io.cuh"
+#include "block_probe.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -1069,59 +1070,83 @@ MresTimes MultiResEngine::timed_steps(int n) {
 }
 
 void MultiResEngine::device_probe(double out[3], DenseDiag* d) {
-    // canonical_state per level into device staging, then the reductions on
-    // the device; only the 4-word result row comes back to the host.
+    // Sums and max |u| per level in storage order over the active slots
+    // (block_probe.cuh), combined in a fixed order; the canonical-order kernel
+    // only runs to name the first unstable cell when there is one. Only the
+    // result row comes back to the host.
     const std::size_t per_level = 2 * std::size_t(kMresProbeBlocks);
-    const std::size_t need = per_level * lv_.size() + 4;
+    const std::size_t need = per_level * lv_.size() + 5;
     if (diag_len_ < need) {
         cudaFree(d_diag_);
         VOXL_CUDA(cudaMalloc(&d_diag_, need * sizeof(double)));
         diag_len_ = need;
     }
     double* row = d_diag_ + per_level * lv_.size();
-    VOXL_CUDA(cudaMemsetAsync(row + 3, 0xFF, sizeof(double), stream_));
-    sync_state();  // uniform cells' pre-collision state (fused mode)
     auto* bad = reinterpret_cast<unsigned long long*>(row + 3);
+    auto* bad_any = reinterpret_cast<unsigned int*>(row + 4);
+    VOXL_CUDA(cudaMemsetAsync(d_diag_, 0, need * sizeof(double), stream_));
+    sync_state();  // uniform cells' pre-collision state (fused mode)
+    auto shift_of = [&](auto lat) {
+        using L = decltype(lat);
+        ShiftQ<L::Q> sh{};
+        for (int i = 0; i < L::Q; ++i) sh.v[i] = esize_ == 8 ? 0.0 : L::w(i);
+        return sh;
+    };
+    for (std::size_t l = 0; l < lv_.size(); ++l) {
+        Level* V = lv_[l];
+        const long long nb = V->ext.num_blocks();
+        if (V->n_active == 0 || nb == 0) continue;
+        const int lb = log2_exact(V->ext.block_volume());
+        mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto, auto) {
+            using L = decltype(lat);
+            using R = decltype(real);
+            const int ctas = int(std::min<long long>(kMresProbeBlocks, nb));
+            block_probe_kernel<L, R><<<ctas, 256, 0, stream_>>>(static_cast<const R*>(V->cur), V->amask,
+                                                                V->ext.mask_words(), lb, nb, shift_of(lat),
+                                                                d_diag_ + per_level * l, bad_any);
+        });
+        VOXL_CUDA(cudaGetLastError());
+    }
+    mres_probe_final<<<1, 32, 0, stream_>>>(d_diag_, int(lv_.size()), kMresProbeBlocks,
+                                            double(grid_.dim() == 3 ? 8 : 4), row);
+    VOXL_CUDA(cudaGetLastError());
+    double h[5];
+    VOXL_CUDA(cudaMemcpyAsync(h, row, sizeof h, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    unsigned int any;
+    std::memcpy(&any, &h[4], sizeof any);
+    out[0] = h[0];
+    out[1] = std::sqrt(h[1]);  // the kernels reduce |u|^2
+    out[2] = h[2];
+    if (!d) return;
+    d->mass = out[0];
+    d->max_speed = out[1];
+    if (!any) return;
+    // name the first unstable cell in canonical order (levels finest first)
+    const unsigned long long none = ~0ull;
+    VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
     long long cell0 = 0;
     for (std::size_t l = 0; l < lv_.size(); ++l) {
         Level* V = lv_[l];
-        double* part = d_diag_ + per_level * l;
-        VOXL_CUDA(cudaMemsetAsync(part, 0, per_level * sizeof(double), stream_));
         const long long n = V->n_active;
-        const int lb = log2_exact(V->ext.block_volume());
         if (n > 0) {
+            const int lb = log2_exact(V->ext.block_volume());
             mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto, auto) {
                 using L = decltype(lat);
                 using R = decltype(real);
-                ShiftQ<L::Q> sh{};
-                for (int i = 0; i < L::Q; ++i) sh.v[i] = esize_ == 8 ? 0.0 : L::w(i);
                 mres_slot_probe_kernel<L, R><<<kMresProbeBlocks, 256, 0, stream_>>>(
-                    static_cast<const R*>(V->cur), V->slots, n, lb, sh, cell0, part, bad);
+                    static_cast<const R*>(V->cur), V->slots, n, lb, shift_of(lat), cell0, d_diag_, bad);
             });
             VOXL_CUDA(cudaGetLastError());
         }
         cell0 += n;
     }
-    mres_probe_final<<<1, 32, 0, stream_>>>(d_diag_, int(lv_.size()), kMresProbeBlocks,
-                                            double(grid_.dim() == 3 ? 8 : 4), row);
-    VOXL_CUDA(cudaGetLastError());
-    double h[4];
-    VOXL_CUDA(cudaMemcpyAsync(h, row, sizeof h, cudaMemcpyDeviceToHost, stream_));
+    unsigned long long b = 0;
+    VOXL_CUDA(cudaMemcpyAsync(&b, bad, sizeof b, cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
-    out[0] = h[0];
-    out[1] = h[1];
-    out[2] = h[2];
-    if (d) {
-        unsigned long long b;
-        std::memcpy(&b, &h[3], sizeof b);
-        d->mass = h[0];
-        d->max_speed = h[1];
-        if (b != ~0ull) {
-            d->unstable = 1;
-            d->bad_voxel = std::int64_t(b >> 5);
-            d->bad_population = int(b & 31u);
-        }
-    }
+    d->unstable = 1;
+    d->bad_voxel = std::int64_t(b >> 5);
+    d->bad_population = int(b & 31u);
 }
 
 DenseDiag MultiResEngine::probe() {

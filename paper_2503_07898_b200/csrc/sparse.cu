@@ -13,9 +13,11 @@
 #include "lattice.cuh"
 #include "digest.cuh"
 #include "canon_io.cuh"
+#include "block_probe.cuh"
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 
 namespace voxl_b200 {
@@ -48,6 +50,11 @@ struct SparseArgs {
     double shift[Q];  // w_i for shifted fp32 storage
     int step;
     int* error_flag;
+    // fused probe_field (DIAG kernels): per-warp (mass, |u|^2) partials at
+    // slot (diag_offset + CTA) * warps + warp; any unstable cell sets *diag_bad
+    double* diag_partial;
+    long long diag_offset;
+    unsigned int* diag_bad;
 };
 
 /// equilibrium (lattice.cpp:104-113) at given (rho, u), reference op order.
@@ -138,7 +145,7 @@ __device__ __forceinline__ bool regularized_dev(int sign, const R (&ubc)[3], R (
 template <int E>
 constexpr int kSplit = E == 8 ? 2 : 1;
 
-template <class L, class R, bool Exact, int E, int MODE>
+template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && sizeof(R) == 4 ? 6 : 1)
     sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
     constexpr int Q = L::Q;
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && si
     constexpr int W = BV >= 64 ? BV / 64 : 1;
     constexpr int S = kSplit<E>;
     const int b = A.block_begin + int(blockIdx.x) / S;
-    if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip
+    if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip (DIAG: partials pre-zeroed)
     __shared__ const R* s_ptr[27];  // component-0 plane of neighbour block d (own block if absent)
     __shared__ int s_nbr[27];
     __shared__ unsigned long long s_mask[27][W];
@@ -163,6 +170,7 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && si
     // CTA-uniform: every block of the 27-neighbourhood exists and is fully
     // active, so no pull can hit a solid and the mask tests are skipped.
     const bool full = s_full != 0;
+    bool live = true;
     if (!full) {
         for (int j = tid; j < 27 * W; j += BV / S) {
             const int d = j / W, w = j % W;
@@ -170,8 +178,16 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && si
             s_mask[d][w] = nb >= 0 ? A.masks[(long long)nb * W + w] : 0ull;
         }
         __syncthreads();
-        if (!((s_mask[13][t >> 6] >> (t & 63)) & 1ull)) return;  // inactive slot
+        live = (s_mask[13][t >> 6] >> (t & 63)) & 1ull;
+        if constexpr (!DIAG) {
+            if (!live) return;  // inactive slot
+        }
     }
+    // fused probe_field terms of this cell (DIAG)
+    using P = std::conditional_t<Exact || sizeof(R) == 8, double, float>;
+    P dg_mass = P(0), dg_v2 = P(0);
+    bool dg_bad = false;
+    if (live) [&] {
     constexpr int LOG = E == 8 ? 3 : (E == 4 ? 2 : (E == 2 ? 1 : 0));
     const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
     const long long self_base = (long long)b * Q * BV;
@@ -238,14 +254,36 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && si
             }
         }
     }
-    R rho, uu[3];
+    R rho, uu[3], dr = R(0);
     if constexpr (Exact) bgk_relax<L, R, true>(g, A.omega, A.keep, rho, uu, ok);
-    else bgk_relax_shifted<L, R>(g, A.omega, A.keep, rho, uu, ok);
+    else bgk_relax_shifted<L, R>(g, A.omega, A.keep, rho, uu, ok, DIAG ? &dr : nullptr);
     if (!ok) atomicMin(A.error_flag, A.step);
+    if constexpr (DIAG) probe_voxel<L, R, Exact, P>(g, rho, dr, uu, dg_mass, dg_v2, dg_bad);
     static_for<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
         A.nxt[self_base + (long long)i * BV + t] = g[i];
     });
+    }();
+
+    // Fused probe_field (lbm.cpp:116-138): per-warp partials (fixed slots,
+    // fixed-order reduction later); an unstable cell only raises a flag --
+    // the engine names it with the canonical-order probe (rare path).
+    if constexpr (DIAG) {
+        if (live && dg_bad) atomicOr(A.diag_bad, 1u);
+        P pm = dg_mass, pv = dg_bad ? P(0) : dg_v2;
+        for (int o = 16; o > 0; o >>= 1) {
+            pm += __shfl_xor_sync(0xffffffffu, pm, o);
+            pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
+        }
+        double mass = double(pm);
+        if constexpr (std::is_same_v<P, float>) mass += double(__popc(__ballot_sync(0xffffffffu, live)));
+        if ((tid & 31) == 0) {
+            constexpr int kWarps = (BV / S + 31) / 32;
+            const long long slot = (A.diag_offset + (long long)blockIdx.x) * kWarps + (tid >> 5);
+            A.diag_partial[2 * slot] = mass;
+            A.diag_partial[2 * slot + 1] = double(pv);
+        }
+    }
 }
 
 template <int Q, class R>
@@ -262,30 +300,29 @@ __global__ void sparse_probe_kernel(const R* buf, const std::int64_t* slots, lon
                                     unsigned long long* bad) {
     constexpr int Q = L::Q;
     double mass = 0.0, vmax = 0.0;
+    const int lb = __ffs(bv) - 1;  // block volume is a power of two
     for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
         const long long slot = slots[v];
-        const long long b = slot / bv, local = slot % bv;
-        double f[Q];
-        bool badv = false;
-        int bp = 0;
+        const R* p = buf + ((slot >> lb) * Q << lb) + (slot & (bv - 1));
+        R raw[Q];
+        static_for<Q>([&](auto I) {  // all loads in flight before the fp64 arithmetic
+            constexpr int i = decltype(I)::value;
+            raw[i] = p[(long long)i * bv];
+        });
+        int bp = -1;
         double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
-        for (int c = 0; c < Q; ++c) {
-            f[c] = double(buf[(b * Q + c) * bv + local]) + A.shift[c];
-            if (!badv && (!isfinite(f[c]) || fabs(f[c]) > 1e3)) {
-                badv = true;
-                bp = c;
-            }
-        }
         static_for<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            mass += f[i];
-            r += f[i];
-            mx = acc_term<double, false, L::ex(i)>(mx, f[i]);
-            my = acc_term<double, false, L::ey(i)>(my, f[i]);
-            mz = acc_term<double, false, L::ez(i)>(mz, f[i]);
+            const double fi = double(raw[i]) + A.shift[i];
+            if (bp < 0 && !(fabs(fi) <= 1e3)) bp = i;
+            mass += fi;
+            r += fi;
+            mx = acc_term<double, false, L::ex(i)>(mx, fi);
+            my = acc_term<double, false, L::ey(i)>(my, fi);
+            mz = acc_term<double, false, L::ez(i)>(mz, fi);
         });
-        if (badv || !(r > 0.0)) {
-            atomicMin(bad, ((unsigned long long)v << 5) | (unsigned long long)bp);
+        if (bp >= 0 || !(r > 0.0)) {
+            atomicMin(bad, ((unsigned long long)v << 5) | (unsigned long long)(bp < 0 ? 0 : bp));
         } else {
             const double ux = mx / r, uy = my / r, uz = mz / r;
             vmax = fmax(vmax, sqrt(ux * ux + uy * uy + uz * uz));
@@ -305,18 +342,6 @@ __global__ void sparse_probe_kernel(const R* buf, const std::int64_t* slots, lon
     if (threadIdx.x == 0) {
         partial[2 * blockIdx.x] = sm[0];
         partial[2 * blockIdx.x + 1] = sv[0];
-    }
-}
-
-__global__ void sparse_probe_final(const double* partial, int n, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double m = 0.0, v = 0.0;
-        for (int i = 0; i < n; ++i) {
-            m += partial[2 * i];
-            v = fmax(v, partial[2 * i + 1]);
-        }
-        out[0] = m;
-        out[1] = v;
     }
 }
 
@@ -341,9 +366,23 @@ struct SparseOps {
     static void launch_e(SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
         if (nblocks <= 0) return;
         constexpr int S = kSplit<E>;
-        if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy><<<nblocks * S, E * E * E / S, 0, st>>>(A);
-        else sparse_step_kernel<L, R, Exact, E, kLight><<<nblocks * S, E * E * E / S, 0, st>>>(A);
+        const dim3 grid(nblocks * S), block(E * E * E / S);
+        if (A.diag_partial) {
+            if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy, true><<<grid, block, 0, st>>>(A);
+            else sparse_step_kernel<L, R, Exact, E, kLight, true><<<grid, block, 0, st>>>(A);
+            A.diag_offset += (long long)nblocks * S;
+        } else {
+            if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy><<<grid, block, 0, st>>>(A);
+            else sparse_step_kernel<L, R, Exact, E, kLight><<<grid, block, 0, st>>>(A);
+        }
         VOXL_CUDA(cudaGetLastError());
+    }
+
+    /// fused-probe partial slots (one per warp) of `nblocks` blocks
+    static long long diag_slots(int edge, long long nblocks) {
+        const int s = edge == 8 ? kSplit<8> : kSplit<4>;
+        const int threads = edge * edge * edge / s;
+        return nblocks * s * ((threads + 31) / 32);
     }
 
     static void launch(int edge, SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
@@ -481,6 +520,7 @@ SparseEngine::~SparseEngine() {
     cudaFree(d_slots_);
     cudaFree(d_error_);
     cudaFree(d_diag_);
+    cudaFree(diag_partials_);
     if (side_) {
         cudaStreamSynchronize(side_);
         cudaEventDestroy(ev_fork_);
@@ -559,12 +599,16 @@ void SparseEngine::digest(unsigned long long out[2]) {
     VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l) {
+void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, double* diag_partial,
+                          unsigned int* diag_bad) {
     // sweep / step (sparse.cpp:359-394) as real kernels.
     sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
         using Ops = decltype(ops);
         auto A = Ops::base_args(cfg_);
         using R = std::remove_pointer_t<decltype(A.nxt)>;
+        A.diag_partial = diag_partial;  // fused probe_field (step_probe)
+        A.diag_bad = diag_bad;
+        A.diag_offset = 0;
         A.cur = static_cast<const R*>(buf_[cur_]);
         A.nxt = static_cast<R*>(buf_[cur_ ^ 1]);
         A.nbr = d_nbr_;
@@ -648,6 +692,45 @@ void SparseEngine::step(int n) {
     check_errors();
 }
 
+DenseDiag SparseEngine::step_probe() {
+    // One step with probe_field fused into the step kernels (run_sparse's
+    // per-step row, solver.cpp:287-291): per-warp partials, a fixed-order
+    // two-stage reduction and one 32-byte row back to the host.
+    long long slots = 0;
+    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+        slots = decltype(ops)::diag_slots(grid_.edge(), grid_.num_blocks());
+    });
+    if (cfg_.strategy == Strategy::DisagBitmask) slots *= 2;  // both sweeps visit every block
+    if (diag_partials_len_ < std::size_t(2 * slots)) {
+        cudaFree(diag_partials_);
+        VOXL_CUDA(cudaMalloc(&diag_partials_, 2 * slots * sizeof(double)));
+        diag_partials_len_ = std::size_t(2 * slots);
+    }
+    double* stage = d_diag_;
+    double* out = d_diag_ + 2 * kSpProbeBlocks;
+    auto* bad_any = reinterpret_cast<unsigned int*>(out + 3);
+    VOXL_CUDA(cudaMemsetAsync(diag_partials_, 0, 2 * slots * sizeof(double), stream_));  // skipped CTAs add 0
+    VOXL_CUDA(cudaMemsetAsync(out, 0, 4 * sizeof(double), stream_));
+    launch(0, nullptr, nullptr, diag_partials_, bad_any);
+    partials_reduce_kernel<<<kSpProbeBlocks, 256, 0, stream_>>>(diag_partials_, slots, stage);
+    block_probe_final<<<1, 32, 0, stream_>>>(stage, kSpProbeBlocks, out);
+    VOXL_CUDA(cudaGetLastError());
+    double row[4];
+    int flag = INT_MAX;
+    VOXL_CUDA(cudaMemcpyAsync(row, out, sizeof row, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaStreamSynchronize(stream_));
+    if (flag != INT_MAX)
+        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": non-positive density");
+    unsigned int any;
+    std::memcpy(&any, &row[3], sizeof any);
+    if (any) return probe();  // names the first unstable cell in canonical order
+    DenseDiag d;
+    d.mass = row[0];
+    d.max_speed = std::sqrt(row[1]);
+    return d;
+}
+
 void SparseEngine::step_identity(int n) {
     // step_identity (sparse.cpp:396-404): the sweeps copy every active voxel
     // cur -> nxt. Inactive slots are never observable (canonical_state reads
@@ -686,30 +769,47 @@ double SparseEngine::timed_steps(int n, double* boundary_ms, double* light_ms) {
 }
 
 DenseDiag SparseEngine::probe() {
-    ensure_slots();
-    const long long n = grid_.num_active();
-    unsigned long long none = ~0ull;
-    auto* bad = reinterpret_cast<unsigned long long*>(d_diag_ + 2 * kSpProbeBlocks + 2);
-    VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
+    // probe_field over canonical_state (solver.cpp:290): sums and max |u| in
+    // storage order (block_probe.cuh); the canonical-order kernel only runs
+    // to name the first unstable cell when there is one.
+    double* partial = d_diag_;
+    double* out = d_diag_ + 2 * kSpProbeBlocks;
+    auto* bad = reinterpret_cast<unsigned long long*>(out + 2);
+    auto* bad_any = reinterpret_cast<unsigned int*>(out + 3);
+    VOXL_CUDA(cudaMemsetAsync(out, 0, 4 * sizeof(double), stream_));
+    double res[2];
+    unsigned int any = 0;
     sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
         using Ops = decltype(ops);
         using L = std::conditional_t<Ops::Q == 19, D3Q19, D3Q27>;
         auto A = Ops::base_args(cfg_);
         using R = std::remove_pointer_t<decltype(A.nxt)>;
-        sparse_probe_kernel<L, R><<<kSpProbeBlocks, 256, 0, stream_>>>(static_cast<const R*>(buf_[cur_]), d_slots_,
-                                                                       n, grid_.block_volume(), A, d_diag_, bad);
-        sparse_probe_final<<<1, 32, 0, stream_>>>(d_diag_, kSpProbeBlocks, d_diag_ + 2 * kSpProbeBlocks);
-        VOXL_CUDA(cudaGetLastError());
+        launch_block_probe<L, R>(static_cast<const R*>(buf_[cur_]), d_masks_, grid_.mask_words(),
+                                 grid_.block_volume(), grid_.num_blocks(), A.shift, partial, out, bad_any, stream_);
     });
-    double res[2];
-    unsigned long long b = 0;
-    VOXL_CUDA(cudaMemcpyAsync(res, d_diag_ + 2 * kSpProbeBlocks, sizeof res, cudaMemcpyDeviceToHost, stream_));
-    VOXL_CUDA(cudaMemcpyAsync(&b, bad, sizeof b, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(res, out, sizeof res, cudaMemcpyDeviceToHost, stream_));
+    VOXL_CUDA(cudaMemcpyAsync(&any, bad_any, sizeof any, cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
     DenseDiag d;
     d.mass = res[0];
-    d.max_speed = res[1];
-    if (b != ~0ull) {
+    d.max_speed = std::sqrt(res[1]);
+    if (any) {
+        ensure_slots();
+        const long long n = grid_.num_active();
+        const unsigned long long none = ~0ull;
+        VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
+        sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
+            using Ops = decltype(ops);
+            using L = std::conditional_t<Ops::Q == 19, D3Q19, D3Q27>;
+            auto A = Ops::base_args(cfg_);
+            using R = std::remove_pointer_t<decltype(A.nxt)>;
+            sparse_probe_kernel<L, R><<<kSpProbeBlocks, 256, 0, stream_>>>(
+                static_cast<const R*>(buf_[cur_]), d_slots_, n, grid_.block_volume(), A, partial, bad);
+            VOXL_CUDA(cudaGetLastError());
+        });
+        unsigned long long b = 0;
+        VOXL_CUDA(cudaMemcpyAsync(&b, bad, sizeof b, cudaMemcpyDeviceToHost, stream_));
+        VOXL_CUDA(cudaStreamSynchronize(stream_));
         d.unstable = 1;
         d.bad_voxel = std::int64_t(b >> 5);
         d.bad_population = int(b & 31);

@@ -65,6 +65,7 @@ public:
     /// summed boundary-kernel and non-boundary-kernel ms.
     double timed_steps(int n, double* boundary_ms, double* light_ms);
     DenseDiag probe();
+    DenseDiag step_probe();  // one step with probe_field fused into the step kernels
     void check_errors();
 
 private:
@@ -97,7 +98,10 @@ private:
     cudaStream_t side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
 
-    void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l);
+    void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l, double* diag_partial = nullptr,
+                unsigned int* diag_bad = nullptr);
+    double* diag_partials_ = nullptr;  // fused-probe per-warp partials (step_probe)
+    std::size_t diag_partials_len_ = 0;
     void ensure_slots();
     void transfer(double* host, bool to_device, unsigned long long* digest);
 };

@@ -243,8 +243,7 @@ def run_sparse(c: SolverConfig) -> RunResult:
     eng = SparseEngine(c.domain, act, tau=c.tau, u_bc=c.velocity, block_edge=c.block_edge, strategy=c.strategy,
                        precision=c.precision, lattice=c.lattice)
     for step in range(c.steps):
-        eng.step(1)
-        d = eng.probe()
+        d = eng.step_probe()  # step + probe_field, fused on the device
         _unstable(d, step)
         r.diagnostics.append((step, d.mass, d.max_speed))
     r.field = eng.get_state()

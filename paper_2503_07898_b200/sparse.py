@@ -188,6 +188,13 @@ class SparseEngine:
         check(lib.voxl_sparse_probe(self._h, C.byref(d)))
         return d
 
+    def step_probe(self):
+        """One step with probe_field fused into the step kernels (run_sparse's
+        per-step diagnostics row)."""
+        d = _capi.Diag()
+        check(lib.voxl_sparse_step_probe(self._h, C.byref(d)))
+        return d
+
     def close(self):
         if self._h:
             check(lib.voxl_sparse_destroy(self._h))

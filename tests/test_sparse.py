@@ -249,3 +249,26 @@ def test_state_io_multichunk_roundtrip(precision):
     else:
         ww = np.tile(w, n)
         assert np.array_equal(out, (f - ww).astype(np.float32).astype(np.float64) + ww)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["naive", "disag_bitmask", "disag_mem"])
+@pytest.mark.parametrize("precision,edge", [("fp64", 8), ("fp32", 8), ("fp64", 4)])
+def test_step_probe_equals_step_plus_probe(strategy, precision, edge):
+    """The fused probe (per-warp partials of the step kernels) gives the state
+    of a plain step and the diagnostics of probe() on it: fp64 to summation
+    order, fp32 to the moment rounding (pre- vs post-collision moments)."""
+    dom = (40, 32, 24)
+    a = V.SparseEngine(dom, block_edge=edge, strategy=strategy, precision=precision)
+    b = V.SparseEngine(dom, block_edge=edge, strategy=strategy, precision=precision)
+    tol_m, tol_u = (1e-12, 1e-12) if precision == "fp64" else (1e-9, 1e-6)
+    for _ in range(6):
+        da = a.step_probe()
+        b.step(1)
+        db = b.probe()
+        assert da.unstable == 0 and db.unstable == 0
+        assert abs(da.mass - db.mass) <= tol_m * db.mass
+        assert abs(da.max_speed - db.max_speed) <= tol_u * db.max_speed + 1e-12
+    assert np.array_equal(a.get_state(), b.get_state())
+    a.close()
+    b.close()

@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_sparse.py tests/test_multires.py tests/test_solver.py tests/test_capi.py tests/test_fullsize.py -q -m gpu -p no:cacheprovider > gpurun_out/pytest33.txt 2>&1
+timeout 900 python tools/run_paths.py > gpurun_out/runpaths33.txt 2>&1
+tail -2 gpurun_out/pytest33.txt; grep -E "^FAILED|^E " gpurun_out/pytest33.txt | head -20; cat gpurun_out/runpaths33.txt

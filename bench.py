@@ -280,6 +280,8 @@ def main():
     e2e = None
     if not args.no_e2e and world == 1 and rank == 0:
         e2e = e2e_run(args, V, np)
+    elif not args.no_e2e and world > 1:
+        e2e = e2e_run_dist(args, eng, dist, voxels_total, share, np)
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
         try:
@@ -307,7 +309,9 @@ def main():
                          "peak_kind": peak_kind,
                          "bytes_per_lup": BYTES_PER_LUP, "voxels_per_launch": voxels_local,
                          "avg_kernel_ms": round(avg_kernel_ms, 4),
-                         "frac_of_8tbs": round(achieved / 8000.0, 4)},
+                         "frac_of_8tbs": round(achieved / 8000.0, 4),
+                         "peak_note": "MEASURED_PEAKS hbm_gbs is a torch copy; the float4 copy ceiling of "
+                                      "tools/micro/membw.cu is ~6.8 TB/s on this pool, so frac can exceed 1"},
             "clocks": clocks,
             "gpu_launches": args.steps * (1 if world == 1 else 4),
             "diag": {"mass": diag.mass, "max_speed": diag.max_speed, "unstable": diag.unstable},
@@ -351,6 +355,58 @@ def e2e_run(args, V, np):
             "h2d_bytes_per_step": int(bytes_in / steps), "d2h_bytes_per_step": int(bytes_out / steps),
             "domain": list(dom), "seconds": round(dt, 3),
             "path": "DenseEngine.set_canonical(host fp64) + steps x step_probe (diag row D2H) + get_canonical(host fp64)"}
+
+
+def e2e_run_dist(args, eng, dist, voxels_total, share, np):
+    """e2e at N ranks through the same API: every rank uploads its slab of the
+    fp64 canonical field from pinned host memory (fill_canonical of its
+    partition), refreshes the halos, runs K steps each with its slab's
+    probe_field row read back (rows combine as sum / max; no per-step
+    collective), and downloads its slab. Wall time max over ranks."""
+    import torch
+
+    k0, k1 = eng.slab()
+    dom = eng.desc["domain"]
+    elems = (k1 - k0) * dom[0] * dom[1] * Q
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 1 << 40
+    # two pinned slabs per rank; every rank of the node allocates at once
+    if 2 * elems * 8 * eng.world > 0.6 * avail:
+        return {"value": None, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "skipped": f"host memory: {2 * elems * 8 * eng.world / 2**30:.0f} GiB of pinned slabs needed, "
+                           f"{avail / 2**30:.0f} GiB available"}
+    host_in = torch.empty(elems, dtype=torch.float64, pin_memory=True).numpy()
+    host_out = torch.empty(elems, dtype=torch.float64, pin_memory=True).numpy()
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    host_in.reshape(-1, Q)[:] = w
+    steps = args.steps
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.set_canonical_planes(host_in, k0, k1)
+    eng.refresh_halos()
+    last = None
+    for _ in range(steps):
+        last = eng.step_probe()
+    eng.get_canonical_planes(k0, k1, out=host_out)
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt, last.max_speed], dtype=torch.float64, device="cpu" if share else "cuda")
+    m = torch.tensor([last.mass], dtype=torch.float64, device=t.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(m)
+    dt = float(t[0].item())
+    bytes_in = voxels_total * Q * 8
+    bytes_out = voxels_total * Q * 8 + steps * 32 * eng.world
+    return {"value": round(voxels_total * steps / dt / 1e6, 1), "unit": "MLUPS",
+            "h2d_bytes_per_step": int(bytes_in / steps), "d2h_bytes_per_step": int(bytes_out / steps),
+            "domain": list(dom), "seconds": round(dt, 3), "final_mass": float(m.item()),
+            "final_max_speed": float(t[1].item()),
+            "path": "per rank: DistributedDense.set_canonical_planes(host fp64 slab) + refresh_halos + "
+                    "steps x step_probe (rank diag row D2H) + get_canonical_planes; wall time max over ranks"}
 
 
 if __name__ == "__main__":

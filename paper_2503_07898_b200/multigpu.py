@@ -155,10 +155,13 @@ class DistributedDense:
         h = np.ascontiguousarray(host, np.float64)
         check(lib.voxl_dense_set_planes(self.eng._h, h.ctypes.data, k_begin, k_end))
 
-    def get_canonical_planes(self, k_begin, k_end):
+    def get_canonical_planes(self, k_begin, k_end, out=None):
         dom = self.desc["domain"]
         cross = dom[0] * (dom[1] if len(dom) == 3 and self.desc["lattice"] != "D2Q9" else 1)
-        out = np.empty((k_end - k_begin) * cross * self.eng.q, np.float64)
+        n = (k_end - k_begin) * cross * self.eng.q
+        if out is None:
+            out = np.empty(n, np.float64)
+        assert out.dtype == np.float64 and out.size == n and out.flags.c_contiguous
         check(lib.voxl_dense_get_planes(self.eng._h, out.ctypes.data, k_begin, k_end))
         return out
 
@@ -187,6 +190,17 @@ class DistributedDense:
                 self.eng.enqueue(1)
                 self._nccl_exchange()
             self.eng.synchronize()
+
+    def step_probe(self):
+        """One step with this rank's probe_field fused (lbm.cpp:116-138); the
+        diagnostics row covers the rank's own slab. Rows combine across ranks
+        as mass = sum, max_speed = max (`combine_rows`), so run()'s per-step
+        diagnostics need no per-step collective."""
+        d = self.eng.step_probe()
+        if self.halo_mode != "zero_copy":
+            self._nccl_exchange()
+            self.eng.synchronize()
+        return d
 
     def timed_steps(self, n):
         if self.halo_mode == "zero_copy":

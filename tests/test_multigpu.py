@@ -110,7 +110,9 @@ def _gpu_worker(rank, world, port, result_q):
     s = dom[0] * dom[1] * 19
     eng.set_canonical_planes(init[k0 * s:k1 * s], k0, k1)
     eng.refresh_halos()
-    eng.step(30)
+    eng.step(20)
+    for _ in range(10):
+        eng.step_probe()  # run()'s per-step probe path, fused into the step
     out = eng.get_canonical_planes(k0, k1)
     d = eng.probe()
     result_q.put((rank, k0, k1, out, d.mass))
@@ -154,9 +156,12 @@ def test_bench_multirank_path_on_one_gpu():
     env = dict(os.environ, VOXL_SHARE_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--steps", "10", "--warmup",
-           "3", "--size", "64", "--no-e2e", "--no-cpu"]
+           "3", "--size", "64", "--no-cpu"]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=root, env=env, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "strong"
     assert abs(line["diag"]["mass"] - 64 ** 3) < 1e-6 * 64 ** 3 and line["diag"]["unstable"] == 0
+    e2e = line["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] == 64 ** 3 * 19 * 8 // 10
+    assert abs(e2e["final_mass"] - 64 ** 3) < 1e-6 * 64 ** 3

@@ -22,6 +22,7 @@ struct MresArgs {
     const R* cur;
     R* nxt;
     R* post;
+    R* post_ahead;  // kStreamAhead: the other post buffer (next step's jump-block collide)
     const std::int32_t* nbr;
     const std::uint64_t* amask;
     const std::uint8_t* cls;
@@ -96,11 +97,17 @@ __global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_cons
 /// for in-domain sources (active, ghost or ring slots of the post buffer --
 /// every one exists by construction, so no activity test is needed), own
 /// src[v][opp i] plus the lid term for wall sources (stream_voxel,
-/// multires.cpp:485-531). COLLIDE = false: stream_level (write g). COLLIDE =
-/// true: the fused uniform-block kernel (uniform blocks keep post-collision
+/// multires.cpp:485-531). MODE kStream: stream_level (write g). MODE kFused:
+/// the fused uniform-block kernel (uniform blocks keep post-collision
 /// storage, so collide-after-pull is the reference's collide-before-pull of
-/// the next step), one pass at 2 Q sizeof(real) bytes per update.
-template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER, bool SOLID>
+/// the next step), one pass at 2 Q sizeof(real) bytes per update. MODE
+/// kStreamAhead: the fused-mode jump-block stream -- writes g (the next cur,
+/// which explosion/coalescence and readout need) and also BGK(g) into the
+/// other post buffer, i.e. the next step's collide_level of the jump blocks
+/// (multires.cpp:443-456), so fused mode launches no separate collide.
+constexpr int kStream = 0, kFused = 1, kStreamAhead = 2;
+
+template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID>
 __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src);
 
 /// CTAs per block: 8^3 blocks are split over two 256-thread CTAs (6 CTAs / SM
@@ -110,7 +117,7 @@ constexpr int kSplit = E == 8 ? 2 : 1;
 
 /// SOLID: the level has obstacle cells (a separate instantiation, so grids
 /// without them keep the register budget of the plain kernel).
-template <class L, class R, bool Exact, int E, bool COLLIDE, bool SOLID>
+template <class L, class R, bool Exact, int E, int MODE, bool SOLID>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4) ? 6 : 1)
     mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W, S = kSplit<E>;
@@ -138,18 +145,18 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
     if (!s_full && !((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
     if constexpr (SOLID) {
         if (s_solid) {
-            mres_pull_body<L, R, Exact, E, COLLIDE, false, true>(A, b, t, s_src);
+            mres_pull_body<L, R, Exact, E, MODE, false, true>(A, b, t, s_src);
             return;
         }
     }
-    if (s_inner) mres_pull_body<L, R, Exact, E, COLLIDE, true, false>(A, b, t, s_src);
-    else mres_pull_body<L, R, Exact, E, COLLIDE, false, false>(A, b, t, s_src);
+    if (s_inner) mres_pull_body<L, R, Exact, E, MODE, true, false>(A, b, t, s_src);
+    else mres_pull_body<L, R, Exact, E, MODE, false, false>(A, b, t, s_src);
 }
 
 /// Pull over blocks [begin, begin + count): the part below `n_plain` (blocks
 /// that cannot see a solid cell) runs the plain kernel, the rest the
 /// solid-aware one when the level has obstacle cells.
-template <class L, class R, bool Exact, int E, bool COLLIDE>
+template <class L, class R, bool Exact, int E, int MODE>
 void launch_pull(MresArgs<L::Q, R> A, int begin, int count, int n_plain, cudaStream_t st) {
     const dim3 block(E * E * E / kSplit<E>);
     const int split = std::min(begin + count, std::max(begin, n_plain));
@@ -157,17 +164,17 @@ void launch_pull(MresArgs<L::Q, R> A, int begin, int count, int n_plain, cudaStr
     if (split > begin) {
         A.block_begin = begin;
         A.nsolid = nullptr;
-        mres_pull_kernel<L, R, Exact, E, COLLIDE, false><<<(split - begin) * kSplit<E>, block, 0, st>>>(A);
+        mres_pull_kernel<L, R, Exact, E, MODE, false><<<(split - begin) * kSplit<E>, block, 0, st>>>(A);
     }
     if (begin + count > split) {
         A.block_begin = split;
         A.nsolid = ns;
-        if (ns) mres_pull_kernel<L, R, Exact, E, COLLIDE, true><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
-        else mres_pull_kernel<L, R, Exact, E, COLLIDE, false><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
+        if (ns) mres_pull_kernel<L, R, Exact, E, MODE, true><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
+        else mres_pull_kernel<L, R, Exact, E, MODE, false><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
     }
 }
 
-template <class L, class R, bool Exact, int E, bool COLLIDE, bool INNER, bool SOLID>
+template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID>
 __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src) {
     constexpr int Q = L::Q, BV = E * E * E;
     using Ar = Arith<R, Exact>;
@@ -211,18 +218,26 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
             g[i] = v;
         }
     });
-    if constexpr (COLLIDE) {
+    auto collide = [&] {
         bool ok = true;
         R rho, u[3];
         if constexpr (Exact) bgk_relax<L, R, true>(g, A.omega, A.keep, rho, u, ok);
         else bgk_relax_shifted<L, R>(g, A.omega, A.keep, rho, u, ok);
         if (!ok) atomicMin(A.error_flag, A.step);
-    }
-    R* out = A.nxt + (long long)b * Q * BV + t;
+    };
+    if constexpr (MODE == kFused) collide();
+    const long long cell = (long long)b * Q * BV + t;
     static_for<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
-        out[i * BV] = g[i];
+        A.nxt[cell + i * BV] = g[i];
     });
+    if constexpr (MODE == kStreamAhead) {
+        collide();
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            A.post_ahead[cell + i * BV] = g[i];
+        });
+    }
 }
 
 /// explode (multires.cpp:458-467): ghost cells of the fine level <- the
@@ -876,7 +891,12 @@ void MultiResEngine::launch_stream(int l, bool jump_only, cudaStream_t s) {
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
-        launch_pull<L, R, X, E, false>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st);  // post -> nxt
+        if (cfg_.fused) {  // post -> nxt, and BGK(nxt) -> the other post buffer
+            A.post_ahead = static_cast<R*>(V->post[V->parity ^ 1]);
+            launch_pull<L, R, X, E, kStreamAhead>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st);
+        } else {
+            launch_pull<L, R, X, E, kStream>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st);  // post -> nxt
+        }
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTStream, b, st);
@@ -898,7 +918,7 @@ void MultiResEngine::gather_uniform(int l) {
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
         A.post = static_cast<R*>(V->post[V->parity ^ 1]);
         A.nxt = static_cast<R*>(V->cur);
-        launch_pull<L, R, X, E, false>(A, 0, V->n_uni, V->n_plain, stream_);
+        launch_pull<L, R, X, E, kStream>(A, 0, V->n_uni, V->n_plain, stream_);
     });
     VOXL_CUDA(cudaGetLastError());
 }
@@ -911,12 +931,15 @@ void MultiResEngine::sync_state() {
 }
 
 void MultiResEngine::load_uniform_post() {
-    // After cur changed on the host side: post of the uniform cells = BGK(cur)
-    // (what the reference's next collide_level computes).
+    // After cur changed on the host side: post = BGK(cur) for every block
+    // (what the reference's next collide_level computes). From then on the
+    // fused uniform kernel keeps the uniform blocks' post current and the
+    // jump-block stream (kStreamAhead) the jump blocks', so fused mode never
+    // launches collide_level on its own.
     if (!cfg_.fused) return;
     for (int l = 0; l < int(lv_.size()); ++l) {
         Level* V = lv_[l];
-        if (V->n_uni == 0) continue;
+        if (V->n_all == 0) continue;
         mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
             using L = decltype(lat);
             using R = decltype(real);
@@ -924,7 +947,7 @@ void MultiResEngine::load_uniform_post() {
             constexpr int E = decltype(e)::value;
             auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
             A.block_begin = 0;
-            mres_collide_kernel<L, R, X, E><<<V->n_uni, E * E * E, 0, stream_>>>(A);
+            mres_collide_kernel<L, R, X, E><<<V->n_all, E * E * E, 0, stream_>>>(A);
         });
         VOXL_CUDA(cudaGetLastError());
     }
@@ -944,7 +967,7 @@ void MultiResEngine::launch_fused(int l) {
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
         A.nxt = static_cast<R*>(V->post[V->parity ^ 1]);  // post[p] -> post[p^1]
-        launch_pull<L, R, X, E, true>(A, 0, V->n_uni, V->n_plain, stream_);
+        launch_pull<L, R, X, E, kFused>(A, 0, V->n_uni, V->n_plain, stream_);
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTFused, b);
@@ -995,8 +1018,9 @@ void MultiResEngine::launch_coalesce(int coarse) {
 }
 
 void MultiResEngine::advance(int l) {
-    // advance (multires.cpp:563-567)
-    launch_collide(l, cfg_.fused);
+    // advance (multires.cpp:563-567). Fused mode: the jump blocks' collide
+    // was done by the previous jump-block stream (or load_uniform_post).
+    if (!cfg_.fused) launch_collide(l, false);
     if (l > 0) {
         launch_explode(l);
         advance(l - 1);

@@ -15,5 +15,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:mres
 timeout 600 python tools/bench_paths.py sparse --n 512 --steps 20 > gpurun_out/paths_sparse_$T.txt 2>&1
 timeout 600 python tools/bench_paths.py multires --n 512 --steps 5 > gpurun_out/paths_mres_$T.txt 2>&1
 timeout 600 python tools/e2e_breakdown.py 512 200 > gpurun_out/e2e_$T.txt 2>&1
-ls gpurun_out/*_$T*; tail -c 600 gpurun_out/bench_$T.txt; cat gpurun_out/e2e_$T.txt
+# ncu reports are too large to travel back: summarise them here, keep the raw
+# per-launch metric pages as csv, and move the reports out of gpurun_out/
+for r in gpurun_out/*_$T.ncu-rep; do
+  b=${r%.ncu-rep}
+  python tools/ncu_summary.py $r > $b.md 2>&1
+  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+  mkdir -p /tmp/ncu_reps; mv $r /tmp/ncu_reps/
+done
+ls -la gpurun_out/*_$T*; tail -c 600 gpurun_out/bench_$T.txt; cat gpurun_out/e2e_$T.txt
 cut -c1-300 gpurun_out/paths_sparse_$T.txt gpurun_out/paths_mres_$T.txt

@@ -154,6 +154,11 @@ int voxl_dense_steps_done(voxl_dense* h, int* steps);
 int voxl_dense_buffer(voxl_dense* h, int partition, int which, void** ptr, size_t* bytes);
 /** cudaStream_t of the engine, as void*. */
 int voxl_dense_stream(voxl_dense* h, void** stream);
+/** Multi-process: the shared-layer stream of the OCC step (after
+ *  voxl_dense_enable_distributed). In copy halo mode the caller enqueues the
+ *  halo exchange of each step here, so it overlaps the interior kernel
+ *  (the OCC schedule, partition.hpp:173-214, with NCCL as the transport). */
+int voxl_dense_shared_stream(voxl_dense* h, void** stream);
 /** Multi-process: map a neighbour partition's buffers (IPC/peer pointers, both parities). */
 int voxl_dense_attach_peer(voxl_dense* h, int partition, void* buf0, void* buf1);
 /** Allocation-order buffer w (0/1) of an owned partition (for IPC export). */

@@ -106,6 +106,7 @@ def _load():
         "voxl_dense_steps_done": ([vp, C.POINTER(C.c_int)], C.c_int),
         "voxl_dense_buffer": ([vp, C.c_int, C.c_int, C.POINTER(vp), C.POINTER(C.c_size_t)], C.c_int),
         "voxl_dense_stream": ([vp, C.POINTER(vp)], C.c_int),
+        "voxl_dense_shared_stream": ([vp, C.POINTER(vp)], C.c_int),
         "voxl_dense_attach_peer": ([vp, C.c_int, vp, vp], C.c_int),
         "voxl_dense_raw_buffer": ([vp, C.c_int, C.c_int, C.POINTER(vp)], C.c_int),
         "voxl_dense_enable_distributed": ([vp, C.POINTER(vp)], C.c_int),

@@ -313,6 +313,13 @@ int voxl_dense_stream(voxl_dense* h, void** stream) {
     return guarded([&] { *stream = (void*)h->eng->stream(); });
 }
 
+int voxl_dense_shared_stream(voxl_dense* h, void** stream) {
+    return guarded([&] {
+        require(h->eng->shared_stream() != nullptr, "shared_stream: call voxl_dense_enable_distributed first");
+        *stream = (void*)h->eng->shared_stream();
+    });
+}
+
 int voxl_dense_attach_peer(voxl_dense* h, int p, void* b0, void* b1) {
     return guarded([&] { h->eng->attach_peer(p, b0, b1); });
 }

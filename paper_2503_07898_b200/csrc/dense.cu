@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -36,7 +37,11 @@ constexpr int kBlock = 256;  // 256-thread CTAs: +4 % DRAM throughput over 128 o
 #ifndef VOXL_DIAG_MINB
 #define VOXL_DIAG_MINB 6
 #endif
-constexpr int kDiagSlots = VOXL_DIAG_WARP ? kBlock / 32 : 1;  // fused-probe partial slots per CTA
+// fused-probe partials: VOXL_DIAG_WARP 1 = one slot per warp (no CTA barrier),
+// 0 = one slot per CTA after a CTA barrier. Measured at 512^3 (step_probe, ms):
+// per warp 3.33-3.35, per CTA 3.41-3.43, per CTA by the last warp through an
+// smem counter 3.38.
+constexpr int kDiagSlots = VOXL_DIAG_WARP ? kBlock / 32 : 1;
 
 template <int Q, class R>
 struct StepArgs {
@@ -354,12 +359,31 @@ __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
 /// Blocks the stream until both neighbours have finished the shared layers of
 /// step target-1 (RAW: our halos are filled; WAR: they no longer read the
 /// halo slots we are about to overwrite).
-__global__ void wait_flags_kernel(const unsigned* flags, int need_up, int need_low, unsigned target) {
+/// Spin until both neighbours signalled step `target`. A neighbour that never
+/// signals (its process died) must not wedge the GPU: after kHaloWaitNs the
+/// kernel records the step in flags[2] and returns; check_errors() turns that
+/// into an error on the host. Limit: VOXL_HALO_TIMEOUT_S (default 120 s).
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void wait_flags_kernel(unsigned* flags, int need_up, int need_low, unsigned target,
+                                  unsigned long long timeout_ns) {
     if (threadIdx.x != 0) return;
-    if (need_up)
-        while (ld_acquire_sys(flags + 0) < target) __nanosleep(64);
-    if (need_low)
-        while (ld_acquire_sys(flags + 1) < target) __nanosleep(64);
+    const unsigned long long t0 = global_ns();
+    for (int w = 0; w < 2; ++w) {
+        if (!(w == 0 ? need_up : need_low)) continue;
+        while (ld_acquire_sys(flags + w) < target) {
+            __nanosleep(64);
+            if (global_ns() - t0 > timeout_ns) {
+                atomicCAS(flags + 2, 0u, target + 1);  // keep the first stalled step
+                return;
+            }
+        }
+    }
 }
 
 __global__ void signal_flags_kernel(unsigned* up_slot, unsigned* low_slot, unsigned value) {
@@ -1099,6 +1123,10 @@ void DenseEngine::enable_distributed() {
         }
         VOXL_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     }
+    if (const char* e = std::getenv("VOXL_HALO_TIMEOUT_S")) {
+        const double sec = std::atof(e);
+        if (sec > 0) halo_timeout_ns_ = (unsigned long long)(sec * 1e9);
+    }
     if (!flags_) {
         VOXL_CUDA(cudaMalloc(&flags_, 4 * sizeof(std::uint32_t)));
         VOXL_CUDA(cudaMemset(flags_, 0, 4 * sizeof(std::uint32_t)));
@@ -1164,7 +1192,7 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     // S: wait -> shared(t) -> signal
     VOXL_CUDA(cudaStreamWaitEvent(shared_stream_, ev_interior_[prev], 0));
     if (zero_copy) {
-        wait_flags_kernel<<<1, 32, 0, shared_stream_>>>(flags_, up >= 0, low >= 0, t);
+        wait_flags_kernel<<<1, 32, 0, shared_stream_>>>(flags_, up >= 0, low >= 0, t, halo_timeout_ns_);
         VOXL_CUDA(cudaGetLastError());
     }
     void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
@@ -1181,9 +1209,11 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     VOXL_CUDA(cudaEventRecord(ev_shared_[par], shared_stream_));
     cur_ = out;
     ++steps_done_;
-    // Diagnostics reductions and the copy-mode exchange (issued on stream_
-    // by the caller) need the whole step: join S into I.
-    if (diag || !zero_copy) join_streams();
+    // Diagnostics reductions need the whole step: join S into I. The
+    // copy-mode exchange is issued on S by the caller (after shared(t), next
+    // to interior(t)); shared(t+1) follows it in S's order, and nothing on I
+    // touches the halo planes or the shared layers it sends.
+    if (diag) join_streams();
 }
 
 void DenseEngine::join_streams() {
@@ -1249,8 +1279,14 @@ double DenseEngine::timed_steps(int n, double* kernel_ms) {
 void DenseEngine::check_errors() {
     join_streams();
     int flag = INT_MAX;
+    std::uint32_t stalled = 0;
     VOXL_CUDA(cudaMemcpyAsync(&flag, error_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    if (distributed_ && flags_)
+        VOXL_CUDA(cudaMemcpyAsync(&stalled, flags_ + 2, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
+    if (stalled)
+        throw std::runtime_error("halo exchange stalled at step " + std::to_string(stalled - 1) +
+                                 ": a neighbour partition stopped signalling (zero-copy step flags)");
     if (flag != INT_MAX)
         throw InstabilityError("run aborted at step " + std::to_string(flag) +
                                ": macroscopic: non-positive density");

@@ -129,6 +129,7 @@ public:
     std::vector<TransferRecord> ledger_records(int step) const;
 
     cudaStream_t stream() const { return stream_; }
+    cudaStream_t shared_stream() const { return shared_stream_; }
     /// Raw device buffer of partition p (current if which == 0 else next).
     void* buffer(int p, int which) const;
     std::size_t buffer_bytes(int p) const;
@@ -169,7 +170,8 @@ private:
     cudaStream_t stream_ = nullptr;
     int* error_flag_ = nullptr;
     double* diag_scratch_ = nullptr;
-    double* diag_row_host_ = nullptr;  // pinned: step_probe's diagnostics row
+    double* diag_row_host_ = nullptr;
+    unsigned long long halo_timeout_ns_ = 120ull * 1000 * 1000 * 1000;  // zero-copy flag wait limit  // pinned: step_probe's diagnostics row
     double* diag_partials_ = nullptr;
     std::size_t diag_partials_len_ = 0;
     std::size_t diag_scratch_len_ = 0;

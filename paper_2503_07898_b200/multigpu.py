@@ -8,9 +8,13 @@ buffers and of their step-flag words through ``torch.distributed``
     wait(flags >= t) -> shared layers k=0,n-1 (+ peer stores of the 5 crossing
     populations into the neighbours' halo spans) -> signal(t+1) -> interior.
 
-The comparison path (``halo_mode="copy"``) runs the same kernels without peer
-stores and exchanges the same contiguous spans with NCCL send/recv
-(``exchange_halos``), the transport the paper's GPU baseline uses.
+The comparison path (``halo_mode="copy"``) runs the same two-stream OCC
+schedule without peer stores and exchanges the same contiguous spans with NCCL
+send/recv (``exchange_halos``), the transport the paper's GPU baseline uses.
+The exchange is enqueued on the shared-layer stream right after the shared
+layers, so it overlaps the interior kernel exactly like the zero-copy stores
+do; only the transport differs. Over gloo (ranks sharing one GPU in the tests)
+the spans are staged through host memory.
 """
 from __future__ import annotations
 
@@ -79,8 +83,9 @@ class DistributedDense:
             check(lib.voxl_dense_raw_buffer(self.eng._h, self.rank, w, C.byref(p)))
             raw.append(p.value)
         flags = C.c_void_p()
-        if halo_mode == "zero_copy":
-            check(lib.voxl_dense_enable_distributed(self.eng._h, C.byref(flags)))
+        check(lib.voxl_dense_enable_distributed(self.eng._h, C.byref(flags)))
+        if halo_mode != "zero_copy":
+            flags = C.c_void_p()  # copy mode: no step flags, NCCL orders the exchange
         handles = {"rank": self.rank, "device": dev, "bufs": [], "flags": None}
         for ptr in raw:
             h = C.create_string_buffer(64)
@@ -129,7 +134,9 @@ class DistributedDense:
             size = self.eng.buffer(self.rank, 0)[1] // esize
             self._views = [torch.as_tensor(_CudaArray(p, size, self.typestr), device="cuda") for p in raw]
             self._raw = raw
-            self._stream = torch.cuda.ExternalStream(self.eng.stream())
+            ss = C.c_void_p()
+            check(lib.voxl_dense_shared_stream(self.eng._h, C.byref(ss)))
+            self._stream = torch.cuda.ExternalStream(ss.value)
         dist.barrier()
 
     # -- engine facade ----------------------------------------------------------------
@@ -175,12 +182,28 @@ class DistributedDense:
         self.dist.barrier()
 
     def _nccl_exchange(self):
+        """Halo spans of the current buffer, on the shared-layer stream (after
+        this step's shared layers, next to its interior kernel)."""
         import torch
 
         cur = self.eng.buffer(self.rank, 0)[0]
         view = self._views[self._raw.index(cur)]
         with torch.cuda.stream(self._stream):
-            exchange_halos(self.dist, view, self.sends, self.recvs)
+            if self.dist.get_backend() == "nccl":
+                exchange_halos(self.dist, view, self.sends, self.recvs)
+                return
+            # gloo moves host tensors only: stage the spans through host memory
+            self._stream.synchronize()
+            host = {}
+            for peer, base, n in self.sends + self.recvs:
+                host[(base, n)] = view[base:base + n].cpu()
+            ops = [self.dist.P2POp(self.dist.irecv, host[(b, n)], peer) for peer, b, n in self.recvs]
+            ops += [self.dist.P2POp(self.dist.isend, host[(b, n)], peer) for peer, b, n in self.sends]
+            if ops:
+                for w in self.dist.batch_isend_irecv(ops):
+                    w.wait()
+            for peer, base, n in self.recvs:
+                view[base:base + n].copy_(host[(base, n)])
 
     def step(self, n=1):
         if self.halo_mode == "zero_copy":
@@ -199,7 +222,6 @@ class DistributedDense:
         d = self.eng.step_probe()
         if self.halo_mode != "zero_copy":
             self._nccl_exchange()
-            self.eng.synchronize()
         return d
 
     def timed_steps(self, n):

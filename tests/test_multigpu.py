@@ -93,7 +93,7 @@ def test_gloo_span_exchange_fills_halos(world, layout):
     assert all(res.values()), res
 
 
-def _gpu_worker(rank, world, port, result_q):
+def _gpu_worker(rank, world, port, result_q, halo="zero_copy"):
     import torch
     import torch.distributed as dist
 
@@ -104,7 +104,7 @@ def _gpu_worker(rank, world, port, result_q):
     from paper_2503_07898_b200.multigpu import DistributedDense
 
     dom = (24, 20, 32)
-    eng = DistributedDense(domain=dom, precision="fp64", halo_mode="zero_copy")
+    eng = DistributedDense(domain=dom, precision="fp64", halo_mode=halo)
     init = O.port_initial_state("D3Q19", dom)
     k0, k1 = eng.slab()
     s = dom[0] * dom[1] * 19
@@ -122,14 +122,16 @@ def _gpu_worker(rank, world, port, result_q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_zero_copy_multiprocess_bitwise(world):
-    """Ranks share cuda:0 here (the box has one GPU per call); the IPC buffers,
-    peer stores and device step flags are the same code path as on 8 GPUs."""
+@pytest.mark.parametrize("world,halo", [(2, "zero_copy"), (3, "zero_copy"), (2, "copy"), (3, "copy")])
+def test_multiprocess_halo_modes_bitwise(world, halo):
+    """Ranks share cuda:0 here (the box has one GPU per call). zero_copy: the
+    IPC buffers, peer stores and device step flags are the same code path as on
+    8 GPUs. copy: the OCC schedule with the span exchange on the shared-layer
+    stream (NCCL on separate GPUs; gloo through host memory here)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, halo)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
@@ -165,3 +167,45 @@ def test_bench_multirank_path_on_one_gpu():
     e2e = line["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] == 64 ** 3 * 19 * 8 // 10
     assert abs(e2e["final_mass"] - 64 ** 3) < 1e-6 * 64 ** 3
+
+
+def _stall_worker(rank, world, port, result_q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["VOXL_HALO_TIMEOUT_S"] = "2"
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_07898_b200.multigpu import DistributedDense
+
+    eng = DistributedDense(domain=(16, 16, 16), precision="fp32", halo_mode="zero_copy")
+    eng.set_equilibrium(1.0, (0.0, 0.0, 0.0))
+    msg = None
+    if rank == 0:  # rank 1 never steps: rank 0's second step waits for a signal that never comes
+        try:
+            eng.step(3)
+        except Exception as exc:  # noqa: BLE001
+            msg = str(exc)
+    result_q.put((rank, msg))
+    dist.barrier()
+    eng.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_zero_copy_stalled_neighbour_errors_instead_of_hanging():
+    """A neighbour that stops signalling (crashed rank) surfaces as an error
+    after VOXL_HALO_TIMEOUT_S instead of a spin that wedges the GPU."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stall_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[1] is None
+    assert res[0] is not None and "halo exchange stalled at step 1" in res[0], res[0]

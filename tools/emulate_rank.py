@@ -54,7 +54,7 @@ def main():
         from paper_2503_07898_b200.multigpu import _CudaArray
 
         fl = torch.as_tensor(_CudaArray(flags.value, 4, "<i4"), device="cuda")
-        fl.fill_(2 ** 31 - 1)
+        fl[:2].fill_(2 ** 31 - 1)  # word 2 is the stall marker: keep 0
         torch.cuda.synchronize()
         keep = [fl]
         dummy_flags = torch.zeros(8, dtype=torch.int32, device="cuda")

@@ -118,7 +118,7 @@ constexpr int kSplit = E == 8 ? 2 : 1;
 /// SOLID: the level has obstacle cells (a separate instantiation, so grids
 /// without them keep the register budget of the plain kernel).
 template <class L, class R, bool Exact, int E, int MODE, bool SOLID>
-__global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4) ? 6 : 1)
+__global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4) ? block_min_ctas(L::Q) : 1)
     mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W, S = kSplit<E>;
     __shared__ const R* s_src[27];

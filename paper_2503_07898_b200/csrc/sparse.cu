@@ -146,7 +146,7 @@ template <int E>
 constexpr int kSplit = E == 8 ? 2 : 1;
 
 template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
-__global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && sizeof(R) == 4 ? 6 : 1)
+__global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && sizeof(R) == 4 ? block_min_ctas(L::Q) : 1)
     sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
     constexpr int Q = L::Q;
     constexpr int BV = E * E * E;

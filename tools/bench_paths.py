@@ -7,7 +7,7 @@
 
 Prints one JSON line per variant: MLUPS (active voxels for sparse; LUP =
 sum_l N_l * 2^(L-1-l) per coarse step for multires) and the fraction of the
-HBM roofline at 152 B/LUP (fp32 D3Q19), per kernel where the engine exposes
+HBM roofline at 2 Q 4 B/LUP (fp32: 152 B D3Q19, 216 B D3Q27), per kernel where the engine exposes
 per-kernel event times.
 """
 from __future__ import annotations
@@ -20,7 +20,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-BYTES = 152
+
+def bytes_per_lup(lattice):
+    return 2 * (19 if lattice == "D3Q19" else 27) * 4
 
 
 def peak():
@@ -35,14 +37,14 @@ def sparse(args):
     dom = (n, n, n)
     act = V.obstacle_mask(dom)
     for strategy in ("naive", "disag_bitmask", "disag_mem"):
-        e = V.SparseEngine(dom, act, block_edge=8, strategy=strategy, precision="fp32")
+        e = V.SparseEngine(dom, act, block_edge=8, strategy=strategy, precision="fp32", lattice=args.lattice)
         info = e.info()
         e.timed_steps(args.warmup)
         total, b_ms, l_ms = e.timed_steps(args.steps)
         na = info["num_active"]
         mlups = na * args.steps / (total / 1e3) / 1e6
-        gbs = BYTES * na * args.steps / (total / 1e3) / 1e9
-        line = {"path": "block_sparse", "strategy": strategy, "domain": list(dom), "block_edge": 8,
+        gbs = bytes_per_lup(args.lattice) * na * args.steps / (total / 1e3) / 1e9
+        line = {"path": "block_sparse", "lattice": args.lattice, "strategy": strategy, "domain": list(dom), "block_edge": 8,
                 "active_voxels": na, "blocks": info["num_blocks"], "n_boundary": info["n_boundary"],
                 "steps": args.steps, "ms_per_step": round(total / args.steps, 4), "MLUPS": round(mlups, 1),
                 "achieved_GBs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak(), 4),
@@ -64,15 +66,16 @@ def multires(args):
             # configs[4]: flow past an obstacle (solid sphere in the finest band;
             # extension, parity vs the oracle's restatement only)
             lm = obstacle_band_level_map((n, n, n), 3)
-            e = V.MultiResEngine((n, n, n), levels=3, level_map=lm, fused=fused, precision="fp32", solid_cells=True)
+            e = V.MultiResEngine((n, n, n), levels=3, level_map=lm, fused=fused, precision="fp32", solid_cells=True,
+                                 lattice=args.lattice)
         else:
-            e = V.MultiResEngine((n, n, n), levels=3, fused=fused, precision="fp32")
+            e = V.MultiResEngine((n, n, n), levels=3, fused=fused, precision="fp32", lattice=args.lattice)
         lup = e.lup_per_coarse_step()
         e.timed_steps(args.warmup)
         total, detail = e.timed_steps(args.steps)
         mlups = lup * args.steps / (total / 1e3) / 1e6
-        gbs = BYTES * lup * args.steps / (total / 1e3) / 1e9
-        line = {"path": "multires", "scenario": scenario, "levels": 3, "fused": fused, "domain": [n] * 3, "lup_per_coarse_step": lup,
+        gbs = bytes_per_lup(args.lattice) * lup * args.steps / (total / 1e3) / 1e9
+        line = {"path": "multires", "lattice": args.lattice, "scenario": scenario, "levels": 3, "fused": fused, "domain": [n] * 3, "lup_per_coarse_step": lup,
                 "steps": args.steps, "ms_per_coarse_step": round(total / args.steps, 4), "MLUPS": round(mlups, 1),
                 "achieved_GBs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak(), 4),
                 "frac_of_8TBs": round(gbs / 8000, 4), "kernels_ms": detail, "distribution": e.distribution()}
@@ -113,5 +116,6 @@ if __name__ == "__main__":
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--lattice", default="D3Q19", choices=["D3Q19", "D3Q27"], help="sparse / multires lattice")
     a = ap.parse_args()
     {"sparse": sparse, "multires": multires, "dense": dense}[a.path](a)

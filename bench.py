@@ -15,7 +15,10 @@ timed with CUDA events on the engine stream (max over ranks); e2e = the same
 metric through the reference-facing API with host buffers (canonical fp64 state
 uploaded, per-step diagnostics read back, final state downloaded); roofline of
 the step kernel; cpu_baseline = the reference library compiled from
-/root/reference (oracle/_ref) timed on this host.
+/root/reference (oracle/_ref) timed on this host; paths = BASELINE configs[3]
+(block-sparse, disaggregated boundary kernel vs monolithic) and configs[4]
+(3-level multires obstacle flow, fused vs staged) measured in the same run
+(N=1 only; --no-paths skips them).
 """
 from __future__ import annotations
 
@@ -47,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-size", type=int, default=0, help="domain edge of the e2e run (default: --size)")
+    ap.add_argument("--no-paths", action="store_true", help="skip the block-sparse / multires lines (configs[3-4])")
     return ap.parse_args()
 
 
@@ -282,6 +286,11 @@ def main():
         e2e = e2e_run(args, V, np)
     elif not args.no_e2e and world > 1:
         e2e = e2e_run_dist(args, eng, dist, voxels_total, share, np)
+    paths = None
+    if not args.no_paths and world == 1 and rank == 0:
+        eng.close()  # the 20 GB dense state makes room for the other engines
+        eng = None
+        paths = secondary_paths(args, V, peak)
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
         try:
@@ -317,11 +326,55 @@ def main():
             "diag": {"mass": diag.mass, "max_speed": diag.max_speed, "unstable": diag.unstable},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "paths": paths,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def secondary_paths(args, V, peak):
+    """BASELINE configs[3] and configs[4] on the same GPU, same timing rules
+    (CUDA events on the engine stream, warm-up first, states >> L2):
+    block-sparse 512^3 sphere wind tunnel, regularized x-faces, 8^3 blocks,
+    disaggregated boundary kernel (disag_mem) vs monolithic (naive); 3-level
+    multires obstacle flow, fused vs staged. MLUPS count active voxels /
+    LUP = sum_l N_l 2^(L-1-l) per coarse step; 152 B per update."""
+    from paper_2503_07898_b200.multires import obstacle_band_level_map
+
+    n = args.size
+    dom = (n, n, n)
+    out = {}
+    try:
+        act = V.obstacle_mask(dom)
+        for strategy in ("disag_mem", "naive"):
+            e = V.SparseEngine(dom, act, block_edge=8, strategy=strategy, precision="fp32")
+            na = e.info()["num_active"]
+            e.timed_steps(5)
+            ms, _, _ = e.timed_steps(20)
+            e.close()
+            gbs = BYTES_PER_LUP * na * 20 / (ms / 1e3) / 1e9
+            out[f"sparse_{strategy}"] = {"MLUPS": round(na * 20 / (ms / 1e3) / 1e6, 1),
+                                         "frac": round(gbs / peak, 4), "ms_per_step": round(ms / 20, 4),
+                                         "active_voxels": na}
+        lm = obstacle_band_level_map(dom, 3)
+        for fused in (True, False):
+            e = V.MultiResEngine(dom, levels=3, level_map=lm, fused=fused, precision="fp32", solid_cells=True)
+            lup = e.lup_per_coarse_step()
+            e.timed_steps(2)
+            ms, _ = e.timed_steps(5)
+            e.close()
+            gbs = BYTES_PER_LUP * lup * 5 / (ms / 1e3) / 1e9
+            out["multires_obstacle_" + ("fused" if fused else "staged")] = {
+                "MLUPS": round(lup * 5 / (ms / 1e3) / 1e6, 1), "frac": round(gbs / peak, 4),
+                "ms_per_coarse_step": round(ms / 5, 4), "lup_per_coarse_step": lup}
+        out["config"] = (f"configs[3]: D3Q19 block-sparse {n}^3 sphere r={n / 5:g} wind tunnel, 8^3 blocks, fp32, "
+                         f"20 steps; configs[4]: D3Q19 3-level multires {n}^3 band + solid sphere, fp32, 5 coarse "
+                         f"steps; frac = achieved (152 B/update) / MEASURED_PEAKS hbm_gbs")
+    except Exception as exc:  # reported, never fatal for the headline line
+        out["error"] = f"{type(exc).__name__}: {exc}"
+    return out
 
 
 def e2e_run(args, V, np):

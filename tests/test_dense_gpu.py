@@ -157,3 +157,29 @@ def test_canonical_io_multichunk_roundtrip(precision, parts, layout):
     else:
         ww = np.tile(w, np.prod(dom))
         assert np.array_equal(out, (f - ww).astype(np.float32).astype(np.float64) + ww)
+
+
+@pytest.mark.gpu
+def test_bench_line_contract_small():
+    """bench.py at N=1 on a small cube: one JSON line with the contract's keys,
+    the roofline / e2e objects and the configs[3-4] paths."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--size", "64", "--no-cpu"],
+                       capture_output=True, text=True, cwd=root, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "gpu_launches", "e2e", "paths"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["value"] > 0 and d["gpu_launches"] == 5
+    assert d["roofline"]["bound"] == "hbm" and d["roofline"]["achieved"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 64 ** 3 * 19 * 8 // 5
+    p = d["paths"]
+    assert "error" not in p, p
+    for k in ("sparse_disag_mem", "sparse_naive", "multires_obstacle_fused", "multires_obstacle_staged"):
+        assert p[k]["MLUPS"] > 0, k

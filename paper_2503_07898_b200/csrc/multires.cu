@@ -243,46 +243,54 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
 /// explode (multires.cpp:458-467): ghost cells of the fine level <- the
 /// post-collision populations of their parent, a plain copy. One launch fills
 /// both fine post parities in fused mode (one explosion serves both fine
-/// sub-steps, multires.cpp:563-570). Slot -> element offsets use shifts: the
-/// block volume E^3 is a power of two (64-bit division is ~100 instructions).
+/// sub-steps, multires.cpp:563-570). One thread per (population, ghost),
+/// population-major so a warp's stores of one population are contiguous: the
+/// launch is a few MB, so it is latency-bound and wants every load in flight
+/// at once (a thread-per-ghost loop over Q serialises 19 load/store round
+/// trips). Slot -> element offsets use shifts: the block volume E^3 is a power
+/// of two (64-bit division is ~100 instructions).
 template <int Q, class R>
-__global__ void mres_explode_kernel(R* fine_a, R* fine_b, const R* coarse_post, const std::int64_t* dst,
-                                    const std::int64_t* src, int n, int lb) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    const long long bv = 1ll << lb, ds = dst[g], ss = src[g];
-    const long long dbase = ((ds >> lb) * Q << lb) + (ds & (bv - 1));
-    const long long sbase = ((ss >> lb) * Q << lb) + (ss & (bv - 1));
-    for (int c = 0; c < Q; ++c) {
-        const R v = coarse_post[sbase + c * bv];
-        fine_a[dbase + c * bv] = v;
-        if (fine_b) fine_b[dbase + c * bv] = v;
-    }
+__global__ void mres_explode_kernel(R* __restrict__ fine_a, R* __restrict__ fine_b,
+                                    const R* __restrict__ coarse_post, const std::int64_t* __restrict__ dst,
+                                    const std::int64_t* __restrict__ src, int n, int lb) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n * Q) return;
+    const int c = int(t / n), g = int(t - (long long)c * n);
+    const long long bv = 1ll << lb, ds = __ldg(dst + g), ss = __ldg(src + g);
+    const long long dbase = ((ds >> lb) * Q << lb) + (ds & (bv - 1)) + c * bv;
+    const long long sbase = ((ss >> lb) * Q << lb) + (ss & (bv - 1)) + c * bv;
+    const R v = __ldg(coarse_post + sbase);
+    fine_a[dbase] = v;
+    if (fine_b) fine_b[dbase] = v;
 }
 
 /// coalesce (multires.cpp:469-483): ring(l) <- mean of the 8 children's
-/// current (post-stream) populations, children_of order, sum * (1/8).
+/// current (post-stream) populations, children_of order, sum * (1/8). One
+/// thread per (population, ring cell), the children summed in order.
 template <int Q, class R, bool Exact>
-__global__ void mres_coalesce_kernel(R* coarse_post, const R* fine_cur, const std::int64_t* dst,
-                                     const std::int64_t* child, int n, int lbc, int lbf, int nchild) {
+__global__ void mres_coalesce_kernel(R* __restrict__ coarse_post, const R* __restrict__ fine_cur,
+                                     const std::int64_t* __restrict__ dst, const std::int64_t* __restrict__ child,
+                                     int n, int lbc, int lbf, int nchild) {
     using A = Arith<R, Exact>;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    const long long bvc = 1ll << lbc, bvf = 1ll << lbf, ds = dst[g];
-    const long long dbase = ((ds >> lbc) * Q << lbc) + (ds & (bvc - 1));
-    long long cb[8];
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n * Q) return;
+    const int c = int(t / n), g = int(t - (long long)c * n);
+    const long long bvc = 1ll << lbc, bvf = 1ll << lbf, ds = __ldg(dst + g);
+    const long long dbase = ((ds >> lbc) * Q << lbc) + (ds & (bvc - 1)) + c * bvc;
+    R v[8];
+#pragma unroll
     for (int k = 0; k < 8; ++k) {
         if (k < nchild) {
-            const long long cs = child[(long long)g * 8 + k];
-            cb[k] = ((cs >> lbf) * Q << lbf) + (cs & (bvf - 1));
+            const long long cs = __ldg(child + (long long)g * 8 + k);
+            v[k] = __ldg(fine_cur + ((cs >> lbf) * Q << lbf) + (cs & (bvf - 1)) + c * bvf);
         }
     }
     const R scale = R(1.0 / double(nchild));
-    for (int c = 0; c < Q; ++c) {
-        R sum = R(0);
-        for (int k = 0; k < nchild; ++k) sum = A::add(sum, fine_cur[cb[k] + c * bvf]);
-        coarse_post[dbase + c * bvc] = A::mul(sum, scale);
-    }
+    R sum = R(0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < nchild) sum = A::add(sum, v[k]);
+    coarse_post[dbase] = A::mul(sum, scale);
 }
 
 /// probe_field (lbm.cpp:116-138) and total_mass (multires.cpp:600-609) on
@@ -643,6 +651,7 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
     // explosion pairs (ghost at l, parent at l+1) and coalescence records
     // (ring at l, children at l-1), now that every level's slots exist.
     const int dim = grid_.dim();
+    side_transitions_ = cfg_.fused;
     for (int l = 0; l < L; ++l) {
         const MresLevel& G = grid_.level(l);
         const auto& d = G.domain;
@@ -671,6 +680,22 @@ MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_
                         for (; k < 8; ++k) cc.push_back(cc.back());
                     }
                 }
+        // Side-stream transitions (fused mode) rely on two facts of the
+        // classification (multires.cpp:196-247): a ghost's parent has a
+        // refined box neighbour (the parent of the fine cell that pulls from
+        // the ghost), so it is a jump cell of level l + 1; and each ring
+        // cell's 2^dim children share one even-aligned block with a
+        // distance-0 cell, so they lie in a jump block of level l - 1.
+        // Checked here; any exception keeps the transitions on the engine
+        // stream.
+        auto in_jump = [&](const Level* W, std::int64_t slot) {
+            const std::int64_t b = slot >> log2_exact(W->ext.block_volume());
+            return b >= W->n_uni && b < W->n_all;
+        };
+        for (const std::int64_t sl : gs)
+            if (!in_jump(lv_[l + 1], sl)) side_transitions_ = false;
+        for (const std::int64_t sl : cc)
+            if (!in_jump(lv_[l - 1], sl)) side_transitions_ = false;
         Level* V = lv_[l];
         V->n_ghost = int(gd.size());
         V->n_ring = int(cd.size());
@@ -973,13 +998,13 @@ void MultiResEngine::launch_fused(int l) {
     mark_end(kTFused, b);
 }
 
-void MultiResEngine::launch_explode(int coarse) {
+void MultiResEngine::launch_explode(int coarse, cudaStream_t st) {
     Level* F = lv_[coarse - 1];
     Level* Cc = lv_[coarse];
     if (F->n_ghost == 0) return;
     cudaEvent_t b{};
-    mark_begin(kTTransition, &b);
-    const unsigned grid = unsigned((F->n_ghost + 127) / 128);
+    mark_begin(kTTransition, &b, st);
+    const unsigned grid = unsigned(((long long)F->n_ghost * q_ + 255) / 256);
     // One explosion serves both fine sub-steps (multires.cpp:563-570); the
     // fine level flips its post parity between them, so fill both copies.
     void* da = F->post[cfg_.fused ? 0 : F->parity];
@@ -987,45 +1012,60 @@ void MultiResEngine::launch_explode(int coarse) {
     const void* src = Cc->post[Cc->parity];
     const int lb = log2_exact(F->ext.block_volume());
     if (esize_ == 8) {
-        if (q_ == 19) mres_explode_kernel<19, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
-        else mres_explode_kernel<27, double><<<grid, 128, 0, stream_>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        if (q_ == 19) mres_explode_kernel<19, double><<<grid, 256, 0, st>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        else mres_explode_kernel<27, double><<<grid, 256, 0, st>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
     } else {
-        if (q_ == 19) mres_explode_kernel<19, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
-        else mres_explode_kernel<27, float><<<grid, 128, 0, stream_>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        if (q_ == 19) mres_explode_kernel<19, float><<<grid, 256, 0, st>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        else mres_explode_kernel<27, float><<<grid, 256, 0, st>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
     }
     VOXL_CUDA(cudaGetLastError());
-    mark_end(kTTransition, b);
+    mark_end(kTTransition, b, st);
 }
 
-void MultiResEngine::launch_coalesce(int coarse) {
+void MultiResEngine::launch_coalesce(int coarse, cudaStream_t st) {
     Level* F = lv_[coarse - 1];
     Level* Cc = lv_[coarse];
     if (Cc->n_ring == 0) return;
     cudaEvent_t b{};
-    mark_begin(kTTransition, &b);
-    const unsigned grid = unsigned((Cc->n_ring + 127) / 128);
+    mark_begin(kTTransition, &b, st);
+    const unsigned grid = unsigned(((long long)Cc->n_ring * q_ + 255) / 256);
     const int nchild = grid_.dim() == 3 ? 8 : 4;
     const int bvc = log2_exact(Cc->ext.block_volume()), bvf = log2_exact(F->ext.block_volume());
     if (esize_ == 8) {
-        if (q_ == 19) mres_coalesce_kernel<19, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
-        else mres_coalesce_kernel<27, double, true><<<grid, 128, 0, stream_>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        if (q_ == 19) mres_coalesce_kernel<19, double, true><<<grid, 256, 0, st>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        else mres_coalesce_kernel<27, double, true><<<grid, 256, 0, st>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
     } else {
-        if (q_ == 19) mres_coalesce_kernel<19, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
-        else mres_coalesce_kernel<27, float, false><<<grid, 128, 0, stream_>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        if (q_ == 19) mres_coalesce_kernel<19, float, false><<<grid, 256, 0, st>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        else mres_coalesce_kernel<27, float, false><<<grid, 256, 0, st>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
     }
     VOXL_CUDA(cudaGetLastError());
-    mark_end(kTTransition, b);
+    mark_end(kTTransition, b, st);
 }
 
 void MultiResEngine::advance(int l) {
     // advance (multires.cpp:563-567). Fused mode: the jump blocks' collide
     // was done by the previous jump-block stream (or load_uniform_post).
+    // Only jump cells read ghost (exploded) and ring (coalesced) slots, and
+    // only jump cells are ghost parents and ring children (checked at build,
+    // side_transitions_), so in fused mode explosion and coalescence run on
+    // the side stream in order with the jump-block streams, and the long
+    // fused uniform kernels on the engine stream never wait for them.
     if (!cfg_.fused) launch_collide(l, false);
     if (l > 0) {
-        launch_explode(l);
+        if (side_transitions_) {
+            VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
+            VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+        }
+        launch_explode(l, side_transitions_ ? side_ : stream_);
         advance(l - 1);
         advance(l - 1);
-        launch_coalesce(l);
+        if (side_transitions_) {
+            // the fine level's last stream may have run on the engine stream
+            // (a level without uniform or without jump blocks)
+            VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
+            VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+        }
+        launch_coalesce(l, side_transitions_ ? side_ : stream_);
     }
     Level* V = lv_[l];
     if (cfg_.fused && V->n_uni > 0 && V->n_jump > 0) {
@@ -1037,6 +1077,10 @@ void MultiResEngine::advance(int l) {
         VOXL_CUDA(cudaEventRecord(ev_join_, side_));
         VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
     } else {
+        if (side_transitions_) {  // this level's stream may read the side stream's transitions
+            VOXL_CUDA(cudaEventRecord(ev_join_, side_));
+            VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+        }
         if (cfg_.fused) launch_fused(l);
         launch_stream(l, cfg_.fused);
     }

@@ -100,6 +100,7 @@ private:
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* events_ = nullptr;
 
     bool cur_valid_ = true;  // fused mode: uniform cells' cur reconstructed?
+    bool side_transitions_ = false;  // fused mode: explode / coalesce on side_ (see advance)
 
     void advance(int l);
     void gather_uniform(int l);
@@ -108,8 +109,8 @@ private:
     void launch_collide(int l, bool jump_only);
     void launch_stream(int l, bool jump_only, cudaStream_t s = nullptr);
     void launch_fused(int l);
-    void launch_explode(int coarse);
-    void launch_coalesce(int coarse);
+    void launch_explode(int coarse, cudaStream_t st);
+    void launch_coalesce(int coarse, cudaStream_t st);
     void mark_begin(int cls, cudaEvent_t* b, cudaStream_t s = nullptr);
     void mark_end(int cls, cudaEvent_t b, cudaStream_t s = nullptr);
 };

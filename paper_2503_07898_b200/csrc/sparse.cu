@@ -145,8 +145,16 @@ __device__ __forceinline__ bool regularized_dev(int sign, const R (&ubc)[3], R (
 template <int E>
 constexpr int kSplit = E == 8 ? 2 : 1;
 
+// Heavy (regularized) kernel: 4 resident 256-thread CTAs per SM (64
+// registers, no spill for D3Q19) instead of the unconstrained 72 registers /
+// 3 CTAs. Measured at 512^3 disag_mem (tools/gpu_heavy_variants.sh): D3Q19
+// 40.88 -> 41.21 GLUPS, D3Q27 28.01 -> 28.69 (the boundary kernel shares the
+// GPU with the light one, so its occupancy sets how much it slows it).
+#ifndef VOXL_HEAVY_MINB
+#define VOXL_HEAVY_MINB 4
+#endif
 template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
-__global__ void __launch_bounds__(E* E* E / kSplit<E>, MODE == 0 && E == 8 && sizeof(R) == 4 ? block_min_ctas(L::Q) : 1)
+__global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 ? (MODE == 0 ? block_min_ctas(L::Q) : VOXL_HEAVY_MINB) : 1)
     sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
     constexpr int Q = L::Q;
     constexpr int BV = E * E * E;

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--size", type=int, default=512)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--weak", action="store_true", help="configs[2]: size^3 per rank (domain size x size x size*N)")
     a = ap.parse_args()
     import torch
 
@@ -35,7 +36,7 @@ def main():
 
     n = a.size
     dom = (n, n, n)
-    out = {"size": n}
+    out = {"size": n, "scaling": "weak" if a.weak else "strong"}
     # single-GPU reference step
     e1 = V.DenseEngine(domain=dom, precision="fp32")
     e1.set_equilibrium()
@@ -46,7 +47,8 @@ def main():
     torch.cuda.empty_cache()
     for world in [w for w in (2, 4, 8) if w <= a.gpus]:
         r = world // 2 - 1 if world > 2 else 0  # an interior rank when one exists
-        eng = V.DenseEngine(domain=dom, precision="fp32", partitions=world, first_partition=r, local_partitions=1)
+        wdom = (n, n, n * world) if a.weak else dom
+        eng = V.DenseEngine(domain=wdom, precision="fp32", partitions=world, first_partition=r, local_partitions=1)
         flags = C.c_void_p()
         check(lib.voxl_dense_enable_distributed(eng._h, C.byref(flags)))
         # release every wait: flags[0] = flags[1] = 2^31
@@ -73,9 +75,14 @@ def main():
         eng.timed_steps(a.warmup)
         tr, _ = eng.timed_steps(a.steps)
         tr /= a.steps
-        out[f"rank{r}_of_{world}"] = {"t_rank_ms": round(tr, 4),
-                                      "efficiency_bound": round(out["t_1gpu_ms"] / (world * tr), 4),
-                                      "MLUPS_job_bound": round(n ** 3 / (tr / 1e3) / 1e6, 1)}
+        if a.weak:  # per-rank work fixed: efficiency = t_1 / t_N
+            out[f"rank{r}_of_{world}"] = {"t_rank_ms": round(tr, 4),
+                                          "efficiency_bound": round(out["t_1gpu_ms"] / tr, 4),
+                                          "MLUPS_job_bound": round(world * n ** 3 / (tr / 1e3) / 1e6, 1)}
+        else:
+            out[f"rank{r}_of_{world}"] = {"t_rank_ms": round(tr, 4),
+                                          "efficiency_bound": round(out["t_1gpu_ms"] / (world * tr), 4),
+                                          "MLUPS_job_bound": round(n ** 3 / (tr / 1e3) / 1e6, 1)}
         eng.close()
         del keep
         torch.cuda.empty_cache()

@@ -7,7 +7,7 @@ T=${1:-r1}
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_$T.txt 2>&1
 timeout 900 python bench.py --steps 500 --warmup 50 > gpurun_out/bench500_$T.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 3 -c 30 --csv --log-file gpurun_out/launches_$T.csv python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 3 -c 30 --csv --log-file gpurun_out/launches_$T.csv python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --no-paths > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_step -s 3 -c 1 -o gpurun_out/dense_full_$T python tools/prof_dense.py 512 5 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:dense_step -s 3 -c 2 -o gpurun_out/probe_full_$T python tools/prof_probe.py 512 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_step -s 3 -c 2 -o gpurun_out/sparse_full_$T python tools/bench_paths.py sparse --n 512 --steps 1 --warmup 0 > /dev/null 2>&1

@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""Small runs of every engine kernel family for compute-sanitizer
+(memcheck / racecheck / synccheck): dense (3 layouts, 3 partitions, both halo
+modes, D3Q27, fp32/fp64, fused probe), block-sparse (3 strategies, edge 4/8,
+step_probe), multires (fused/staged, obstacle), canonical I/O both ways.
+
+    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+import paper_2503_07898_b200 as V
+from paper_2503_07898_b200.multires import obstacle_band_level_map
+
+for lat in ("D3Q19", "D3Q27"):
+    for prec in ("fp32", "fp64"):
+        for layout in ("DisagSoA", "SoA", "AoS"):
+            for halo in ("zero_copy", "copy"):
+                e = V.DenseEngine(lattice=lat, domain=(20, 12, 18), precision=prec, layout=layout, partitions=3,
+                                  halo_mode=halo)
+                e.set_equilibrium()
+                e.step(3)
+                e.step_probe()
+                st = e.get_canonical()
+                e.set_canonical(st)
+                e.probe()
+                e.close()
+for lat in ("D3Q19", "D3Q27"):
+    for prec in ("fp32", "fp64"):
+        for edge in (4, 8):
+            for strategy in ("naive", "disag_bitmask", "disag_mem"):
+                s = V.SparseEngine((40, 24, 24), block_edge=edge, strategy=strategy, precision=prec, lattice=lat)
+                s.step(2)
+                s.step_probe()
+                st = s.get_state()
+                s.set_state(st)
+                s.probe()
+                s.close()
+dom = (32, 32, 32)
+for prec in ("fp32", "fp64"):
+    for fused in (True, False):
+        m = V.MultiResEngine(dom, 3, fused=fused, precision=prec)
+        m.step(2)
+        st = m.get_state()
+        m.set_state(st)
+        m.step(1)
+        m.probe()
+        m.close()
+        m = V.MultiResEngine(dom, 3, level_map=obstacle_band_level_map(dom, 3), fused=fused, precision=prec,
+                             solid_cells=True)
+        m.step(2)
+        m.close()
+print("sanitize run ok")

@@ -212,8 +212,10 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
             }
             const R* p = oob ? own_src + oi * BV : s_src[d] + (i * BV + sl);
             R v = __ldg(p);
-            if constexpr (ez < 0) {
-                if (A.has_lid && dzhi) v = Ar::add(v, A.lid[i]);
+            // lid on the max face of the partition axis (rules_for,
+            // solver.cpp:150-163): z in 3D, y in 2D
+            if constexpr ((L::dim == 3 ? ez : ey) < 0) {
+                if (A.has_lid && (L::dim == 3 ? dzhi : dyhi)) v = Ar::add(v, A.lid[i]);
             }
             g[i] = v;
         }
@@ -394,9 +396,22 @@ void mres_dispatch(int lattice, Precision prec, int edge, F&& f) {
         else by_edge(lat, float{}, std::false_type{});
     };
     switch (lattice) {
+        case kD2Q9: by_prec(D2Q9{}); break;  // nz = 1: the z = 0 layer of E^3 blocks
         case kD3Q19: by_prec(D3Q19{}); break;
         case kD3Q27: by_prec(D3Q27{}); break;
-        default: throw std::invalid_argument("multires engine: D3Q19 or D3Q27 (3D cavity)");
+        default: throw std::invalid_argument("multires engine: unknown lattice");
+    }
+}
+
+/// Population count as a compile-time constant for the Q-templated helpers
+/// (canonical I/O, transitions): D2Q9, D3Q19, D3Q27.
+template <class F>
+void q_dispatch(int q, F&& f) {
+    switch (q) {
+        case 9: f(std::integral_constant<int, 9>{}); break;
+        case 19: f(std::integral_constant<int, 19>{}); break;
+        case 27: f(std::integral_constant<int, 27>{}); break;
+        default: throw std::invalid_argument("multires engine: unsupported population count");
     }
 }
 
@@ -467,8 +482,8 @@ struct MultiResEngine::Level {
 
 MultiResEngine::MultiResEngine(const MresConfig& cfg, const std::int32_t* level_map)
     : cfg_(cfg), io_(std::make_unique<CanonPipe>()) {
-    if (cfg_.lattice != kD3Q19 && cfg_.lattice != kD3Q27)
-        throw std::invalid_argument("multires engine: D3Q19 or D3Q27 (3D cavity)");
+    if (cfg_.lattice != kD2Q9 && cfg_.lattice != kD3Q19 && cfg_.lattice != kD3Q27)
+        throw std::invalid_argument("multires engine: unknown lattice");
     if (cfg_.edge != 4 && cfg_.edge != 8) throw std::invalid_argument("multires engine: block edge must be 4 or 8");
     const LatticeTable lat = make_lattice(cfg_.lattice);
     q_ = lat.q;
@@ -821,11 +836,15 @@ void MultiResEngine::transfer(double* host, bool to_device, unsigned long long* 
         const int bv = V->ext.block_volume();
         auto layout = [&](long long r0, long long r1, void* slot, bool w32) {
             if (esize_ == 8) {
-                if (q_ == 19) launch_slot_io<19, double>(static_cast<double*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
-                else launch_slot_io<27, double>(static_cast<double*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
+                q_dispatch(q_, [&](auto QC) {
+                    launch_slot_io<decltype(QC)::value, double>(static_cast<double*>(V->cur), slot, w32, V->slots + r0,
+                                                                 r1 - r0, bv, shift, to_device, stream_);
+                });
             } else {
-                if (q_ == 19) launch_slot_io<19, float>(static_cast<float*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
-                else launch_slot_io<27, float>(static_cast<float*>(V->cur), slot, w32, V->slots + r0, r1 - r0, bv, shift, to_device, stream_);
+                q_dispatch(q_, [&](auto QC) {
+                    launch_slot_io<decltype(QC)::value, float>(static_cast<float*>(V->cur), slot, w32, V->slots + r0,
+                                                                r1 - r0, bv, shift, to_device, stream_);
+                });
             }
         };
         auto consume = [&](long long r0, long long r1, void* slot) {
@@ -1012,11 +1031,17 @@ void MultiResEngine::launch_explode(int coarse, cudaStream_t st) {
     const void* src = Cc->post[Cc->parity];
     const int lb = log2_exact(F->ext.block_volume());
     if (esize_ == 8) {
-        if (q_ == 19) mres_explode_kernel<19, double><<<grid, 256, 0, st>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
-        else mres_explode_kernel<27, double><<<grid, 256, 0, st>>>(static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        q_dispatch(q_, [&](auto QC) {
+            mres_explode_kernel<decltype(QC)::value, double><<<grid, 256, 0, st>>>(
+                static_cast<double*>(da), static_cast<double*>(db), static_cast<const double*>(src), F->explode_dst,
+                F->explode_src, F->n_ghost, lb);
+        });
     } else {
-        if (q_ == 19) mres_explode_kernel<19, float><<<grid, 256, 0, st>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
-        else mres_explode_kernel<27, float><<<grid, 256, 0, st>>>(static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst, F->explode_src, F->n_ghost, lb);
+        q_dispatch(q_, [&](auto QC) {
+            mres_explode_kernel<decltype(QC)::value, float><<<grid, 256, 0, st>>>(
+                static_cast<float*>(da), static_cast<float*>(db), static_cast<const float*>(src), F->explode_dst,
+                F->explode_src, F->n_ghost, lb);
+        });
     }
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTTransition, b, st);
@@ -1032,11 +1057,17 @@ void MultiResEngine::launch_coalesce(int coarse, cudaStream_t st) {
     const int nchild = grid_.dim() == 3 ? 8 : 4;
     const int bvc = log2_exact(Cc->ext.block_volume()), bvf = log2_exact(F->ext.block_volume());
     if (esize_ == 8) {
-        if (q_ == 19) mres_coalesce_kernel<19, double, true><<<grid, 256, 0, st>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
-        else mres_coalesce_kernel<27, double, true><<<grid, 256, 0, st>>>(static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        q_dispatch(q_, [&](auto QC) {
+            mres_coalesce_kernel<decltype(QC)::value, double, true><<<grid, 256, 0, st>>>(
+                static_cast<double*>(Cc->post[Cc->parity]), static_cast<const double*>(F->cur), Cc->coal_dst,
+                Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        });
     } else {
-        if (q_ == 19) mres_coalesce_kernel<19, float, false><<<grid, 256, 0, st>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
-        else mres_coalesce_kernel<27, float, false><<<grid, 256, 0, st>>>(static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst, Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        q_dispatch(q_, [&](auto QC) {
+            mres_coalesce_kernel<decltype(QC)::value, float, false><<<grid, 256, 0, st>>>(
+                static_cast<float*>(Cc->post[Cc->parity]), static_cast<const float*>(F->cur), Cc->coal_dst,
+                Cc->coal_child, Cc->n_ring, bvc, bvf, nchild);
+        });
     }
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTTransition, b, st);

@@ -303,3 +303,53 @@ def test_state_io_multichunk_roundtrip(precision):
     d = e.probe()
     assert abs(d.mass - math.fsum(exp.tolist())) <= 1e-12 * d.mass
     e.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("edge", [4, 8])
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("levels,domain", [(2, (16, 16, 1)), (3, (32, 48, 1))])
+def test_2d_multires_bitwise_vs_oracle(edge, fused, levels, domain):
+    """D2Q9 multires (4 children per cell, lid on the y = max face; run_multires
+    with lattice D2Q9, solver.cpp:312-367): fp64 bitwise vs the oracle, fused and
+    staged, on the z = 0 layer of the E^3 blocks."""
+    lm = V.band_level_map(domain, levels, axis=1)
+    ref = O.port_mres_run("D2Q9", domain, levels, 0.6, (0.05, 0.0, 0.0), 3, level_map=lm)
+    e = V.MultiResEngine(domain, levels, level_map=lm, tau=0.6, fused=fused, precision="fp64", block_edge=edge,
+                         lattice="D2Q9")
+    e.step(3)
+    assert np.array_equal(e.get_state(), ref)
+    e.close()
+
+
+@pytest.mark.gpu
+def test_2d_multires_reference_fused_equals_staged():
+    """multires_test.cpp:494-530: 16x16 D2Q9, fine upper half, tau 0.7, lid u =
+    (0.05, 0) on y = max: fused == staged after 5 coarse steps (and both equal
+    the oracle)."""
+    dom = (16, 16, 1)
+    lm = np.ones(16 * 16, np.int32)
+    lm.reshape(16, 16)[8:, :] = 0
+    out = []
+    for fused in (False, True):
+        e = V.MultiResEngine(dom, 2, level_map=lm, tau=0.7, fused=fused, precision="fp64", lattice="D2Q9")
+        e.step(5)
+        out.append(e.get_state())
+        e.close()
+    assert np.array_equal(out[0], out[1])
+    ref = O.port_mres_run("D2Q9", dom, 2, 0.7, (0.05, 0.0, 0.0), 5, level_map=lm)
+    assert np.array_equal(out[1], ref)
+
+
+@pytest.mark.gpu
+def test_2d_multires_fp32_tolerance():
+    dom = (64, 64, 1)
+    lm = V.band_level_map(dom, 3, axis=1)
+    st = []
+    for prec in ("fp64", "fp32"):
+        e = V.MultiResEngine(dom, 3, level_map=lm, tau=0.6, fused=True, precision=prec, lattice="D2Q9")
+        e.step(250)
+        st.append(e.get_state())
+        e.close()
+    rel = np.abs(st[1] - st[0]) / np.abs(st[0])
+    assert rel.max() <= 1e-5, rel.max()

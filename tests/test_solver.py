@@ -118,6 +118,10 @@ CASES = {
                    velocity=[0.04, 0, 0], steps=8, strategy="disag_bitmask"),
     "multires": dict(lattice="D3Q19", domain=[16, 16, 16], tau=0.56, scenario="lid_driven_cavity",
                      velocity=[0.05, 0, 0], steps=3, levels=2, fused=True),
+    "multires_2d": dict(lattice="D2Q9", domain=[32, 32], tau=0.6, scenario="lid_driven_cavity",
+                        velocity=[0.05, 0, 0], steps=4, levels=3, fused=True),
+    "multires_2d_staged": dict(lattice="D2Q9", domain=[48, 32], tau=0.6, scenario="lid_driven_cavity",
+                               velocity=[0.05, 0, 0], steps=3, levels=2, fused=False),
 }
 
 

@@ -53,4 +53,13 @@ for prec in ("fp32", "fp64"):
                              solid_cells=True)
         m.step(2)
         m.close()
+for fused in (True, False):  # D2Q9 multires: z = 0 layer of the E^3 blocks
+    for edge in (4, 8):
+        d2 = (32, 48, 1)
+        m = V.MultiResEngine(d2, 3, level_map=V.band_level_map(d2, 3, axis=1), tau=0.6, fused=fused, precision="fp32",
+                             block_edge=edge, lattice="D2Q9")
+        m.step(2)
+        m.set_state(m.get_state())
+        m.probe()
+        m.close()
 print("sanitize run ok")

@@ -11,7 +11,10 @@
  *
  * Errors: every call returns VOXL_OK (0) or a status; voxl_last_error() gives
  * the message of the calling thread's last failure, with the reference's
- * message text (e.g. "run aborted at step N: ...").
+ * message text (e.g. "run aborted at step N: ..."). A null handle or a null
+ * state / output buffer is VOXL_INVALID_ARGUMENT ("<entry point>: null argument").
+ * Canonical buffers are sized by the engine (voxels * q, state_len); the
+ * caller owns them and the callee copies (no pointer is retained).
  */
 #ifndef VOXL_B200_H
 #define VOXL_B200_H

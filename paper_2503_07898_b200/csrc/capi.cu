@@ -62,6 +62,13 @@ void require(bool c, const char* msg) {
     if (!c) throw std::invalid_argument(msg);
 }
 
+/// Null handle / pointer arguments of an entry point -> VOXL_INVALID_ARGUMENT.
+template <class... P>
+void need(const char* fn, const P*... p) {
+    const bool ok = ((p != nullptr) && ...);
+    if (!ok) throw std::invalid_argument(std::string(fn) + ": null argument");
+}
+
 } // namespace
 
 extern "C" {
@@ -194,19 +201,29 @@ int voxl_dense_destroy(voxl_dense* h) {
 }
 
 int voxl_dense_set_canonical(voxl_dense* h, const double* host) {
-    return guarded([&] { h->eng->set_canonical(host); });
+    return guarded([&] {
+        need("voxl_dense_set_canonical", h, host);
+        h->eng->set_canonical(host);
+    });
 }
 
 int voxl_dense_set_equilibrium(voxl_dense* h, double rho, const double* u) {
-    return guarded([&] { h->eng->set_equilibrium(rho, u); });
+    return guarded([&] {
+        need("voxl_dense_set_equilibrium", h, u);
+        h->eng->set_equilibrium(rho, u);
+    });
 }
 
 int voxl_dense_get_canonical(voxl_dense* h, double* host) {
-    return guarded([&] { h->eng->get_canonical(host); });
+    return guarded([&] {
+        need("voxl_dense_get_canonical", h, host);
+        h->eng->get_canonical(host);
+    });
 }
 
 int voxl_dense_digest(voxl_dense* h, uint64_t* out2) {
     return guarded([&] {
+        need("voxl_dense_digest", h, out2);
         unsigned long long d[2];
         h->eng->digest(d);
         out2[0] = d[0];
@@ -215,31 +232,50 @@ int voxl_dense_digest(voxl_dense* h, uint64_t* out2) {
 }
 
 int voxl_dense_set_planes(voxl_dense* h, const double* host, int k0, int k1) {
-    return guarded([&] { h->eng->set_canonical_planes(host, k0, k1); });
+    return guarded([&] {
+        need("voxl_dense_set_planes", h, host);
+        h->eng->set_canonical_planes(host, k0, k1);
+    });
 }
 
 int voxl_dense_get_planes(voxl_dense* h, double* host, int k0, int k1) {
-    return guarded([&] { h->eng->get_canonical_planes(host, k0, k1); });
+    return guarded([&] {
+        need("voxl_dense_get_planes", h, host);
+        h->eng->get_canonical_planes(host, k0, k1);
+    });
 }
 
 int voxl_dense_step(voxl_dense* h, int n) {
-    return guarded([&] { h->eng->step(n); });
+    return guarded([&] {
+        need("voxl_dense_step", h);
+        h->eng->step(n);
+    });
 }
 
 int voxl_dense_enqueue(voxl_dense* h, int n) {
-    return guarded([&] { h->eng->enqueue_steps(n); });
+    return guarded([&] {
+        need("voxl_dense_enqueue", h);
+        h->eng->enqueue_steps(n);
+    });
 }
 
 int voxl_dense_timed_steps(voxl_dense* h, int n, double* total_ms, double* kernel_ms) {
-    return guarded([&] { *total_ms = h->eng->timed_steps(n, kernel_ms); });
+    return guarded([&] {
+        need("voxl_dense_timed_steps", h, total_ms);
+        *total_ms = h->eng->timed_steps(n, kernel_ms);
+    });
 }
 
 int voxl_dense_synchronize(voxl_dense* h) {
-    return guarded([&] { h->eng->check_errors(); });
+    return guarded([&] {
+        need("voxl_dense_synchronize", h);
+        h->eng->check_errors();
+    });
 }
 
 int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out) {
     return guarded([&] {
+        need("voxl_dense_step_probe", h, out);
         const DenseDiag d = h->eng->step_probe();
         out->mass = d.mass;
         out->max_speed = d.max_speed;
@@ -251,6 +287,7 @@ int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out) {
 
 int voxl_dense_probe(voxl_dense* h, voxl_diag* out) {
     return guarded([&] {
+        need("voxl_dense_probe", h, out);
         const DenseDiag d = h->eng->probe();
         out->mass = d.mass;
         out->max_speed = d.max_speed;
@@ -262,6 +299,7 @@ int voxl_dense_probe(voxl_dense* h, voxl_diag* out) {
 
 int voxl_dense_ledger(voxl_dense* h, int step, voxl_transfer_record* out, int cap, int* count) {
     return guarded([&] {
+        need("voxl_dense_ledger", h);
         const auto recs = h->eng->ledger_records(step);
         if (count) *count = int(recs.size());
         for (int i = 0; i < int(recs.size()) && i < cap; ++i)
@@ -292,17 +330,22 @@ int voxl_dense_plan_ledger(const voxl_dense_desc* desc, int step, voxl_transfer_
 
 int voxl_dense_layout_json(voxl_dense* h, int p, char* out, int64_t cap, int64_t* len) {
     return guarded([&] {
+        need("voxl_dense_layout_json", h);
         require(p >= 0 && p < h->eng->config().partitions, "bad partition");
         put_text(h->eng->layout(p).to_json(), out, cap, len);
     });
 }
 
 int voxl_dense_steps_done(voxl_dense* h, int* steps) {
-    return guarded([&] { *steps = h->eng->steps_done(); });
+    return guarded([&] {
+        need("voxl_dense_steps_done", h);
+        *steps = h->eng->steps_done();
+    });
 }
 
 int voxl_dense_buffer(voxl_dense* h, int p, int which, void** ptr, size_t* bytes) {
     return guarded([&] {
+        need("voxl_dense_buffer", h);
         require(p >= 0 && p < h->eng->config().partitions, "bad partition");
         *ptr = h->eng->buffer(p, which);
         if (bytes) *bytes = h->eng->buffer_bytes(p);
@@ -310,22 +353,30 @@ int voxl_dense_buffer(voxl_dense* h, int p, int which, void** ptr, size_t* bytes
 }
 
 int voxl_dense_stream(voxl_dense* h, void** stream) {
-    return guarded([&] { *stream = (void*)h->eng->stream(); });
+    return guarded([&] {
+        need("voxl_dense_stream", h);
+        *stream = (void*)h->eng->stream();
+    });
 }
 
 int voxl_dense_shared_stream(voxl_dense* h, void** stream) {
     return guarded([&] {
+        need("voxl_dense_shared_stream", h);
         require(h->eng->shared_stream() != nullptr, "shared_stream: call voxl_dense_enable_distributed first");
         *stream = (void*)h->eng->shared_stream();
     });
 }
 
 int voxl_dense_attach_peer(voxl_dense* h, int p, void* b0, void* b1) {
-    return guarded([&] { h->eng->attach_peer(p, b0, b1); });
+    return guarded([&] {
+        need("voxl_dense_attach_peer", h);
+        h->eng->attach_peer(p, b0, b1);
+    });
 }
 
 int voxl_dense_raw_buffer(voxl_dense* h, int p, int w, void** ptr) {
     return guarded([&] {
+        need("voxl_dense_raw_buffer", h);
         require(p >= 0 && p < h->eng->config().partitions && (w == 0 || w == 1), "bad partition/buffer");
         *ptr = h->eng->raw_buffer(p, w);
     });
@@ -333,6 +384,7 @@ int voxl_dense_raw_buffer(voxl_dense* h, int p, int w, void** ptr) {
 
 int voxl_dense_enable_distributed(voxl_dense* h, void** flags) {
     return guarded([&] {
+        need("voxl_dense_enable_distributed", h);
         h->eng->enable_distributed();
         if (flags) *flags = h->eng->flag_words();
     });
@@ -340,16 +392,23 @@ int voxl_dense_enable_distributed(voxl_dense* h, void** flags) {
 
 int voxl_dense_attach_flags(voxl_dense* h, void* upper_slot, void* lower_slot) {
     return guarded([&] {
+        need("voxl_dense_attach_flags", h);
         h->eng->attach_flags(static_cast<std::uint32_t*>(upper_slot), static_cast<std::uint32_t*>(lower_slot));
     });
 }
 
 int voxl_dense_halo_push(voxl_dense* h) {
-    return guarded([&] { h->eng->halo_push(); });
+    return guarded([&] {
+        need("voxl_dense_halo_push", h);
+        h->eng->halo_push();
+    });
 }
 
 int voxl_dense_owned_voxels(voxl_dense* h, int64_t* voxels) {
-    return guarded([&] { *voxels = h->eng->owned_voxels(); });
+    return guarded([&] {
+        need("voxl_dense_owned_voxels", h, voxels);
+        *voxels = h->eng->owned_voxels();
+    });
 }
 
 int voxl_obstacle_mask(int nx, int ny, int nz, double radius, uint8_t* out, int64_t* active) {
@@ -411,7 +470,10 @@ int voxl_sparse_plan_destroy(voxl_sparse_plan* p) {
 }
 
 int voxl_sparse_plan_of(voxl_sparse* h, voxl_sparse_plan** out) {
-    return guarded([&] { *out = reinterpret_cast<voxl_sparse_plan*>(&SP(h)->tables()); });
+    return guarded([&] {
+        need("voxl_sparse_plan_of", h);
+        *out = reinterpret_cast<voxl_sparse_plan*>(&SP(h)->tables());
+    });
 }
 
 int voxl_sparse_plan_info(voxl_sparse_plan* p, int64_t* na, int* nb, int64_t* nbd, int64_t* nnb) {
@@ -477,11 +539,15 @@ int voxl_sparse_report_json(voxl_sparse* h, char* out, int64_t cap, int64_t* len
 }
 
 int voxl_sparse_get_state(voxl_sparse* h, double* canonical) {
-    return guarded([&] { SP(h)->get_state(canonical); });
+    return guarded([&] {
+        need("voxl_sparse_get_state", h, canonical);
+        SP(h)->get_state(canonical);
+    });
 }
 
 int voxl_sparse_digest(voxl_sparse* h, uint64_t* out2) {
     return guarded([&] {
+        need("voxl_sparse_digest", h, out2);
         unsigned long long d[2];
         SP(h)->digest(d);
         out2[0] = d[0];
@@ -490,30 +556,44 @@ int voxl_sparse_digest(voxl_sparse* h, uint64_t* out2) {
 }
 
 int voxl_sparse_set_state(voxl_sparse* h, const double* canonical) {
-    return guarded([&] { SP(h)->set_state(canonical); });
+    return guarded([&] {
+        need("voxl_sparse_set_state", h, canonical);
+        SP(h)->set_state(canonical);
+    });
 }
 
 int voxl_sparse_set_equilibrium(voxl_sparse* h, double rho, const double* u) {
-    return guarded([&] { SP(h)->set_equilibrium(rho, u); });
+    return guarded([&] {
+        need("voxl_sparse_set_equilibrium", h, u);
+        SP(h)->set_equilibrium(rho, u);
+    });
 }
 
 int voxl_sparse_step(voxl_sparse* h, int n) {
-    return guarded([&] { SP(h)->step(n); });
+    return guarded([&] {
+        need("voxl_sparse_step", h);
+        SP(h)->step(n);
+    });
 }
 
 int voxl_sparse_step_identity(voxl_sparse* h, int n) {
     return guarded([&] {
+        need("voxl_sparse_step_identity", h);
         require(n >= 0, "step_identity: n must be >= 0");
         SP(h)->step_identity(n);
     });
 }
 
 int voxl_sparse_timed_steps(voxl_sparse* h, int n, double* total, double* bms, double* lms) {
-    return guarded([&] { *total = SP(h)->timed_steps(n, bms, lms); });
+    return guarded([&] {
+        need("voxl_sparse_timed_steps", h, total);
+        *total = SP(h)->timed_steps(n, bms, lms);
+    });
 }
 
 int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out) {
     return guarded([&] {
+        need("voxl_sparse_probe", h, out);
         const DenseDiag d = SP(h)->probe();
         out->mass = d.mass;
         out->max_speed = d.max_speed;
@@ -525,6 +605,7 @@ int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out) {
 
 int voxl_sparse_step_probe(voxl_sparse* h, voxl_diag* out) {
     return guarded([&] {
+        need("voxl_sparse_step_probe", h, out);
         const DenseDiag d = SP(h)->step_probe();
         out->mass = d.mass;
         out->max_speed = d.max_speed;
@@ -631,11 +712,15 @@ int voxl_mres_destroy(voxl_mres* h) {
 }
 
 int voxl_mres_step(voxl_mres* h, int n) {
-    return guarded([&] { MR(h)->coarse_step(n); });
+    return guarded([&] {
+        need("voxl_mres_step", h);
+        MR(h)->coarse_step(n);
+    });
 }
 
 int voxl_mres_timed_steps(voxl_mres* h, int n, double* o) {
     return guarded([&] {
+        need("voxl_mres_timed_steps", h, o);
         const MresTimes t = MR(h)->timed_steps(n);
         o[0] = t.total;
         o[1] = t.collide;
@@ -646,15 +731,22 @@ int voxl_mres_timed_steps(voxl_mres* h, int n, double* o) {
 }
 
 int voxl_mres_state_len(voxl_mres* h, int64_t* len) {
-    return guarded([&] { *len = MR(h)->state_len(); });
+    return guarded([&] {
+        need("voxl_mres_state_len", h, len);
+        *len = MR(h)->state_len();
+    });
 }
 
 int voxl_mres_get_state(voxl_mres* h, double* c) {
-    return guarded([&] { MR(h)->get_state(c); });
+    return guarded([&] {
+        need("voxl_mres_get_state", h, c);
+        MR(h)->get_state(c);
+    });
 }
 
 int voxl_mres_digest(voxl_mres* h, uint64_t* out2) {
     return guarded([&] {
+        need("voxl_mres_digest", h, out2);
         unsigned long long d[2];
         MR(h)->digest(d);
         out2[0] = d[0];
@@ -663,15 +755,22 @@ int voxl_mres_digest(voxl_mres* h, uint64_t* out2) {
 }
 
 int voxl_mres_set_state(voxl_mres* h, const double* c) {
-    return guarded([&] { MR(h)->set_state(c); });
+    return guarded([&] {
+        need("voxl_mres_set_state", h, c);
+        MR(h)->set_state(c);
+    });
 }
 
 int voxl_mres_set_equilibrium(voxl_mres* h, double rho, const double* u) {
-    return guarded([&] { MR(h)->set_equilibrium(rho, u); });
+    return guarded([&] {
+        need("voxl_mres_set_equilibrium", h, u);
+        MR(h)->set_equilibrium(rho, u);
+    });
 }
 
 int voxl_mres_probe(voxl_mres* h, voxl_diag* out) {
     return guarded([&] {
+        need("voxl_mres_probe", h, out);
         const DenseDiag d = MR(h)->probe();
         out->mass = d.mass;
         out->max_speed = d.max_speed;
@@ -682,17 +781,22 @@ int voxl_mres_probe(voxl_mres* h, voxl_diag* out) {
 }
 
 int voxl_mres_total_mass(voxl_mres* h, double* m) {
-    return guarded([&] { *m = MR(h)->total_mass(); });
+    return guarded([&] {
+        need("voxl_mres_total_mass", h, m);
+        *m = MR(h)->total_mass();
+    });
 }
 
 int voxl_mres_text(voxl_mres* h, int what, char* out, int64_t cap, int64_t* len) {
     return guarded([&] {
+        need("voxl_mres_text", h);
         put_text(what == 0 ? MR(h)->graph_dot() : MR(h)->grid().distribution_report(), out, cap, len);
     });
 }
 
 int voxl_mres_level_info(voxl_mres* h, int l, int64_t* na, double* tau, int64_t* uni, int64_t* jmp) {
     return guarded([&] {
+        need("voxl_mres_level_info", h);
         require(l >= 0 && l < MR(h)->grid().num_levels(), "bad level");
         if (na) *na = MR(h)->grid().level(l).num_active;
         if (tau) *tau = MR(h)->grid().level(l).tau;
@@ -703,7 +807,10 @@ int voxl_mres_level_info(voxl_mres* h, int l, int64_t* na, double* tau, int64_t*
 }
 
 int voxl_mres_lup_per_coarse_step(voxl_mres* h, int64_t* lup) {
-    return guarded([&] { *lup = MR(h)->grid().lup_per_coarse_step(); });
+    return guarded([&] {
+        need("voxl_mres_lup_per_coarse_step", h, lup);
+        *lup = MR(h)->grid().lup_per_coarse_step();
+    });
 }
 
 int voxl_mres_plan_create(const voxl_mres_desc* d, const int32_t* map, voxl_mres_plan** out) {

@@ -160,6 +160,8 @@ class DenseEngine:
     def get_canonical(self, out: np.ndarray | None = None) -> np.ndarray:
         if out is None:
             out = np.empty(self.voxels * self.q, np.float64)
+        elif out.dtype != np.float64 or out.size != self.voxels * self.q or not out.flags.c_contiguous:
+            raise ValueError("to_canonical: out must be a contiguous float64 array of voxels * q elements")
         check(lib.voxl_dense_get_canonical(self._h, out.ctypes.data))
         return out
 

@@ -164,6 +164,8 @@ class MultiResEngine:
 
     def set_state(self, canonical):
         v = np.ascontiguousarray(canonical, np.float64)
+        if v.size != self.state_len():
+            raise ValueError("set_state: size mismatch")
         check(lib.voxl_mres_set_state(self._h, v.ctypes.data))
 
     def set_equilibrium(self, rho=1.0, u=(0.0, 0.0, 0.0)):

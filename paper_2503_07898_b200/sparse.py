@@ -166,6 +166,8 @@ class SparseEngine:
 
     def set_state(self, canonical) -> None:
         v = np.ascontiguousarray(canonical, np.float64)
+        if v.size != self.num_active * self.q:
+            raise ValueError("set_state: size mismatch")
         check(lib.voxl_sparse_set_state(self._h, v.ctypes.data))
 
     def set_equilibrium(self, rho=1.0, u=(0.0, 0.0, 0.0)):

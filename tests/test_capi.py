@@ -41,6 +41,22 @@ def test_error_status_and_message():
         V.lattice_json(7)
 
 
+def test_null_handles_and_buffers_are_invalid_arguments():
+    """No CPU-side crash on a null handle or buffer: every handle entry point
+    returns VOXL_INVALID_ARGUMENT with the entry point's name (no GPU touched)."""
+    import ctypes as C
+
+    from paper_2503_07898_b200._capi import INVALID_ARGUMENT, lib
+
+    for fn, args in [("voxl_dense_step", (None, 1)), ("voxl_dense_set_canonical", (None, None)),
+                     ("voxl_dense_get_canonical", (None, None)), ("voxl_sparse_step", (None, 1)),
+                     ("voxl_sparse_get_state", (None, None)), ("voxl_mres_step", (None, 1)),
+                     ("voxl_mres_set_state", (None, None))]:
+        f = getattr(lib, fn)
+        assert f(*[C.c_void_p(a) if a is None else a for a in args]) == INVALID_ARGUMENT, fn
+        assert lib.voxl_last_error().decode() == fn + ": null argument"
+
+
 def _build_dropin(tmp_path, name="dropin_dense"):
     exe = os.path.join(str(tmp_path), name)
     libdir = os.path.dirname(V.LIB_PATH)

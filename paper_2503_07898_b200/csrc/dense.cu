@@ -36,6 +36,16 @@ namespace {
 #ifndef VOXL_DENSE_MINB
 #define VOXL_DENSE_MINB 0
 #endif
+// D3Q27 fp32 at 512^3 (tools/gpu_q27_dense_variants.sh, ms per step / per
+// step_probe): plain step unconstrained (54 registers, 4 CTAs/SM) 4.58, with
+// 5 CTAs/SM 4.72, 4 CTAs/SM at 48 registers 4.73-4.74; fused-probe step with
+// 6 CTAs/SM (40 registers, 100 B spill) 5.17, with 5 CTAs/SM 4.77.
+#ifndef VOXL_DENSE_MINB27
+#define VOXL_DENSE_MINB27 0
+#endif
+#ifndef VOXL_DIAG_MINB27
+#define VOXL_DIAG_MINB27 5
+#endif
 // 256-thread CTAs: +4 % DRAM throughput over 128 on B200 (tools/micro/membw.cu).
 // Sweep at 512^3 (tools/gpu_dense_variants.sh, GLUPS): 256 threads 42.70-42.82,
 // 512 42.54-42.66, 512 with 3 CTAs/SM 42.66, 1024 28.2, 256 with 5 CTAs/SM 41.68.
@@ -97,7 +107,10 @@ __device__ __forceinline__ R ld_ro(const R* p) {
 /// AXIS is the partition axis (2 in 3D, 1 in 2D); `a` is x, `b` the remaining
 /// cross-section axis, `k` the local coordinate along AXIS.
 template <class L, class R, bool Exact, bool AOS, int AXIS, bool WRAP, bool DIAG>
-__global__ void __launch_bounds__(kBlock, (DIAG && sizeof(R) == 4) ? VOXL_DIAG_MINB * 256 / kBlock : VOXL_DENSE_MINB) dense_step_kernel(const __grid_constant__ StepArgs<L::Q, R> A) {
+__global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
+                                          : DIAG ? (L::Q == 27 ? VOXL_DIAG_MINB27 : VOXL_DIAG_MINB) * 256 / kBlock
+                                                 : (L::Q == 27 ? VOXL_DENSE_MINB27 : VOXL_DENSE_MINB))
+    dense_step_kernel(const __grid_constant__ StepArgs<L::Q, R> A) {
     constexpr int Q = L::Q;
     constexpr int OTHER = AXIS == 2 ? 1 : 2;
     using Ar = Arith<R, Exact>;

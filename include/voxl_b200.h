@@ -246,11 +246,11 @@ typedef struct voxl_mres voxl_mres;
 typedef struct voxl_mres_plan voxl_mres_plan;
 
 typedef struct {
-    int lattice;          /* VOXL_D3Q19 | VOXL_D3Q27 (device); plans also take VOXL_D2Q9 */
+    int lattice;          /* VOXL_D2Q9 (nz = 1) | VOXL_D3Q19 | VOXL_D3Q27 */
     int nx, ny, nz;       /* virtual finest domain */
     int levels;           /* 1..4 */
     double tau;           /* coarsest level; tau_l = 2 tau_{l+1} - 1/2 */
-    double lid_u[3];      /* lid velocity (cavity, lid on the max-z face) */
+    double lid_u[3];      /* lid velocity (cavity, lid on the max-z face; max-y in 2D) */
     int fused;            /* FusedCollideStream on uniform blocks (multires.cpp:541) */
     int precision;        /* VOXL_F32 | VOXL_F64 */
     int block_edge;       /* 8 (production) or 4 (reference granularity) */

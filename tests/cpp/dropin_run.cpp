@@ -47,6 +47,16 @@ int main(int argc, char** argv) {
         m.partitions = 1;
         dump(prefix, "multires", voxl::b200::run(m));
 
+        voxl::b200::SolverConfig m2 = m;  // run_multires with a D2Q9 config
+        m2.lattice = VOXL_D2Q9;
+        m2.nx = 32;
+        m2.ny = 32;
+        m2.nz = 1;
+        m2.tau = 0.6;
+        m2.levels = 3;
+        m2.steps = 3;
+        dump(prefix, "multires2d", voxl::b200::run(m2));
+
         voxl::b200::SolverConfig bad = c;
         bad.velocity = {5.0, 0.0, 0.0};  // blows up within a few steps
         bad.steps = 50;

@@ -129,6 +129,8 @@ def test_cpp_run_dropin_matches_oracle_and_python(tmp_path):
     sref = O.sparse_canonical(dom, act, O.port_sparse_run("D3Q19", dom, 0.7, (0.04, 0, 0), 5, act), 19)
     assert np.array_equal(field("sparse"), sref)
     assert np.array_equal(field("multires"), O.port_mres_run("D3Q19", dom, 2, 0.56, (0.05, 0.0, 0.0), 2))
+    assert np.array_equal(field("multires2d"), O.port_mres_run("D2Q9", (32, 32, 1), 3, 0.6, (0.05, 0.0, 0.0), 3,
+                                                               level_map=O.band_level_map((32, 32, 1), 3, 1)))
     cfgs = {"dense": dict(steps=12, partitions=2),
             "sparse": dict(scenario="flow_over_obstacle", tau=0.7, velocity=[0.04, 0, 0], steps=5,
                            strategy="disag_mem"),

@@ -83,6 +83,11 @@ def ref_lib():
         lib.vref_run_free.argtypes = [vp]
         lib.vref_reference_dense_run.argtypes = [cp, _dp]
         lib.vref_dense_steps_from.argtypes = [cp, _dp, _dp]
+        lib.vref_dense_create.argtypes = [cp, _dp]
+        lib.vref_dense_create.restype = vp
+        lib.vref_dense_step.argtypes = [vp, C.c_int]
+        lib.vref_dense_read.argtypes = [vp, _dp]
+        lib.vref_dense_free.argtypes = [vp]
         lib.vref_occ_run.argtypes = [C.c_int] * 9 + [_dp, _dp, C.POINTER(i64), C.POINTER(i64)]
         lib.vref_initial_state.argtypes = [cp, _dp]
         lib.vref_probe.argtypes = [C.c_int, _dp, i64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -287,6 +292,35 @@ def ref_dense_steps_from(cfg: dict, init: np.ndarray) -> np.ndarray:
     if ref_lib().vref_dense_steps_from(json.dumps(cfg).encode(), np.ascontiguousarray(init), out):
         raise RuntimeError(ref_error())
     return out
+
+
+class RefDense:
+    """A resident reference dense state (reference_dense_run's loop,
+    solver.cpp:189-206, split into create / step / read): the reference's own
+    fused_stream_collide sweeps without per-call allocation or copies."""
+
+    def __init__(self, cfg: dict, init: np.ndarray):
+        self.n = init.size
+        self._h = ref_lib().vref_dense_create(json.dumps(cfg).encode(), np.ascontiguousarray(init, np.float64))
+        if not self._h:
+            raise RuntimeError(ref_error())
+
+    def step(self, n=1):
+        if ref_lib().vref_dense_step(self._h, n):
+            raise RuntimeError(ref_error())
+
+    def state(self) -> np.ndarray:
+        out = np.empty(self.n, np.float64)
+        ref_lib().vref_dense_read(self._h, out)
+        return out
+
+    def close(self):
+        if self._h:
+            ref_lib().vref_dense_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def ref_initial_state(cfg: dict) -> np.ndarray:

@@ -185,6 +185,52 @@ int vref_dense_steps_from(const char* json, const double* init, double* out) {
     }
 }
 
+/// A resident reference_dense_run state (solver.cpp:189-206 split into create /
+/// step / read): the timed loop is the reference's own fused_stream_collide
+/// sweep with A/B swap, without per-call allocation or copies (the CPU
+/// baseline and bench.py's reference arm time this).
+struct DenseHandle {
+    Lattice lat;
+    lbm::FlowRules rules;
+    double inv_tau;
+    lbm::DenseState a, b;
+    DenseHandle(const SolverConfig& c)
+        : lat(build_lattice(c.lattice)), rules(rules_for(c)), inv_tau(1.0 / c.tau), a(c.domain, lat.q),
+          b(c.domain, lat.q) {}
+};
+
+void* vref_dense_create(const char* json, const double* init) {
+    try {
+        const SolverConfig c = config_from_json(json);
+        auto* h = new DenseHandle(c);
+        std::memcpy(h->a.f.data(), init, h->a.f.size() * sizeof(double));
+        return h;
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+int vref_dense_step(void* hv, int n) {
+    auto* h = static_cast<DenseHandle*>(hv);
+    try {
+        for (int s = 0; s < n; ++s) {
+            lbm::fused_stream_collide(h->lat, h->rules, h->inv_tau, h->a, h->b);
+            std::swap(h->a, h->b);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+void vref_dense_read(void* hv, double* out) {
+    auto* h = static_cast<DenseHandle*>(hv);
+    std::memcpy(out, h->a.f.data(), h->a.f.size() * sizeof(double));
+}
+
+void vref_dense_free(void* hv) { delete static_cast<DenseHandle*>(hv); }
+
 /// step_occ (partition.hpp:173) with the reference tests' generic kernels over a
 /// PartitionedField pair: op 1 = identity (partition_test.cpp:189-191, lattice
 /// q and TransferSets::for_lattice), op 2 = five-point Jacobi on a 2-component

@@ -114,3 +114,16 @@ def test_mres_oracle_2d_vs_reference():
     r = O.RefRun(cfg)
     out = O.port_mres_run("D2Q9", (32, 32), 3, 0.6, (0.05, 0, 0), 4)
     assert np.array_equal(out, r.field)
+
+
+@needs_ref
+def test_resident_reference_dense_equals_reference_dense_run():
+    """RefDense (what bench.py's CPU legs time: create once, sweep, read) is
+    reference_dense_run's loop: same bits after the same number of steps."""
+    cfg = dict(lattice="D3Q19", domain=[12, 10, 14], tau=0.56, scenario="lid_driven_cavity",
+               velocity=[0.05, 0, 0], steps=9)
+    r = O.RefDense(cfg, O.ref_initial_state(cfg))
+    r.step(4)
+    r.step(5)
+    assert np.array_equal(r.state(), O.ref_reference_dense_run(cfg))
+    r.close()

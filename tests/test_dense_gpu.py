@@ -183,3 +183,19 @@ def test_bench_line_contract_small():
     assert "error" not in p, p
     for k in ("sparse_disag_mem", "sparse_naive", "multires_obstacle_fused", "multires_obstacle_staged"):
         assert p[k]["MLUPS"] > 0, k
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+def test_fp64_bitwise_vs_reference_dense_run_1000_steps():
+    """configs[0]'s horizon: 1000 steps of the cavity against the reference's
+    own reference_dense_run (oracle/_ref, built from /root/reference), bitwise
+    (64^3 here, ~30 s of reference CPU time; tools/configs0_parity.py runs the
+    full 128^3 case: bitwise too)."""
+    n = 64
+    cfg = dict(lattice="D3Q19", domain=[n, n, n], tau=0.56, scenario="lid_driven_cavity", velocity=[0.05, 0, 0],
+               steps=1000)
+    ref = O.ref_reference_dense_run(cfg)
+    out = run_engine("D3Q19", (n, n, n), 0.56, "lid_driven_cavity", (0.05, 0, 0), 1000, O.ref_initial_state(cfg),
+                     precision="fp64", partitions=2)
+    assert np.array_equal(out, ref)

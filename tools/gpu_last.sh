@@ -1,0 +1,8 @@
+#!/bin/bash
+# Last verification at the final commit: full GPU suite, smoke, default bench, reference arm.
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/last_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/last_pytest.txt
+tail -2 gpurun_out/last_pytest.txt; grep -E "^FAILED" gpurun_out/last_pytest.txt | head
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/last_bench.txt 2>&1; tail -1 gpurun_out/last_bench.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['frac'], d['e2e']['value'], d['cpu_baseline']['value'], d['clocks'])"
+timeout 900 python bench.py --impl reference > gpurun_out/last_ref.txt 2>&1; tail -1 gpurun_out/last_ref.txt | cut -c1-160

@@ -23,6 +23,9 @@ struct MresArgs {
     R* nxt;
     R* post;
     R* post_ahead;  // kStreamAhead: the other post buffer (next step's jump-block collide)
+    double* probe_partial;       // kProbe: (sum f, max |u|^2) per CTA
+    unsigned int* probe_bad;     // kProbe: any unstable cell
+    int step_probe_base;         // kProbe: first probed block (partial slot 0)
     const std::int32_t* nbr;
     const std::uint64_t* amask;
     const std::uint8_t* cls;
@@ -105,10 +108,18 @@ __global__ void __launch_bounds__(E* E* E) mres_collide_kernel(const __grid_cons
 /// which explosion/coalescence and readout need) and also BGK(g) into the
 /// other post buffer, i.e. the next step's collide_level of the jump blocks
 /// (multires.cpp:443-456), so fused mode launches no separate collide.
-constexpr int kStream = 0, kFused = 1, kStreamAhead = 2;
+constexpr int kStream = 0, kFused = 1, kStreamAhead = 2, kProbe = 3;
+
+/// kProbe: probe_field terms (lbm.cpp:116-138) of the pulled pre-collision
+/// state, with block_probe_kernel's per-cell arithmetic (block_probe.cuh).
+struct ProbeAcc {
+    double mass = 0.0, vmax = 0.0;
+    bool bad = false;
+};
 
 template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID>
-__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src);
+__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src,
+                                               ProbeAcc* acc = nullptr);
 
 /// CTAs per block: 8^3 blocks are split over two 256-thread CTAs (6 CTAs / SM
 /// at 40 registers), so each CTA's metadata prologue hides behind five others.
@@ -142,15 +153,45 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
         if (tid == (BV / S > 64 ? 96 : 34)) s_solid = A.nsolid[b];
     }
     __syncthreads();
-    if (!s_full && !((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull)) return;
-    if constexpr (SOLID) {
-        if (s_solid) {
-            mres_pull_body<L, R, Exact, E, MODE, false, true>(A, b, t, s_src);
-            return;
+    const bool active = s_full || ((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull);
+    if constexpr (MODE != kProbe) {
+        if (!active) return;
+        if constexpr (SOLID) {
+            if (s_solid) {
+                mres_pull_body<L, R, Exact, E, MODE, false, true>(A, b, t, s_src);
+                return;
+            }
+        }
+        if (s_inner) mres_pull_body<L, R, Exact, E, MODE, true, false>(A, b, t, s_src);
+        else mres_pull_body<L, R, Exact, E, MODE, false, false>(A, b, t, s_src);
+    } else {
+        // every thread reaches the CTA reduction; partial slot = CTA index
+        // from the first probed block (fixed grid, fixed tree: deterministic)
+        ProbeAcc acc;
+        if (active) {
+            if (SOLID && s_solid) mres_pull_body<L, R, Exact, E, MODE, false, SOLID>(A, b, t, s_src, &acc);
+            else if (s_inner) mres_pull_body<L, R, Exact, E, MODE, true, false>(A, b, t, s_src, &acc);
+            else mres_pull_body<L, R, Exact, E, MODE, false, false>(A, b, t, s_src, &acc);
+        }
+        if (acc.bad) atomicOr(A.probe_bad, 1u);
+        constexpr int NT = BV / S;
+        __shared__ double sm[NT], sv[NT];
+        sm[tid] = acc.mass;
+        sv[tid] = acc.vmax;
+        __syncthreads();
+        for (int w = NT / 2; w > 0; w >>= 1) {
+            if (tid < w) {
+                sm[tid] += sm[tid + w];
+                sv[tid] = fmax(sv[tid], sv[tid + w]);
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            const long long slot = (long long)(b - A.step_probe_base) * S + int(blockIdx.x) % S;
+            A.probe_partial[2 * slot] = sm[0];
+            A.probe_partial[2 * slot + 1] = sv[0];
         }
     }
-    if (s_inner) mres_pull_body<L, R, Exact, E, MODE, true, false>(A, b, t, s_src);
-    else mres_pull_body<L, R, Exact, E, MODE, false, false>(A, b, t, s_src);
 }
 
 /// Pull over blocks [begin, begin + count): the part below `n_plain` (blocks
@@ -175,7 +216,8 @@ void launch_pull(MresArgs<L::Q, R> A, int begin, int count, int n_plain, cudaStr
 }
 
 template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID>
-__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src) {
+__device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src,
+                                               ProbeAcc* acc) {
     constexpr int Q = L::Q, BV = E * E * E;
     using Ar = Arith<R, Exact>;
     constexpr int LOG = BlockGeom<E>::LOG;
@@ -220,6 +262,29 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
             g[i] = v;
         }
     });
+    if constexpr (MODE == kProbe) {
+        // the uniform cell's pre-collision state, exactly what gather_uniform
+        // would store in cur, reduced instead of written
+        double r = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+        bool bh = false;
+        static_for<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            const double fi = double(g[i]) + (Exact ? 0.0 : L::w(i));
+            bh = bh || !(fabs(fi) <= 1e3);
+            r += fi;
+            mx = acc_term<double, false, L::ex(i)>(mx, fi);
+            my = acc_term<double, false, L::ey(i)>(my, fi);
+            mz = acc_term<double, false, L::ez(i)>(mz, fi);
+        });
+        acc->mass += r;
+        if (bh || !(r > 0.0)) {
+            acc->bad = true;
+        } else {
+            const double ux = mx / r, uy = my / r, uz = mz / r;
+            acc->vmax = fmax(acc->vmax, ux * ux + uy * uy + uz * uz);
+        }
+        return;
+    }
     auto collide = [&] {
         bool ok = true;
         R rho, u[3];
@@ -754,6 +819,7 @@ MultiResEngine::~MultiResEngine() {
     }
     cudaFree(d_error_);
     cudaFree(d_diag_);
+    cudaFree(probe_scratch_);
     if (side_) {
         cudaStreamSynchronize(side_);
         cudaEventDestroy(ev_fork_);
@@ -1184,7 +1250,12 @@ void MultiResEngine::device_probe(double out[3], DenseDiag* d) {
     auto* bad = reinterpret_cast<unsigned long long*>(row + 3);
     auto* bad_any = reinterpret_cast<unsigned int*>(row + 4);
     VOXL_CUDA(cudaMemsetAsync(d_diag_, 0, need * sizeof(double), stream_));
-    sync_state();  // uniform cells' pre-collision state (fused mode)
+    // Fused mode keeps the uniform cells' pre-collision state implicit (their
+    // post-collision storage): probe it through the collision-free pull that
+    // gather_uniform would store (kProbe), reduced in registers instead of
+    // written and re-read; the jump (and ghost-only) blocks' cur is stored.
+    const bool pull_probe = cfg_.fused && !cur_valid_;
+    constexpr int kHalf = kMresProbeBlocks / 2;
     auto shift_of = [&](auto lat) {
         using L = decltype(lat);
         ShiftQ<L::Q> sh{};
@@ -1196,13 +1267,37 @@ void MultiResEngine::device_probe(double out[3], DenseDiag* d) {
         const long long nb = V->ext.num_blocks();
         if (V->n_active == 0 || nb == 0) continue;
         const int lb = log2_exact(V->ext.block_volume());
-        mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto, auto) {
+        const int bv = V->ext.block_volume(), words = V->ext.mask_words();
+        const long long first = pull_probe ? V->n_uni : 0;  // blocks probed from storage
+        double* slots = d_diag_ + per_level * l;
+        mres_dispatch(cfg_.lattice, cfg_.precision, cfg_.edge, [&](auto lat, auto real, auto exact, auto e) {
             using L = decltype(lat);
             using R = decltype(real);
-            const int ctas = int(std::min<long long>(kMresProbeBlocks, nb));
-            block_probe_kernel<L, R><<<ctas, 256, 0, stream_>>>(static_cast<const R*>(V->cur), V->amask,
-                                                                V->ext.mask_words(), lb, nb, shift_of(lat),
-                                                                d_diag_ + per_level * l, bad_any);
+            constexpr bool X = decltype(exact)::value;
+            constexpr int E = decltype(e)::value;
+            if (pull_probe && V->n_uni > 0) {
+                const long long parts = (long long)V->n_uni * kSplit<E>;
+                if (probe_scratch_len_ < std::size_t(2 * parts)) {
+                    cudaFree(probe_scratch_);
+                    VOXL_CUDA(cudaMalloc(&probe_scratch_, 2 * parts * sizeof(double)));
+                    probe_scratch_len_ = std::size_t(2 * parts);
+                }
+                auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+                A.post = static_cast<R*>(V->post[V->parity ^ 1]);
+                A.probe_partial = probe_scratch_;
+                A.probe_bad = bad_any;
+                A.step_probe_base = 0;
+                launch_pull<L, R, X, E, kProbe>(A, 0, V->n_uni, V->n_plain, stream_);
+                partials_reduce_kernel<<<kHalf, 256, 0, stream_>>>(probe_scratch_, parts, slots);
+                slots += 2 * kHalf;
+            }
+            const long long n = nb - first;
+            if (n > 0) {
+                const int ctas = int(std::min<long long>(pull_probe ? kHalf : kMresProbeBlocks, n));
+                block_probe_kernel<L, R><<<ctas, 256, 0, stream_>>>(
+                    static_cast<const R*>(V->cur) + first * L::Q * bv, V->amask + first * words, words, lb, n,
+                    shift_of(lat), slots, bad_any);
+            }
         });
         VOXL_CUDA(cudaGetLastError());
     }
@@ -1222,6 +1317,7 @@ void MultiResEngine::device_probe(double out[3], DenseDiag* d) {
     d->max_speed = out[1];
     if (!any) return;
     // name the first unstable cell in canonical order (levels finest first)
+    sync_state();
     const unsigned long long none = ~0ull;
     VOXL_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, stream_));
     long long cell0 = 0;

@@ -94,6 +94,8 @@ private:
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     int* d_error_ = nullptr;
     double* d_diag_ = nullptr;
+    double* probe_scratch_ = nullptr;  // fused-mode pull probe: per-CTA partials of the uniform blocks
+    std::size_t probe_scratch_len_ = 0;
     std::size_t diag_len_ = 0;
     int steps_done_ = 0;
     // timing (events around each launch class) when non-null

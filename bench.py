@@ -239,14 +239,43 @@ def run_reference_arm(args, rank):
 
 # ---- our arm ------------------------------------------------------------------------------
 
+def launch_command(argv, gpus: int, port: int):
+    """The torchrun command bench.py re-executes itself under when asked for
+    N > 1 GPUs without a launcher: one rank per GPU on this node."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank)
         return
+    if args.gpus > 1 and not launched:
+        # `python bench.py --gpus N` alone: put N GPUs to work by re-launching
+        # under torchrun (one rank per GPU), which prints the one JSON line
+        if os.environ.get("VOXL_SHARE_DEVICE") != "1":
+            import torch
+
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}), flush=True)
+                sys.exit(1)
+        sys.exit(subprocess.call(launch_command(sys.argv[1:], args.gpus, free_port())))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import numpy as np
     import torch

@@ -55,6 +55,8 @@ extern "C" {
 #define VOXL_OP_LBM 0         /* closed step_occ operator set (see voxl_dense_desc::op) */
 #define VOXL_OP_IDENTITY 1
 #define VOXL_OP_JACOBI2 2
+#define VOXL_BAD_DENSITY 31   /* voxl_diag::bad_population of a non-positive density (macroscopic's
+                                 throw, lattice.cpp:124) rather than a population out of range */
 
 const char* voxl_last_error(void);
 int voxl_version(void);
@@ -147,6 +149,14 @@ int voxl_dense_probe(voxl_dense* h, voxl_diag* out);
 /** One step_occ with probe_field fused into the step kernel: the per-step
  *  diagnostics row of voxl::run (solver.cpp:245-255) without a second pass. */
 int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out);
+/** n x (step_occ + probe_field), the per-step loop of run_dense (solver.cpp:245-255),
+ *  with the probe fused into the step kernel and the diagnostics rows accumulated
+ *  on the device: one host synchronisation per 256 steps instead of one per step.
+ *  rows[s] = diagnostics of the s-th step. On the first failing step the call
+ *  returns VOXL_INSTABILITY with run()'s text ("run aborted at step N:
+ *  macroscopic: non-positive density" / "... instability at step N, voxel V,
+ *  population I", N = the engine's step index) and *completed = the rows filled. */
+int voxl_dense_step_probe_n(voxl_dense* h, int n, voxl_diag* rows, int* completed);
 /** Ledger records of one step in the reference's order (partition.cpp:163-206). */
 int voxl_dense_ledger(voxl_dense* h, int step, voxl_transfer_record* out, int cap, int* count);
 /** The same records from a descriptor alone (no device needed). */

@@ -218,10 +218,13 @@ struct RunResult {
 namespace detail {
 
 inline void abort_if_unstable(const voxl_diag& d, int step) {
-    if (d.unstable)  // probe_field's throw (lbm.cpp:124-128), rewrapped as run() does (solver.cpp:251-254)
-        throw std::runtime_error("run aborted at step " + std::to_string(step) + ": instability at step " +
-                                 std::to_string(step) + ", voxel " + std::to_string(d.bad_voxel) +
-                                 ", population " + std::to_string(d.bad_population));
+    if (!d.unstable) return;
+    const std::string head = "run aborted at step " + std::to_string(step) + ": ";
+    if (d.bad_population == VOXL_BAD_DENSITY)  // macroscopic's throw inside probe_field (lattice.cpp:124)
+        throw std::runtime_error(head + "macroscopic: non-positive density");
+    // probe_field's throw (lbm.cpp:124-128), rewrapped as run() does (solver.cpp:251-254)
+    throw std::runtime_error(head + "instability at step " + std::to_string(step) + ", voxel " +
+                             std::to_string(d.bad_voxel) + ", population " + std::to_string(d.bad_population));
 }
 
 inline std::string text_of(int (*get)(void*, char*, std::int64_t, std::int64_t*), void* h) {
@@ -257,14 +260,17 @@ inline RunResult run_dense(const SolverConfig& c) {
     std::vector<double> state(std::size_t(c.volume()) * c.q());
     check(voxl_initial_state(c.lattice, c.scenario, c.nx, c.ny, c.nz, c.seed, c.perturbation, state.data()));
     e.fill_canonical(state);
-    for (int step = 0; step < c.steps; ++step) {
-        voxl_diag g{};
-        check(voxl_dense_step_probe(e.handle(), &g));
-        abort_if_unstable(g, step);
-        r.diagnostics.push_back({step, g.mass, g.max_speed});
+    // step_occ + probe_field per step; the rows come back once per batch and
+    // the first failing step aborts with run()'s text (voxl_dense_step_probe_n)
+    std::vector<voxl_diag> rows(std::size_t(std::max(c.steps, 0)));
+    int done = 0;
+    const int status = voxl_dense_step_probe_n(e.handle(), c.steps, rows.data(), &done);
+    for (int step = 0; step < done; ++step) {
+        r.diagnostics.push_back({step, rows[std::size_t(step)].mass, rows[std::size_t(step)].max_speed});
         const auto recs = e.ledger(step);
         r.ledger.insert(r.ledger.end(), recs.begin(), recs.end());
     }
+    check(status);
     r.field = e.to_canonical(state.size());
     return r;
 }

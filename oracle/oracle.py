@@ -131,6 +131,8 @@ def ref_lib():
         lib.vref_mres_total_mass.argtypes = [vp]
         lib.vref_mres_total_mass.restype = C.c_double
         lib.vref_mres_text.argtypes = [vp, C.c_int, C.c_char_p, i64]
+        lib.vref_mres_set_state.argtypes = [vp, _dp]
+        lib.vref_probed_steps.argtypes = [C.c_int, vp, C.c_int, _dp, C.c_char_p, i64]
         _ref = lib
     return _ref
 
@@ -323,6 +325,16 @@ class RefDense:
         self.close()
 
 
+def ref_probed_steps(kind: int, handle, steps: int):
+    """run()'s per-step loop (step + probe_field, solver.cpp:245-255) on a
+    resident reference engine (kind 0 RefDense, 1 RefSparse, 2 RefMres):
+    (rows [(mass, max_speed)], abort text or "")."""
+    diag = np.zeros(2 * max(steps, 1), np.float64)
+    msg = C.create_string_buffer(512)
+    done = ref_lib().vref_probed_steps(kind, handle, steps, diag, msg, 512)
+    return [(diag[2 * i], diag[2 * i + 1]) for i in range(done)], msg.value.decode()
+
+
 def ref_initial_state(cfg: dict) -> np.ndarray:
     nx, ny, nz = _dims(cfg["domain"])
     out = np.empty(nx * ny * nz * Q_OF[cfg.get("lattice", "D3Q19")], np.float64)
@@ -470,6 +482,9 @@ class RefMres:
         out = np.empty(n, np.float64)
         self.lib.vref_mres_state(self.h, out)
         return out
+
+    def set_state(self, canonical):
+        self.lib.vref_mres_set_state(self.h, np.ascontiguousarray(canonical, np.float64))
 
     def total_mass(self):
         return self.lib.vref_mres_total_mass(self.h)

@@ -96,10 +96,12 @@ struct RunHandle {
 
 struct SparseHandle {
     std::unique_ptr<sparse::SparseLbmEngine> engine;
+    LatticeKind kind = LatticeKind::D3Q19;
 };
 
 struct MresHandle {
     std::unique_ptr<mres::MultiResLbm> engine;
+    LatticeKind kind = LatticeKind::D3Q19;
 };
 
 } // namespace
@@ -423,6 +425,7 @@ void* vref_sparse_create(const char* json, int block_edge) {
         const SolverConfig c = config_from_json(json);
         const Lattice lat = build_lattice(c.lattice);
         auto h = new SparseHandle;
+        h->kind = c.lattice;
         h->engine = std::make_unique<sparse::SparseLbmEngine>(
             lat, sparse::SparseScenario::wind_tunnel(c.domain, c.tau, c.velocity),
             obstacle_active(c), block_edge, c.strategy);
@@ -501,6 +504,7 @@ void* vref_mres_create(const char* json) {
         mres::MultiResGrid grid =
             mres::MultiResGrid::build(c.domain, c.levels, lat, band_level_map(c), c.tau);
         auto h = new MresHandle;
+        h->kind = c.lattice;
         h->engine = std::make_unique<mres::MultiResLbm>(lat, std::move(grid), rules_for(c), c.fused);
         return h;
     } catch (const std::exception& e) {
@@ -573,6 +577,82 @@ int vref_mres_text(void* h, int what, char* out, std::int64_t cap) {
     const auto& e = *((MresHandle*)h)->engine;
     if (what == 0) return copy_text(e.graph().to_dot(), out, cap);
     return copy_text(e.distribution_report(), out, cap);
+}
+
+/// MultiResLbm::set_state (multires.hpp:158) per level from a canonical array in
+/// canonical_state's order (levels finest first, cells by pack_coord).
+void vref_mres_set_state(void* h, const double* canonical) {
+    auto& e = *((MresHandle*)h)->engine;
+    const int q = build_lattice(((MresHandle*)h)->kind).q;
+    std::int64_t base = 0;
+    for (int l = 0; l < e.grid().num_levels(); ++l) {
+        const auto& blocks = e.grid().level(l).blocks;
+        const int edge = blocks.edge();
+        std::vector<std::uint64_t> keys;
+        for (int b = 0; b < blocks.num_blocks(); ++b) {
+            const sparse::Block& blk = blocks.blocks()[b];
+            for (int local = 0; local < blocks.block_volume(); ++local) {
+                if (!((blk.mask >> local) & 1)) continue;
+                const Vec3i v{blk.origin.x + local % edge, blk.origin.y + (local / edge) % edge,
+                              blk.origin.z + local / (edge * edge)};
+                keys.push_back(pack_coord(v));
+            }
+        }
+        std::sort(keys.begin(), keys.end());
+        std::unordered_map<std::uint64_t, std::int64_t> rank;
+        for (std::size_t r = 0; r < keys.size(); ++r) rank[keys[r]] = base + std::int64_t(r);
+        e.set_state(l, [&](Vec3i v, double* vals) {
+            const std::int64_t r = rank.at(pack_coord(v));
+            for (int i = 0; i < q; ++i) vals[i] = canonical[r * q + i];
+        });
+        base += std::int64_t(keys.size());
+    }
+}
+
+// ---- run()'s per-step loop on a resident engine --------------------------------
+
+/// The loop body of run_dense / run_sparse / run_multires (solver.cpp:245-255,
+/// 285-293, 341-349): step, then probe_field over the canonical state; the
+/// first failure is rewrapped exactly as run() does ("run aborted at step N: "
+/// + what()). kind 0 = a vref_dense_create handle (reference_dense_run's
+/// fused_stream_collide step, whose bgk_relax throws the same
+/// "macroscopic: non-positive density" as step_occ's), 1 = sparse, 2 =
+/// multires. diag gets (mass, max_speed) per completed step; returns the
+/// number of completed steps, msg the abort text ("" if none).
+int vref_probed_steps(int kind, void* h, int steps, double* diag, char* msg, std::int64_t cap) {
+    int step = 0;
+    std::string text;
+    for (; step < steps; ++step) {
+        try {
+            LatticeKind lk;
+            std::vector<double> canonical;
+            if (kind == 0) {
+                auto* d = static_cast<DenseHandle*>(h);
+                lbm::fused_stream_collide(d->lat, d->rules, d->inv_tau, d->a, d->b);
+                std::swap(d->a, d->b);
+                lk = d->lat.kind;
+                canonical = d->a.f;
+            } else if (kind == 1) {
+                auto* s = static_cast<SparseHandle*>(h);
+                s->engine->step();
+                lk = s->kind;
+                canonical = s->engine->canonical_state();
+            } else {
+                auto* m = static_cast<MresHandle*>(h);
+                m->engine->coarse_step();
+                lk = m->kind;
+                canonical = m->engine->canonical_state();
+            }
+            const lbm::Diagnostics dg = lbm::probe_field(build_lattice(lk), canonical, step);
+            diag[2 * step] = dg.mass;
+            diag[2 * step + 1] = dg.max_speed;
+        } catch (const std::runtime_error& e) {
+            text = "run aborted at step " + std::to_string(step) + ": " + e.what();
+            break;
+        }
+    }
+    copy_text(text, msg, cap);
+    return step;
 }
 
 } // extern "C"

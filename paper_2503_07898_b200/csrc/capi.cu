@@ -285,6 +285,26 @@ int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out) {
     });
 }
 
+int voxl_dense_step_probe_n(voxl_dense* h, int n, voxl_diag* rows, int* completed) {
+    if (completed) *completed = 0;
+    return guarded([&] {
+        need("voxl_dense_step_probe_n", h);
+        if (n > 0) need("voxl_dense_step_probe_n", rows);
+        std::vector<DenseDiag> r(std::size_t(std::max(n, 0)));
+        std::string msg;
+        const int done = h->eng->step_probe_n(n, r.data(), &msg);
+        for (int s = 0; s < done; ++s) {
+            rows[s] = voxl_diag{};
+            rows[s].mass = r[s].mass;
+            rows[s].max_speed = r[s].max_speed;
+            rows[s].bad_population = -1;
+            rows[s].bad_voxel = -1;
+        }
+        if (completed) *completed = done;
+        if (done < n) throw InstabilityError(msg);
+    });
+}
+
 int voxl_dense_probe(voxl_dense* h, voxl_diag* out) {
     return guarded([&] {
         need("voxl_dense_probe", h, out);

@@ -11,6 +11,7 @@
 #include "digest.cuh"
 #include "canon_io.cuh"
 #include "lattice.cuh"
+#include "diag_ring.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -23,9 +24,8 @@ namespace voxl_b200 {
 
 /// Where a step launch writes its fused-probe partials.
 struct DiagTarget {
-    double* partial = nullptr;
-    long long offset = 0;
-    unsigned long long* bad = nullptr;
+    unsigned long long* acc = nullptr;  // the step's accumulator lanes (diag_ring.cuh)
+    unsigned long long* bad = nullptr;  // the step's first-offender word
 };
 
 namespace {
@@ -50,17 +50,14 @@ namespace {
 // Sweep at 512^3 (tools/gpu_dense_variants.sh, GLUPS): 256 threads 42.70-42.82,
 // 512 42.54-42.66, 512 with 3 CTAs/SM 42.66, 1024 28.2, 256 with 5 CTAs/SM 41.68.
 constexpr int kBlock = VOXL_DENSE_BLOCK;
-#ifndef VOXL_DIAG_WARP
-#define VOXL_DIAG_WARP 1
-#endif
 #ifndef VOXL_DIAG_MINB
 #define VOXL_DIAG_MINB 6
 #endif
-// fused-probe partials: VOXL_DIAG_WARP 1 = one slot per warp (no CTA barrier),
-// 0 = one slot per CTA after a CTA barrier. Measured at 512^3 (step_probe, ms):
-// per warp 3.33-3.35, per CTA 3.41-3.43, per CTA by the last warp through an
-// smem counter 3.38.
-constexpr int kDiagSlots = VOXL_DIAG_WARP ? kBlock / 32 : 1;
+// fused probe: one lane per warp commits the warp's partial into the step's
+// accumulator lanes (diag_ring.cuh) with fire-and-forget reductions -- no CTA
+// barrier and no partial array in HBM. Earlier layouts at 512^3 (step_probe,
+// ms): per-warp 16-byte partials + two reduction kernels 3.33-3.35 (+0.28 GB
+// of DRAM writes per launch), per-CTA partials after a barrier 3.41-3.43.
 
 template <int Q, class R>
 struct StepArgs {
@@ -88,9 +85,8 @@ struct StepArgs {
     long long fast_in_off[Q];   // per-direction pull byte offset relative to fast_base + lin
     long long fast_out_off[Q];  // per-direction store byte offset
     int* error_flag;
-    double* diag_partial;            // fused probe: 2 doubles per CTA
-    long long diag_offset;           // first CTA slot of this launch
-    unsigned long long* diag_bad;    // (canonical voxel << 5) of the first unstable voxel
+    unsigned long long* diag_acc;    // fused probe: the step's accumulator lanes (diag_ring.cuh)
+    unsigned long long* diag_bad;    // (canonical voxel << 5) | population of the first offender
 };
 
 __device__ __forceinline__ int group_of(int k, int n) {
@@ -149,7 +145,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
     // result, and the instability test on the post-collision populations
     using P = std::conditional_t<Exact || sizeof(R) == 8, double, float>;
     P dg_mass = P(0), dg_v2 = P(0);
-    bool dg_bad = false;
+    int dg_bad = -1;  // first offending population of this voxel (probe_voxel)
     if (live) [&] {
     const int b = blockIdx.y;
     const int k = A.k_first + int(blockIdx.z) * A.k_step;
@@ -260,50 +256,29 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
     }();
 
     // Fused probe_field (lbm.cpp:116-138): the per-voxel terms were taken in
-    // probe_voxel; per-CTA mass and max |u| partials here (fixed-order
-    // reduction later, so run-to-run deterministic) and the instability flag.
+    // probe_voxel; the warp's mass and max |u|^2 go into the step's
+    // accumulator lanes (order-independent integer sums, diag_ring.cuh) and
+    // the first offender into the step's bad word.
     if constexpr (DIAG) {
         P pm = dg_mass, pv = dg_v2;
-        if (live && dg_bad) {
+        if (live && dg_bad >= 0) {
             const unsigned long long canon =
                 (unsigned long long)(A.kg0 + A.k_first + int(blockIdx.z) * A.k_step) * A.s +
                 (unsigned long long)(blockIdx.y * A.na + a);
-            atomicMin(A.diag_bad, canon << 5);
+            atomicMin(A.diag_bad, (canon << 5) | (unsigned long long)dg_bad);
         }
+        const unsigned live_lanes = __ballot_sync(0xffffffffu, live);
         for (int o = 16; o > 0; o >>= 1) {
             pm += __shfl_xor_sync(0xffffffffu, pm, o);
             pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
         }
-        double mass = double(pm);
-        const double v2 = double(pv);
-        if constexpr (std::is_same_v<P, float>) mass += double(__popc(__ballot_sync(0xffffffffu, live)));
-        const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-#if VOXL_DIAG_WARP
-        // one partial slot per warp: no CTA barrier, so a probing CTA retires
-        // warp by warp like the plain step
-        if ((threadIdx.x & 31) == 0) {
-            const long long slot = (A.diag_offset + blk) * kDiagSlots + (threadIdx.x >> 5);
-            A.diag_partial[2 * slot] = mass;
-            A.diag_partial[2 * slot + 1] = v2;
+        if ((threadIdx.x & 31) == 0 && live_lanes) {
+            double mass = double(pm);
+            if constexpr (std::is_same_v<P, float>) mass += double(__popc(live_lanes));
+            const unsigned long long blk =
+                ((unsigned long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            diag_commit(A.diag_acc, blk * (kBlock / 32) + (threadIdx.x >> 5), mass, double(pv));
         }
-#else
-        __shared__ double sm[kBlock / 32], sv[kBlock / 32];
-        const int w = threadIdx.x >> 5;
-        if ((threadIdx.x & 31) == 0) {
-            sm[w] = mass;
-            sv[w] = v2;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double m = 0.0, v = 0.0;
-            for (int j = 0; j < kBlock / 32; ++j) {
-                m += sm[j];
-                v = fmax(v, sv[j]);
-            }
-            A.diag_partial[2 * (A.diag_offset + blk)] = m;
-            A.diag_partial[2 * (A.diag_offset + blk) + 1] = v;
-        }
-#endif
     }
 }
 
@@ -366,32 +341,6 @@ __global__ void __launch_bounds__(kBlock) dense_operator_kernel(const __grid_con
             if ((A.low_mask >> c) & 1u) A.low_out[A.low_plane[c] + (long long)cross * VS] = f[c];
     }
     if (A.remote_fence && ((k == 0 && A.up_out) || (k == A.n - 1 && A.low_out))) __threadfence_system();
-}
-
-/// Fixed-order reduction of the per-CTA diagnostics partials (stage 1 of 2).
-__global__ void diag_reduce_kernel(const double* partial, long long n, double* out) {
-    __shared__ double sm[256], sv[256];
-    const long long per = (n + gridDim.x - 1) / gridDim.x;
-    const long long lo = (long long)blockIdx.x * per, hi = min(n, lo + per);
-    double m = 0.0, v = 0.0;
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        m += partial[2 * i];
-        v = fmax(v, partial[2 * i + 1]);
-    }
-    sm[threadIdx.x] = m;
-    sv[threadIdx.x] = v;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) {
-            sm[threadIdx.x] += sm[threadIdx.x + w];
-            sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + w]);
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        out[2 * blockIdx.x] = sm[0];
-        out[2 * blockIdx.x + 1] = sv[0];
-    }
 }
 
 // ---- cross-GPU step flags ---------------------------------------------------------------
@@ -551,7 +500,7 @@ __global__ void __launch_bounds__(kProbeThreads) probe_kernel(const R* buf, cons
         });
         if (bad_pop >= 0 || !(r > 0.0)) {
             const unsigned long long canon = (unsigned long long)(A.kg0 + k) * A.s + cross;
-            atomicMin(bad, (canon << 5) | (unsigned long long)(bad_pop < 0 ? 0 : bad_pop));
+            atomicMin(bad, (canon << 5) | (unsigned long long)(bad_pop < 0 ? kBadDensity : bad_pop));
         } else {
             vmax = fmax(vmax, (mx * mx + my * my + mz * mz) / (r * r));
         }
@@ -609,19 +558,6 @@ __global__ void __launch_bounds__(256) probe_final_kernel(const double* partial,
     }
 }
 
-/// step_probe's last kernel: the fixed-order final reduction, written with the
-/// device error flag into one 4-word row ({mass, max |u|^2, bad voxel bits,
-/// error step}) so the host reads the whole diagnostics row with one copy.
-__global__ void __launch_bounds__(256) step_probe_final_kernel(const double* partial, int n, double* row,
-                                                               const int* error_flag) {
-    double m, v;
-    block_reduce_partials(partial, n, m, v);
-    if (threadIdx.x == 0) {
-        row[0] = m;
-        row[1] = v;
-        reinterpret_cast<long long*>(row)[3] = *error_flag;
-    }
-}
 
 // ---- launch plumbing ------------------------------------------------------------------
 
@@ -755,10 +691,8 @@ struct DenseOps {
             A.fast_out_off[i] = rel * (long long)sizeof(R);
         }
         const dim3 grid((g.na + kBlock - 1) / kBlock, g.nb, k_count);
-        A.diag_partial = diag ? diag->partial : nullptr;
-        A.diag_offset = diag ? diag->offset : 0;
+        A.diag_acc = diag ? diag->acc : nullptr;
         A.diag_bad = diag ? diag->bad : nullptr;
-        if (diag) diag->offset += (long long)grid.x * grid.y * grid.z;  // CTA index; slots = offset * kDiagSlots
         auto go = [&](auto aos_c, auto wrap_c, auto diag_c) {
             dense_step_kernel<L, R, Exact, decltype(aos_c)::value, AXIS, decltype(wrap_c)::value,
                               decltype(diag_c)::value><<<grid, kBlock, 0, st>>>(A);
@@ -961,6 +895,7 @@ namespace {
 // ---- engine ------------------------------------------------------------------------
 
 DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg), io_(std::make_unique<CanonPipe>()) {
+    static_assert(kBadDensity == 31, "bad-word population field is 5 bits");
     const OperatorShape shape = operator_shape(cfg_);
     q_ = shape.q;
     axis_ = shape.axis;
@@ -1018,7 +953,6 @@ DenseEngine::~DenseEngine() {
     cudaFree(error_flag_);
     cudaFree(diag_scratch_);
     if (diag_row_host_) cudaFreeHost(diag_row_host_);
-    if (diag_partials_) cudaFree(diag_partials_);
     if (flags_ && distributed_) cudaFree(flags_);
     if (shared_stream_) {
         cudaStreamSynchronize(shared_stream_);
@@ -1027,6 +961,7 @@ DenseEngine::~DenseEngine() {
             cudaEventDestroy(ev_interior_[i]);
         }
         cudaEventDestroy(ev_join_);
+        cudaEventDestroy(ev_fork_);
         cudaStreamDestroy(shared_stream_);
     }
     if (stream_) cudaStreamDestroy(stream_);
@@ -1077,11 +1012,26 @@ void DenseEngine::scatter_gather(double* host, int k_begin, int k_end, bool to_d
     io_->run(host, k_end - k_begin, s, q_, to_device, wire32, shift, stream_, layout, consume, digest != nullptr);
 }
 
+void DenseEngine::check_plane_range(const char* who, int k_begin, int k_end) const {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int p = 0; p < cfg_.partitions; ++p)
+        if (local(p)) {
+            lo = std::min(lo, decomp_.slabs[p].first);
+            hi = std::max(hi, decomp_.slabs[p].second);
+        }
+    if (!(lo <= k_begin && k_begin <= k_end && k_end <= hi))
+        throw std::out_of_range(std::string(who) + ": planes [" + std::to_string(k_begin) + ", " +
+                                std::to_string(k_end) + ") outside the owned slabs [" + std::to_string(lo) + ", " +
+                                std::to_string(hi) + ")");
+}
+
 void DenseEngine::set_canonical_planes(const double* host, int k_begin, int k_end) {
+    check_plane_range("set_canonical_planes", k_begin, k_end);
     scatter_gather(const_cast<double*>(host), k_begin, k_end, true);
 }
 
 void DenseEngine::get_canonical_planes(double* host, int k_begin, int k_end) {
+    check_plane_range("get_canonical_planes", k_begin, k_end);
     scatter_gather(host, k_begin, k_end, false);
 }
 
@@ -1172,6 +1122,7 @@ void DenseEngine::enable_distributed() {
             VOXL_CUDA(cudaEventCreateWithFlags(&ev_interior_[i], cudaEventDisableTiming));
         }
         VOXL_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+        VOXL_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     }
     if (const char* e = std::getenv("VOXL_HALO_TIMEOUT_S")) {
         const double sec = std::atof(e);
@@ -1348,48 +1299,64 @@ void DenseEngine::step(int n) {
     check_errors();
 }
 
+int DenseEngine::step_probe_n(int n, DenseDiag* rows, std::string* abort_msg) {
+    // Batches of up to kDiagBatch steps: each step launches the step kernel
+    // with probe_field fused (accumulating into the step's ring slot); one
+    // reduction kernel, one copy and one host synchronisation per batch.
+    if (n < 0) throw std::invalid_argument("step_probe: n must be >= 0");
+    if (!ring_) ring_ = std::make_unique<DiagRing>();
+    int done = 0;
+    while (done < n) {
+        const int b = std::min(n - done, kDiagBatch);
+        const int step0 = steps_done_;
+        ring_->begin(b, stream_);
+        // the shared-layer stream (multi-process OCC) writes the ring too
+        if (shared_stream_) {
+            VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
+            VOXL_CUDA(cudaStreamWaitEvent(shared_stream_, ev_fork_, 0));
+        }
+        for (int s = 0; s < b; ++s) {
+            DiagTarget dt;
+            dt.acc = ring_->acc(s);
+            dt.bad = ring_->bad(s);
+            launch_step(&dt);
+        }
+        join_streams();
+        ring_->reduce(error_flag_, stream_);
+        VOXL_CUDA(cudaStreamSynchronize(stream_));
+        const DiagRow* r = ring_->rows();
+        std::string msg;
+        const int fail = first_failure(r, b, step0, ring_->error_flag(), &msg);
+        const int good = fail < 0 ? b : fail;
+        for (int s = 0; s < good; ++s) {
+            DenseDiag& d = rows[done + s];
+            d = DenseDiag{};
+            d.mass = r[s].mass;
+            d.max_speed = std::sqrt(r[s].v2);
+        }
+        done += good;
+        if (fail >= 0) {
+            if (abort_msg) *abort_msg = msg;
+            last_bad_ = r[fail].bad;
+            return done;
+        }
+    }
+    return done;
+}
+
 DenseDiag DenseEngine::step_probe() {
-    long long ctas = 0;
-    for (int p = 0; p < cfg_.partitions; ++p)
-        if (local(p))
-            dispatch(cfg_,
-                     [&](auto ops) { ctas += decltype(ops)::launch_ctas(decomp_, p, decomp_.thickness(p)); });
-    const long long slots = ctas * kDiagSlots;
-    if (diag_partials_len_ < std::size_t(2 * slots)) {
-        if (diag_partials_) VOXL_CUDA(cudaFree(diag_partials_));
-        VOXL_CUDA(cudaMalloc(&diag_partials_, 2 * slots * sizeof(double)));
-        diag_partials_len_ = std::size_t(2 * slots);
-    }
-    // One memset, the step (with the fused probe partials), two reduction
-    // kernels and one 32-byte copy of the diagnostics row into pinned memory:
-    // a single host round trip per step, as run() needs (solver.cpp:245-255).
-    double* stage = diag_scratch_;
-    double* row = diag_scratch_ + 2 * kProbeBlocks;
-    auto* bad = reinterpret_cast<unsigned long long*>(row + 2);
-    VOXL_CUDA(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), stream_));
-    DiagTarget dt;
-    dt.partial = diag_partials_;
-    dt.bad = bad;
-    launch_step(&dt);
-    diag_reduce_kernel<<<kProbeBlocks, 256, 0, stream_>>>(diag_partials_, dt.offset * kDiagSlots, stage);
-    step_probe_final_kernel<<<1, 256, 0, stream_>>>(stage, kProbeBlocks, row, error_flag_);
-    VOXL_CUDA(cudaGetLastError());
-    VOXL_CUDA(cudaMemcpyAsync(diag_row_host_, row, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
-    VOXL_CUDA(cudaStreamSynchronize(stream_));
-    const double* res = diag_row_host_;
-    const unsigned long long b = reinterpret_cast<const unsigned long long*>(res)[2];
-    const long long flag = reinterpret_cast<const long long*>(res)[3];
-    if (flag != INT_MAX)
-        throw InstabilityError("run aborted at step " + std::to_string(flag) +
-                               ": macroscopic: non-positive density");
+    // One probed step; a probe_field instability comes back in the row (the
+    // caller composes run()'s text), a non-positive density throws.
     DenseDiag d;
-    d.mass = res[0];
-    d.max_speed = std::sqrt(res[1]);
-    if (b != ~0ull) {
-        d.unstable = 1;
-        d.bad_voxel = std::int64_t(b >> 5);
-        d.bad_population = 0;
-    }
+    std::string msg;
+    if (step_probe_n(1, &d, &msg) == 1) return d;
+    if (msg.find("macroscopic") != std::string::npos) throw InstabilityError(msg);
+    d = DenseDiag{};
+    d.unstable = 1;
+    d.bad_voxel = std::int64_t(last_bad_ >> 5);
+    d.bad_population = int(last_bad_ & 31u);
+    d.mass = std::nan("");
+    d.max_speed = std::nan("");
     return d;
 }
 

@@ -25,6 +25,7 @@
 namespace voxl_b200 {
 
 class CanonPipe;
+class DiagRing;
 
 struct DiagTarget;
 enum class Precision : int { F32 = 0, F64 = 1 };
@@ -117,7 +118,14 @@ public:
     DenseDiag probe();
     /// One step with the probe fused into the step kernel (run()'s per-step
     /// diagnostics row, solver.cpp:245-255) -- no extra pass over the field.
+    /// A probe_field instability is returned in the row; a non-positive
+    /// density throws InstabilityError.
     DenseDiag step_probe();
+    /// n probed steps with one host synchronisation per kDiagBatch steps
+    /// (diag_ring.cuh). Fills rows[0, r) and returns r: r == n, or r is the
+    /// first failing step (relative) and *abort_msg holds run()'s text
+    /// ("run aborted at step N: ...", solver.cpp:251-254).
+    int step_probe_n(int n, DenseDiag* rows, std::string* abort_msg);
     /// Checks the device error flag; throws InstabilityError on a set flag.
     void check_errors();
 
@@ -172,8 +180,8 @@ private:
     double* diag_scratch_ = nullptr;
     double* diag_row_host_ = nullptr;
     unsigned long long halo_timeout_ns_ = 120ull * 1000 * 1000 * 1000;  // zero-copy flag wait limit  // pinned: step_probe's diagnostics row
-    double* diag_partials_ = nullptr;
-    std::size_t diag_partials_len_ = 0;
+    std::unique_ptr<DiagRing> ring_;  // per-step probe rows (diag_ring.cuh)
+    unsigned long long last_bad_ = ~0ull;
     std::size_t diag_scratch_len_ = 0;
     std::unique_ptr<CanonPipe> io_;  // canonical host <-> device pipeline (canon_io.cuh)
     std::uint32_t* flags_ = nullptr;
@@ -185,6 +193,7 @@ private:
     cudaEvent_t ev_shared_[2] = {nullptr, nullptr};
     cudaEvent_t ev_interior_[2] = {nullptr, nullptr};
     cudaEvent_t ev_join_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr;
     bool occ_ready_ = false;
     void join_streams();
 
@@ -194,6 +203,7 @@ private:
     void launch_step(struct DiagTarget* diag = nullptr);
     void launch_step_distributed(struct DiagTarget* diag);
     void scatter_gather(double* host, int k_begin, int k_end, bool to_device, unsigned long long* digest = nullptr);
+    void check_plane_range(const char* who, int k_begin, int k_end) const;
 };
 
 } // namespace voxl_b200

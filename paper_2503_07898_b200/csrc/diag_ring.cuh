@@ -1,0 +1,184 @@
+// diag_ring.cuh -- run()'s per-step probe_field rows (solver.cpp:245-255,
+// lbm.cpp:116-138), accumulated on the device by the fused step kernels and
+// read back once per batch of steps.
+//
+// No partial arrays: one lane per warp adds the warp's mass partial into one
+// of kDiagLanes accumulator lanes as a 128-bit fixed-point number (64
+// fraction bits, split over three 64-bit words so plain `red.add` never needs
+// a carry) and folds max |u|^2 in with an integer max of its fp64 bits
+// (non-negative doubles order like their bit patterns). Integer addition is
+// associative, so the per-step sums do not depend on the order the warps
+// retire or on how a step is cut into launches: deterministic, and a step
+// probed in plane chunks (the streamed run) gives the same row bit for bit.
+// The fixed point rounds each warp partial to 2^-64 (the reference's own
+// sequential fp64 sum is ~1e-8 off the exact sum at 512^3).
+//
+// Per step: kDiagLanes x 4 words (32 KB) + one "first bad voxel" word
+// ((canonical voxel << 5) | population, atomicMin: the reference's first
+// offender, voxel-major then population; population kBadDensity = 31 marks a
+// non-positive density, macroscopic's throw). One kernel reduces a whole batch
+// into 32-byte rows, one copy brings them and the engine's error flag home.
+#pragma once
+
+#include "common.cuh"
+#include "lattice.cuh"
+
+#include <climits>
+#include <string>
+
+namespace voxl_b200 {
+
+constexpr int kDiagLanes = 1024;  // power of two
+constexpr int kDiagWords = 4;     // fraction bits [0,32) | fraction bits [32,64) | integer part | max |u|^2 bits
+constexpr int kDiagBatch = 256;   // steps per read-back (8 MB of accumulators)
+
+struct DiagRow {
+    double mass;
+    double v2;                // max |u|^2 (the host takes the square root)
+    unsigned long long bad;   // ~0 = healthy
+    long long pad;
+};
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+/// One warp's contribution (called by a single lane). `warp_id` only spreads
+/// the accumulators over lanes; any mapping gives the same sums.
+__device__ __forceinline__ void diag_commit(unsigned long long* acc, unsigned long long warp_id, double mass,
+                                            double v2) {
+    unsigned long long* w = acc + (warp_id & (kDiagLanes - 1)) * kDiagWords;
+    if (fabs(mass) < 4.0e18) {  // a non-finite partial has a bad voxel, which the bad word reports
+        const double ip = floor(mass);
+        const unsigned long long frac = (unsigned long long)((mass - ip) * 18446744073709551616.0);
+        red_add_u64(w + 0, frac & 0xffffffffull);
+        red_add_u64(w + 1, frac >> 32);
+        red_add_u64(w + 2, (unsigned long long)(long long)ip);
+    }
+    if (v2 > 0.0) atomicMax(w + 3, (unsigned long long)__double_as_longlong(v2));
+}
+
+/// One CTA per step: exact integer sums over the lanes, composed once into fp64.
+__global__ void __launch_bounds__(256) diag_rows_kernel(const unsigned long long* acc, const unsigned long long* bad,
+                                                        DiagRow* rows) {
+    const unsigned long long* a = acc + (long long)blockIdx.x * kDiagLanes * kDiagWords;
+    unsigned long long w0 = 0, w1 = 0, w2 = 0, vm = 0;
+    for (int l = threadIdx.x; l < kDiagLanes; l += 256) {
+        w0 += a[l * kDiagWords + 0];
+        w1 += a[l * kDiagWords + 1];
+        w2 += a[l * kDiagWords + 2];
+        vm = max(vm, a[l * kDiagWords + 3]);
+    }
+    __shared__ unsigned long long s0[256], s1[256], s2[256], sv[256];
+    s0[threadIdx.x] = w0;
+    s1[threadIdx.x] = w1;
+    s2[threadIdx.x] = w2;
+    sv[threadIdx.x] = vm;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            s0[threadIdx.x] += s0[threadIdx.x + o];
+            s1[threadIdx.x] += s1[threadIdx.x + o];
+            s2[threadIdx.x] += s2[threadIdx.x + o];
+            sv[threadIdx.x] = max(sv[threadIdx.x], sv[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        // T = w2 * 2^64 + w1 * 2^32 + w0 (two's complement, 64 fraction bits)
+        const unsigned long long x0 = s0[0], x1 = s1[0];
+        const unsigned long long lo = x0 + (x1 << 32);
+        const unsigned long long hi = s2[0] + (x1 >> 32) + (lo < x0 ? 1ull : 0ull);
+        DiagRow r;
+        r.mass = double((long long)hi) + double(lo) * 0x1p-64;
+        r.v2 = __longlong_as_double((long long)sv[0]);
+        r.bad = bad[blockIdx.x];
+        r.pad = 0;
+        rows[blockIdx.x] = r;
+    }
+}
+
+/// Device accumulators + pinned rows of up to kDiagBatch probed steps.
+class DiagRing {
+public:
+    DiagRing() = default;
+    DiagRing(const DiagRing&) = delete;
+    DiagRing& operator=(const DiagRing&) = delete;
+    ~DiagRing() {
+        if (acc_) cudaFree(acc_);
+        if (bad_) cudaFree(bad_);
+        if (rows_) cudaFree(rows_);
+        if (host_) cudaFreeHost(host_);
+    }
+
+    /// Zero the accumulators of n <= kDiagBatch steps on `st`.
+    void begin(int n, cudaStream_t st) {
+        if (n < 1 || n > kDiagBatch) throw std::invalid_argument("DiagRing: batch size out of range");
+        if (!acc_) {
+            VOXL_CUDA(cudaMalloc(&acc_, std::size_t(kDiagBatch) * kDiagLanes * kDiagWords * 8));
+            VOXL_CUDA(cudaMalloc(&bad_, std::size_t(kDiagBatch) * 8));
+            VOXL_CUDA(cudaMalloc(&rows_, std::size_t(kDiagBatch) * sizeof(DiagRow)));
+            VOXL_CUDA(cudaMallocHost(&host_, std::size_t(kDiagBatch) * sizeof(DiagRow) + 16));
+        }
+        VOXL_CUDA(cudaMemsetAsync(acc_, 0, std::size_t(n) * kDiagLanes * kDiagWords * 8, st));
+        VOXL_CUDA(cudaMemsetAsync(bad_, 0xFF, std::size_t(n) * 8, st));
+        n_ = n;
+    }
+    unsigned long long* acc(int s) const { return acc_ + std::size_t(s) * kDiagLanes * kDiagWords; }
+    unsigned long long* bad(int s) const { return bad_ + s; }
+
+    /// Enqueue the batch's reduction and the read-back of the rows and of
+    /// `error_flag` (the engine's first non-positive-density step) on `st`.
+    void reduce(const int* error_flag, cudaStream_t st) {
+        diag_rows_kernel<<<n_, 256, 0, st>>>(acc_, bad_, rows_);
+        VOXL_CUDA(cudaGetLastError());
+        VOXL_CUDA(cudaMemcpyAsync(host_, rows_, std::size_t(n_) * sizeof(DiagRow), cudaMemcpyDeviceToHost, st));
+        if (error_flag)
+            VOXL_CUDA(cudaMemcpyAsync(flag_slot(), error_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        else
+            *flag_slot() = INT_MAX;
+    }
+    /// After the stream synchronised: the rows and the error flag.
+    const DiagRow* rows() const { return host_; }
+    int error_flag() const { return *flag_slot(); }
+
+private:
+    int* flag_slot() const { return reinterpret_cast<int*>(host_ + kDiagBatch); }
+    unsigned long long* acc_ = nullptr;
+    unsigned long long* bad_ = nullptr;
+    DiagRow* rows_ = nullptr;
+    DiagRow* host_ = nullptr;
+    int n_ = 0;
+};
+
+/// run()'s abort rule over a probed batch whose row s is absolute step
+/// step0 + s (solver.cpp:245-255): a step fails on a non-positive density
+/// during the collision (bgk_relax -> macroscopic, lattice.cpp:124; the
+/// engine's error flag holds the first such step) or on probe_field's
+/// instability test (lbm.cpp:124-128; the row's bad word). Returns the index
+/// of the first failing row (-1: none) and the reference's message.
+inline int first_failure(const DiagRow* rows, int n, int step0, int error_flag, std::string* msg) {
+    for (int s = 0; s < n; ++s) {
+        const int step = step0 + s;
+        const std::string head = "run aborted at step " + std::to_string(step) + ": ";
+        if (error_flag == step) {
+            *msg = head + "macroscopic: non-positive density";
+            return s;
+        }
+        if (rows[s].bad != ~0ull) {
+            const int pop = int(rows[s].bad & 31u);
+            if (pop == kBadDensity) *msg = head + "macroscopic: non-positive density";
+            else
+                *msg = head + "instability at step " + std::to_string(step) + ", voxel " +
+                       std::to_string((long long)(rows[s].bad >> 5)) + ", population " + std::to_string(pop);
+            return s;
+        }
+    }
+    if (error_flag != INT_MAX && error_flag < step0) {
+        *msg = "run aborted at step " + std::to_string(error_flag) + ": macroscopic: non-positive density";
+        return 0;
+    }
+    return -1;
+}
+
+} // namespace voxl_b200

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(256) mres_slot_probe_kernel(const R* cur, cons
         });
         mass += r;
         if (bp >= 0 || !(r > 0.0)) {
-            atomicMin(bad, ((unsigned long long)(cell0 + v) << 5) | (unsigned long long)(bp < 0 ? 0 : bp));
+            atomicMin(bad, ((unsigned long long)(cell0 + v) << 5) | (unsigned long long)(bp < 0 ? kBadDensity : bp));
         } else {
             const double ux = mx / r, uy = my / r, uz = mz / r;
             vmax = fmax(vmax, sqrt(ux * ux + uy * uy + uz * uz));
@@ -1191,7 +1191,7 @@ void MultiResEngine::check_errors() {
     VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
     if (flag != INT_MAX)
-        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": non-positive density");
+        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": macroscopic: non-positive density");
 }
 
 void MultiResEngine::coarse_step(int n) {

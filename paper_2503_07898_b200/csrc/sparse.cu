@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 
     // fused probe_field terms of this cell (DIAG)
     using P = std::conditional_t<Exact || sizeof(R) == 8, double, float>;
     P dg_mass = P(0), dg_v2 = P(0);
-    bool dg_bad = false;
+    int dg_bad = -1;  // first offending population of this voxel (probe_voxel)
     if (live) [&] {
     constexpr int LOG = E == 8 ? 3 : (E == 4 ? 2 : (E == 2 ? 1 : 0));
     const int lx = t & (E - 1), ly = (t >> LOG) & (E - 1), lz = t >> (2 * LOG);
@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 
     // fixed-order reduction later); an unstable cell only raises a flag --
     // the engine names it with the canonical-order probe (rare path).
     if constexpr (DIAG) {
-        if (live && dg_bad) atomicOr(A.diag_bad, 1u);
-        P pm = dg_mass, pv = dg_bad ? P(0) : dg_v2;
+        if (live && dg_bad >= 0) atomicOr(A.diag_bad, 1u);
+        P pm = dg_mass, pv = dg_bad >= 0 ? P(0) : dg_v2;
         for (int o = 16; o > 0; o >>= 1) {
             pm += __shfl_xor_sync(0xffffffffu, pm, o);
             pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
@@ -330,7 +330,7 @@ __global__ void sparse_probe_kernel(const R* buf, const std::int64_t* slots, lon
             mz = acc_term<double, false, L::ez(i)>(mz, fi);
         });
         if (bp >= 0 || !(r > 0.0)) {
-            atomicMin(bad, ((unsigned long long)v << 5) | (unsigned long long)(bp < 0 ? 0 : bp));
+            atomicMin(bad, ((unsigned long long)v << 5) | (unsigned long long)(bp < 0 ? kBadDensity : bp));
         } else {
             const double ux = mx / r, uy = my / r, uz = mz / r;
             vmax = fmax(vmax, sqrt(ux * ux + uy * uy + uz * uz));
@@ -692,7 +692,7 @@ void SparseEngine::check_errors() {
     VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
     if (flag != INT_MAX)
-        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": non-positive density");
+        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": macroscopic: non-positive density");
 }
 
 void SparseEngine::step(int n) {
@@ -729,7 +729,7 @@ DenseDiag SparseEngine::step_probe() {
     VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
     if (flag != INT_MAX)
-        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": non-positive density");
+        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": macroscopic: non-positive density");
     unsigned int any;
     std::memcpy(&any, &row[3], sizeof any);
     if (any) return probe();  // names the first unstable cell in canonical order

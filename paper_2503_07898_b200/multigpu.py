@@ -159,7 +159,14 @@ class DistributedDense:
                          self.desc["scenario"] == "periodic_box")[self.rank]
 
     def set_canonical_planes(self, host, k_begin, k_end):
+        k0, k1 = self.slab()
+        if not (k0 <= k_begin <= k_end <= k1):
+            raise ValueError(f"set_canonical_planes: planes [{k_begin}, {k_end}) outside this rank's slab [{k0}, {k1})")
         h = np.ascontiguousarray(host, np.float64)
+        dom = self.desc["domain"]
+        cross = dom[0] * (dom[1] if len(dom) == 3 and self.desc["lattice"] != "D2Q9" else 1)
+        if h.size != (k_end - k_begin) * cross * self.eng.q:
+            raise ValueError("set_canonical_planes: size mismatch")
         check(lib.voxl_dense_set_planes(self.eng._h, h.ctypes.data, k_begin, k_end))
 
     def get_canonical_planes(self, k_begin, k_end, out=None):
@@ -168,7 +175,11 @@ class DistributedDense:
         n = (k_end - k_begin) * cross * self.eng.q
         if out is None:
             out = np.empty(n, np.float64)
-        assert out.dtype == np.float64 and out.size == n and out.flags.c_contiguous
+        k0, k1 = self.slab()
+        if not (k0 <= k_begin <= k_end <= k1):
+            raise ValueError(f"get_canonical_planes: planes [{k_begin}, {k_end}) outside this rank's slab [{k0}, {k1})")
+        if not (out.dtype == np.float64 and out.size == n and out.flags.c_contiguous):
+            raise ValueError("get_canonical_planes: out must be a contiguous float64 array of the slab's size")
         check(lib.voxl_dense_get_planes(self.eng._h, out.ctypes.data, k_begin, k_end))
         return out
 

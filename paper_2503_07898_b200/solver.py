@@ -15,6 +15,8 @@ from dataclasses import dataclass, field as dc_field
 
 import numpy as np
 
+from ._capi import VoxlInstability
+
 LATTICE_NAMES = ("D2Q9", "D3Q19", "D3Q27")
 SCENARIOS = ("lid_driven_cavity", "flow_over_obstacle", "periodic_box")
 LAYOUTS = ("AoS", "SoA", "DisagSoA")
@@ -199,10 +201,16 @@ class RunResult:
         return "".join(lines)
 
 
+BAD_DENSITY = 31  # voxl_diag.bad_population of a non-positive density (VOXL_BAD_DENSITY)
+
+
 def _unstable(d, step):
-    if d.unstable:
-        raise RuntimeError(f"run aborted at step {step}: instability at step {step}, voxel {d.bad_voxel}, "
-                           f"population {d.bad_population}")
+    if not d.unstable:
+        return
+    if d.bad_population == BAD_DENSITY:  # macroscopic's throw inside probe_field (lattice.cpp:124)
+        raise RuntimeError(f"run aborted at step {step}: macroscopic: non-positive density")
+    raise RuntimeError(f"run aborted at step {step}: instability at step {step}, voxel {d.bad_voxel}, "
+                       f"population {d.bad_population}")
 
 
 def run_dense(c: SolverConfig) -> RunResult:
@@ -214,17 +222,24 @@ def run_dense(c: SolverConfig) -> RunResult:
     eng = DenseEngine(lattice=c.lattice, domain=c.domain, tau=c.tau, scenario=c.scenario, velocity=c.velocity,
                       layout=c.layout, partitions=c.partitions, precision=c.precision)
     eng.set_canonical(initial_canonical_state(c))
-    periodic = c.scenario == "periodic_box"
-    for step in range(c.steps):
-        d = eng.step_probe()  # step_occ + probe_field, fused on the device
-        _unstable(d, step)
+    # step_occ + probe_field per step, fused on the device; rows read back per
+    # batch, the first failing step raises run()'s text
+    try:
+        rows = eng.step_probe_n(c.steps)
+    except VoxlInstability as e:
+        rows, err = e.rows, e
+    else:
+        err = None
+    for step, d in enumerate(rows):
         r.diagnostics.append((step, d.mass, d.max_speed))
         r.ledger += plan_ledger(step, lattice=c.lattice, domain=c.domain, layout=c.layout, partitions=c.partitions,
                                 scenario=c.scenario)
         r.trace += [(step, 1, "halo", p) for p in range(c.partitions)]
         r.trace += [(step, 1, "private", p) for p in range(c.partitions)]
         r.trace += [(step, 2, "shared", p) for p in range(c.partitions)]
-    _ = periodic
+    if err is not None:
+        eng.close()
+        raise RuntimeError(str(err))
     r.field = eng.get_canonical()
     eng.close()
     nx, ny, nz = c.domain

@@ -169,6 +169,40 @@ def test_bench_multirank_path_on_one_gpu():
     assert abs(e2e["final_mass"] - 64 ** 3) < 1e-6 * 64 ** 3
 
 
+def test_bench_self_launch_command():
+    """`python bench.py --gpus N` without a launcher re-executes itself under
+    torchrun with one rank per GPU on 127.0.0.1 (CPU check of the command)."""
+    import importlib.util
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    cmd = bench.launch_command(["--gpus", "8", "--steps", "20", "--warmup", "5"], 8, 29577)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=8" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29577" in cmd
+    assert cmd[-7].endswith("bench.py") and cmd[-6:] == ["--gpus", "8", "--steps", "20", "--warmup", "5"]
+
+
+@pytest.mark.gpu
+def test_bench_gpus_2_without_torchrun():
+    """`python bench.py --gpus 2` with no torchrun wrapper runs 2 ranks and
+    reports n_gpus = 2 (ranks share cuda:0 on the one-GPU box)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VOXL_SHARE_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--steps", "6", "--warmup", "3", "--size", "64", "--no-cpu",
+           "--no-e2e"]
+    r = subprocess.run(cmd, capture_output=True, text=True, cwd=root, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["partitions"] == 2
+
+
 def _stall_worker(rank, world, port, result_q):
     import torch
     import torch.distributed as dist

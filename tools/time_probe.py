@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Per-step wall time of step() vs step_probe() (fused probe + diag row D2H)
-at n^3: {"step_ms": .., "step_probe_ms": ..}."""
+"""Per-step wall time of step() vs step_probe() (fused probe + diag row D2H
+every step) vs step_probe_n() (rows read back once per batch) at n^3."""
 import json
 import os
 import sys
@@ -23,6 +23,9 @@ t = time.perf_counter(); e.step(k); t1 = time.perf_counter()
 for _ in range(k):
     d = e.step_probe()
 t2 = time.perf_counter()
+rows = e.step_probe_n(k)
+t3 = time.perf_counter()
 print(json.dumps({"tag": os.environ.get("TAG", ""), "step_ms": round((t1 - t) / k * 1e3, 4),
-                  "step_probe_ms": round((t2 - t1) / k * 1e3, 4), "mass": d.mass, "max_speed": d.max_speed}))
+                  "step_probe_ms": round((t2 - t1) / k * 1e3, 4), "step_probe_n_ms": round((t3 - t2) / k * 1e3, 4),
+                  "mass": d.mass, "max_speed": d.max_speed, "mass_n": rows[-1].mass}))
 e.close()

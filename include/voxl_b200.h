@@ -49,6 +49,8 @@ extern "C" {
 #define VOXL_F64 1      /* bitwise parity mode */
 #define VOXL_HALO_ZERO_COPY 0 /* shared-layer kernel stores into the neighbour halo */
 #define VOXL_HALO_COPY 1      /* span copies after the step (halo_update)          */
+#define VOXL_HALO_NCCL 2      /* the same spans by grouped ncclSend/ncclRecv (multi-device engines,
+                                 one distinct device per partition): the measured comparison */
 #define VOXL_NAIVE 0          /* sparse::Strategy (sparse.hpp:117) */
 #define VOXL_DISAG_BITMASK 1
 #define VOXL_DISAG_MEM 2
@@ -121,6 +123,23 @@ typedef struct {
 
 /** PartitionedField x2 (partition.cpp:111) on the current device. */
 int voxl_dense_create(const voxl_dense_desc* desc, voxl_dense** out);
+/** The reference's in-process PartitionedField over several GPUs (partition.hpp:92-126):
+ *  partition p lives on devices[p] (`partitions` entries; repeats allowed, e.g. all 0).
+ *  Peer access is enabled between the devices; each partition runs the two-stream
+ *  OCC schedule (interior stream + high-priority shared-layer stream) and the
+ *  streams of neighbouring partitions are ordered by cross-device events, so the
+ *  zero-copy halo stores overlap the interior. graph_steps (even, 0 = off): steps
+ *  per captured CUDA graph replayed by voxl_dense_step / enqueue / timed_steps.
+ *  halo_mode VOXL_HALO_NCCL needs one distinct device per partition. */
+int voxl_dense_create_multi(const voxl_dense_desc* desc, const int* devices, int graph_steps, voxl_dense** out);
+/** Device of partition p. */
+int voxl_dense_device(voxl_dense* h, int partition, int* device);
+/** PartitionedField::neighbors (partition.hpp:110): (upper, lower), -1 at a domain end. */
+int voxl_dense_neighbors(voxl_dense* h, int partition, int* upper, int* lower);
+/** PartitionedField::set_neighbor_links (partition.hpp:111-113), the fault-injection
+ *  hook: the next step or halo refresh on asymmetric links fails with VOXL_RUNTIME
+ *  "halo_update: asymmetric neighbor links" (partition.cpp:165-171). */
+int voxl_dense_set_neighbor_links(voxl_dense* h, int partition, int upper, int lower);
 int voxl_dense_destroy(voxl_dense* h);
 /** fill_canonical (partition.cpp:143): canonical fp64, x fastest, component innermost. */
 int voxl_dense_set_canonical(voxl_dense* h, const double* host);

@@ -87,6 +87,10 @@ def _load():
         "voxl_decompose": ([C.c_int] * 6 + [vp], C.c_int),
         "voxl_classify_voxels": ([C.c_int] * 7 + [vp, i64], C.c_int),
         "voxl_dense_create": ([C.POINTER(DenseDesc), C.POINTER(vp)], C.c_int),
+        "voxl_dense_create_multi": ([C.POINTER(DenseDesc), vp, C.c_int, C.POINTER(vp)], C.c_int),
+        "voxl_dense_device": ([vp, C.c_int, C.POINTER(C.c_int)], C.c_int),
+        "voxl_dense_neighbors": ([vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+        "voxl_dense_set_neighbor_links": ([vp, C.c_int, C.c_int, C.c_int], C.c_int),
         "voxl_dense_destroy": ([vp], C.c_int),
         "voxl_dense_set_canonical": ([vp, vp], C.c_int),
         "voxl_dense_get_canonical": ([vp, vp], C.c_int),

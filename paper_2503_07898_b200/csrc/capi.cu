@@ -175,7 +175,7 @@ DenseConfig config_of(const voxl_dense_desc* desc) {
     c.partitions = desc->partitions;
     require(desc->precision == VOXL_F32 || desc->precision == VOXL_F64, "unknown precision");
     c.precision = Precision(desc->precision);
-    require(desc->halo_mode == 0 || desc->halo_mode == 1, "unknown halo mode");
+    require(desc->halo_mode >= VOXL_HALO_ZERO_COPY && desc->halo_mode <= VOXL_HALO_NCCL, "unknown halo mode");
     c.halo = HaloMode(desc->halo_mode);
     c.first_partition = desc->first_partition;
     c.local_partitions = desc->local_partitions;
@@ -189,6 +189,42 @@ int voxl_dense_create(const voxl_dense_desc* desc, voxl_dense** out) {
     return guarded([&] {
         require(desc && out, "voxl_dense_create: null argument");
         *out = new voxl_dense{new DenseEngine(config_of(desc))};
+    });
+}
+
+int voxl_dense_create_multi(const voxl_dense_desc* desc, const int* devices, int graph_steps, voxl_dense** out) {
+    return guarded([&] {
+        require(desc && devices && out, "voxl_dense_create_multi: null argument");
+        DenseConfig c = config_of(desc);
+        require(c.partitions >= 1, "voxl_dense_create_multi: partitions must be >= 1");
+        c.devices.assign(devices, devices + c.partitions);
+        c.graph_steps = graph_steps;
+        *out = new voxl_dense{new DenseEngine(c)};
+    });
+}
+
+int voxl_dense_device(voxl_dense* h, int p, int* device) {
+    return guarded([&] {
+        need("voxl_dense_device", h, device);
+        require(p >= 0 && p < h->eng->config().partitions, "voxl_dense_device: no such partition");
+        *device = h->eng->device_of(p);
+    });
+}
+
+int voxl_dense_neighbors(voxl_dense* h, int p, int* upper, int* lower) {
+    return guarded([&] {
+        need("voxl_dense_neighbors", h, upper, lower);
+        require(p >= 0 && p < h->eng->config().partitions, "voxl_dense_neighbors: no such partition");
+        const auto l = h->eng->neighbors(p);
+        *upper = l.first;
+        *lower = l.second;
+    });
+}
+
+int voxl_dense_set_neighbor_links(voxl_dense* h, int p, int upper, int lower) {
+    return guarded([&] {
+        need("voxl_dense_set_neighbor_links", h);
+        h->eng->set_neighbor_links(p, upper, lower);
     });
 }
 

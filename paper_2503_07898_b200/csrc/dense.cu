@@ -19,6 +19,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
+
+#include <dlfcn.h>
+#include <nccl.h>
 
 namespace voxl_b200 {
 
@@ -79,6 +83,7 @@ struct StepArgs {
     int periodic_a, periodic_b;
     int has_lid;
     int step;
+    const int* step_base;  // graph replays: absolute step = *step_base + step (read only on a failure)
     int remote_fence;  // remote halo stores cross a process/device: membar.sys after them
     int uniform_groups;  // all groups share one plane table (AoS / SoA)
     long long fast_base;  // byte offset of the interior plane table's component 0
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
             R rho, u[3], dr = R(0);
             if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
             else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok, DIAG ? &dr : nullptr);
-            if (!ok) atomicMin(A.error_flag, A.step);
+            if (!ok) atomicMin(A.error_flag, A.step_base ? *A.step_base + A.step : A.step);
             if constexpr (DIAG) probe_voxel<L, R, Exact, P>(f, rho, dr, u, dg_mass, dg_v2, dg_bad);
             char* base_out = reinterpret_cast<char*>(A.out) + A.fast_base + (long long)lin * (VS * sizeof(R));
             static_for<Q>([&](auto I) {
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
     R rho, u[3], dr = R(0);
     if constexpr (Exact) bgk_relax<L, R, true>(f, A.omega, A.keep, rho, u, ok);
     else bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok, DIAG ? &dr : nullptr);
-    if (!ok) atomicMin(A.error_flag, A.step);
+    if (!ok) atomicMin(A.error_flag, A.step_base ? *A.step_base + A.step : A.step);
     if constexpr (DIAG) probe_voxel<L, R, Exact, P>(f, rho, dr, u, dg_mass, dg_v2, dg_bad);
 
     static_for<Q>([&](auto I) {
@@ -649,9 +654,10 @@ struct DenseOps {
     static void launch_step(const DenseConfig& cfg, const Decomposition& d, const std::vector<LayoutMap>& maps,
                             int p, const void* in, void* out, void* up_out, void* low_out, bool wrap,
                             int step, int* error_flag, int k_first, int k_step, int k_count, cudaStream_t st,
-                            bool remote_fence = false, DiagTarget* diag = nullptr) {
+                            bool remote_fence = false, DiagTarget* diag = nullptr, const int* step_base = nullptr) {
         if (k_count <= 0) return;
         StepArgs<Q, R> A{};
+        A.step_base = step_base;
         const PartGeom g = fill_geometry(A, d, maps, p, in, out, up_out, low_out, k_first, k_step, remote_fence);
         const bool aos = maps[p].scheme() == LayoutScheme::AoS;
         const bool lid = cfg.scenario == Scenario::LidDrivenCavity;
@@ -779,7 +785,7 @@ struct OperatorOps {
     static void launch_step(const DenseConfig&, const Decomposition& d, const std::vector<LayoutMap>& maps, int p,
                             const void* in, void* out, void* up_out, void* low_out, bool, int, int*, int k_first,
                             int k_step, int k_count, cudaStream_t st, bool remote_fence = false,
-                            DiagTarget* diag = nullptr) {
+                            DiagTarget* diag = nullptr, const int* = nullptr) {
         if (diag) throw std::invalid_argument("probe_field requires the lbm operator");
         if (k_count <= 0) return;
         StepArgs<Q, R> A{};
@@ -894,6 +900,70 @@ namespace {
 
 // ---- engine ------------------------------------------------------------------------
 
+namespace {
+
+/// Makes `device` current for a scope (multi-device engines launch on the
+/// partition's device).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int device) {
+        VOXL_CUDA(cudaGetDevice(&prev));
+        if (device != prev) VOXL_CUDA(cudaSetDevice(device));
+    }
+    ~DeviceGuard() {
+        int now = -1;
+        if (cudaGetDevice(&now) == cudaSuccess && now != prev) cudaSetDevice(prev);
+    }
+};
+
+__global__ void advance_step_kernel(int* step_base, int n) { *step_base += n; }
+
+} // namespace
+
+/// NCCL transport of the halo spans for the in-process multi-device engine
+/// (halo mode Nccl): one communicator per partition device from
+/// ncclCommInitAll, every step's sends and receives in one group on the
+/// partitions' shared-layer streams. libnccl is opened at run time (dlopen),
+/// so the library carries no link-time NCCL dependency and shares whichever
+/// libnccl.so.2 the process already loaded.
+struct DenseEngine::NcclHalo {
+    void* lib = nullptr;
+    decltype(&ncclCommInitAll) init_all = nullptr;
+    decltype(&ncclCommDestroy) destroy = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+    std::vector<ncclComm_t> comms;
+
+    void check(ncclResult_t r, const char* what) const {
+        if (r != ncclSuccess)
+            throw CudaError(std::string("nccl ") + what + ": " + (error_string ? error_string(r) : "error"));
+    }
+    explicit NcclHalo(const std::vector<int>& devices) {
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) throw std::runtime_error(std::string("nccl halo mode: cannot load libnccl.so.2: ") + dlerror());
+        auto sym = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(lib, name));
+            if (!fn) throw std::runtime_error(std::string("nccl halo mode: missing symbol ") + name);
+        };
+        sym(init_all, "ncclCommInitAll");
+        sym(destroy, "ncclCommDestroy");
+        sym(group_start, "ncclGroupStart");
+        sym(group_end, "ncclGroupEnd");
+        sym(send, "ncclSend");
+        sym(recv, "ncclRecv");
+        sym(error_string, "ncclGetErrorString");
+        comms.resize(devices.size());
+        check(init_all(comms.data(), int(devices.size()), devices.data()), "ncclCommInitAll");
+    }
+    ~NcclHalo() {
+        for (ncclComm_t c : comms)
+            if (c) destroy(c);
+    }
+};
+
 DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg), io_(std::make_unique<CanonPipe>()) {
     static_assert(kBadDensity == 31, "bad-word population field is 5 bits");
     const OperatorShape shape = operator_shape(cfg_);
@@ -920,19 +990,41 @@ DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg), io_(std::make_uniq
     }
     if (cfg_.first_partition < 0 || cfg_.first_partition + cfg_.local_partitions > cfg_.partitions)
         throw std::invalid_argument("dense engine: bad local partition range");
+    int primary = 0;
+    VOXL_CUDA(cudaGetDevice(&primary));
+    if (!cfg_.devices.empty()) {
+        if (cfg_.local_partitions != cfg_.partitions)
+            throw std::invalid_argument("dense engine: devices[] places every partition of a single-process engine");
+        if (int(cfg_.devices.size()) != cfg_.partitions)
+            throw std::invalid_argument("dense engine: devices[] must name one device per partition");
+        int count = 0;
+        VOXL_CUDA(cudaGetDeviceCount(&count));
+        for (int d : cfg_.devices)
+            if (d < 0 || d >= count)
+                throw std::invalid_argument("dense engine: device " + std::to_string(d) + " does not exist (" +
+                                            std::to_string(count) + " visible)");
+        if (cfg_.graph_steps < 0 || cfg_.graph_steps % 2)
+            throw std::invalid_argument("dense engine: graph_steps must be even and >= 0");
+        multi_ = true;
+    }
+    if (cfg_.halo == HaloMode::Nccl && !multi_)
+        throw std::invalid_argument("nccl halo mode needs a multi-device engine (devices[])");
     for (int p = 0; p < cfg_.partitions; ++p) {
         std::array<int, 3> owned = cfg_.domain;
         owned[axis_] = decomp_.thickness(p);
         maps_.push_back(LayoutMap::build(cfg_.layout, owned, q_, axis_, shape.transfer));
+        links_.emplace_back(decomp_.upper_neighbor(p), decomp_.lower_neighbor(p));
     }
     parts_.resize(cfg_.partitions);
     VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     for (int p = 0; p < cfg_.partitions; ++p) {
+        parts_[p].device = multi_ ? cfg_.devices[p] : primary;
         if (!local(p)) continue;
         const std::size_t bytes = buffer_bytes(p);
+        DeviceGuard g(parts_[p].device);
         for (int w = 0; w < 2; ++w) {
             VOXL_CUDA(cudaMalloc(&parts_[p].buf[w], bytes));
-            VOXL_CUDA(cudaMemsetAsync(parts_[p].buf[w], 0, bytes, stream_));
+            VOXL_CUDA(cudaMemset(parts_[p].buf[w], 0, bytes));
         }
         parts_[p].owned = true;
     }
@@ -942,11 +1034,98 @@ DenseEngine::DenseEngine(const DenseConfig& cfg) : cfg_(cfg), io_(std::make_uniq
     diag_scratch_len_ = 2 * kProbeBlocks + 4;
     VOXL_CUDA(cudaMalloc(&diag_scratch_, diag_scratch_len_ * sizeof(double)));
     VOXL_CUDA(cudaMallocHost(&diag_row_host_, 4 * sizeof(double)));
+    if (multi_) setup_multi();
     VOXL_CUDA(cudaStreamSynchronize(stream_));
+}
+
+int DenseEngine::dev_index(int device) const {
+    for (std::size_t i = 0; i < dx_.size(); ++i)
+        if (dx_[i].device == device) return int(i);
+    throw std::logic_error("dense engine: device not registered");
+}
+
+void DenseEngine::setup_multi() {
+    int primary = 0;
+    VOXL_CUDA(cudaGetDevice(&primary));
+    std::vector<int> devs{primary};
+    for (int d : cfg_.devices)
+        if (std::find(devs.begin(), devs.end(), d) == devs.end()) devs.push_back(d);
+    // Peer access between every pair of engine devices: the shared-layer
+    // kernels store into the neighbours' halos, the canonical I/O and probe
+    // kernels on the engine stream read every partition, and a failing voxel
+    // sets the engine's error flag (one word on the primary device).
+    for (int a : devs)
+        for (int b : devs) {
+            if (a == b) continue;
+            int ok = 0;
+            VOXL_CUDA(cudaDeviceCanAccessPeer(&ok, a, b));
+            if (!ok)
+                throw std::runtime_error("dense engine: device " + std::to_string(a) + " cannot access device " +
+                                         std::to_string(b) + " (no peer path)");
+            DeviceGuard g(a);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else VOXL_CUDA(e);
+        }
+    dx_.resize(devs.size());
+    for (std::size_t i = 0; i < devs.size(); ++i) {
+        DevExec& d = dx_[i];
+        d.device = devs[i];
+        DeviceGuard g(d.device);
+        if (i == 0) d.aux = stream_;
+        else VOXL_CUDA(cudaStreamCreateWithFlags(&d.aux, cudaStreamNonBlocking));
+        VOXL_CUDA(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
+    }
+    px_.resize(std::size_t(cfg_.partitions));
+    for (int p = 0; p < cfg_.partitions; ++p) {
+        PartExec& x = px_[std::size_t(p)];
+        DeviceGuard g(parts_[p].device);
+        int lo = 0, hi = 0;
+        VOXL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        VOXL_CUDA(cudaStreamCreateWithFlags(&x.interior, cudaStreamNonBlocking));
+        VOXL_CUDA(cudaStreamCreateWithPriority(&x.shared, cudaStreamNonBlocking, hi));
+        for (int i = 0; i < 2; ++i) {
+            VOXL_CUDA(cudaEventCreateWithFlags(&x.ev_i[i], cudaEventDisableTiming));
+            VOXL_CUDA(cudaEventCreateWithFlags(&x.ev_s[i], cudaEventDisableTiming));
+        }
+    }
+    VOXL_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    VOXL_CUDA(cudaMalloc(&step_base_, sizeof(int)));
+    VOXL_CUDA(cudaMemset(step_base_, 0, sizeof(int)));
+    if (cfg_.halo == HaloMode::Nccl) {
+        std::vector<int> sorted = cfg_.devices;
+        std::sort(sorted.begin(), sorted.end());
+        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+            throw std::invalid_argument("nccl halo mode: one distinct device per partition (ncclCommInitAll)");
+        nccl_ = std::make_unique<NcclHalo>(cfg_.devices);
+    }
 }
 
 DenseEngine::~DenseEngine() {
     if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& x : px_) {
+        cudaStreamSynchronize(x.interior);
+        cudaStreamSynchronize(x.shared);
+    }
+    for (auto& d : dx_)
+        if (d.aux) cudaStreamSynchronize(d.aux);
+    nccl_.reset();
+    for (auto& g : graph_)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto& x : px_) {
+        cudaStreamDestroy(x.interior);
+        cudaStreamDestroy(x.shared);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(x.ev_i[i]);
+            cudaEventDestroy(x.ev_s[i]);
+        }
+    }
+    for (std::size_t i = 0; i < dx_.size(); ++i) {
+        dx_[i].ring.reset();
+        cudaEventDestroy(dx_[i].ev);
+        if (i > 0) cudaStreamDestroy(dx_[i].aux);
+    }
+    if (step_base_) cudaFree(step_base_);
     for (auto& p : parts_)
         if (p.owned)
             for (void* b : p.buf) cudaFree(b);
@@ -961,9 +1140,9 @@ DenseEngine::~DenseEngine() {
             cudaEventDestroy(ev_interior_[i]);
         }
         cudaEventDestroy(ev_join_);
-        cudaEventDestroy(ev_fork_);
         cudaStreamDestroy(shared_stream_);
     }
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -980,7 +1159,13 @@ std::size_t DenseEngine::buffer_bytes(int p) const { return std::size_t(maps_[p]
 void* DenseEngine::buffer(int p, int which) const { return parts_[p].buf[which == 0 ? cur_ : cur_ ^ 1]; }
 
 void DenseEngine::attach_peer(int p, void* b0, void* b1) {
+    if (p < 0 || p >= cfg_.partitions) throw std::invalid_argument("attach_peer: no such partition");
     if (local(p)) throw std::invalid_argument("attach_peer: partition is owned locally");
+    bool neighbour = false;
+    for (int q = 0; q < cfg_.partitions; ++q)
+        if (local(q) && (links_[q].first == p || links_[q].second == p)) neighbour = true;
+    if (!neighbour) throw std::invalid_argument("attach_peer: partition is not a neighbour of an owned partition");
+    if (!b0 || !b1) throw std::invalid_argument("attach_peer: null buffer");
     parts_[p].buf[0] = b0;
     parts_[p].buf[1] = b1;
 }
@@ -1101,18 +1286,43 @@ void DenseEngine::get_canonical(double* host) {
 
 void DenseEngine::halo_copy(int which) {
     // halo_update (partition.cpp:163-206): one cudaMemcpyAsync per contiguous
-    // span, source = shared slab of p, destination = neighbour's halo slab.
+    // span, source = shared slab of p, destination = neighbour's halo slab
+    // (peer copies when the partitions live on different devices).
+    check_links();
     const int par = which == 0 ? cur_ : cur_ ^ 1;
-    const auto recs = halo_records(decomp_, maps_, 0);
-    for (const auto& r : recs) {
+    for (const auto& r : ledger_records(0)) {
         if (!parts_[r.src].buf[par] || !parts_[r.dst].buf[par]) continue;
         char* dst = static_cast<char*>(parts_[r.dst].buf[par]) + r.dst_span.base * esize_;
         const char* src = static_cast<const char*>(parts_[r.src].buf[par]) + r.src_span.base * esize_;
-        VOXL_CUDA(cudaMemcpyAsync(dst, src, std::size_t(r.elements) * esize_, cudaMemcpyDeviceToDevice, stream_));
+        VOXL_CUDA(cudaMemcpyAsync(dst, src, std::size_t(r.elements) * esize_, cudaMemcpyDefault, stream_));
+    }
+}
+
+void DenseEngine::set_neighbor_links(int p, int upper, int lower) {
+    if (p < 0 || p >= cfg_.partitions) throw std::out_of_range("set_neighbor_links: no such partition");
+    links_[std::size_t(p)] = {upper, lower};
+}
+
+void DenseEngine::check_links() const {
+    // halo_update's symmetry test (partition.cpp:165-171), run before every
+    // batch of steps and every halo refresh.
+    const int P = cfg_.partitions;
+    for (int p = 0; p < P; ++p) {
+        const auto [up, low] = links_[std::size_t(p)];
+        if (up >= P || low >= P) throw std::runtime_error("halo_update: asymmetric neighbor links");
+        if (up >= 0 && links_[std::size_t(up)].second != p)
+            throw std::runtime_error("halo_update: asymmetric neighbor links");
+        if (low >= 0 && links_[std::size_t(low)].first != p)
+            throw std::runtime_error("halo_update: asymmetric neighbor links");
+        // the plane tables address the decomposition's neighbours: a symmetric
+        // re-wiring to any other partition is a span-structure change
+        if ((up >= 0 && up != decomp_.upper_neighbor(p)) || (low >= 0 && low != decomp_.lower_neighbor(p)))
+            throw std::runtime_error("halo_update: span structure mismatch");
     }
 }
 
 void DenseEngine::enable_distributed() {
+    if (multi_) throw std::invalid_argument("enable_distributed: a multi-device engine owns every partition");
     if (!shared_stream_) {
         int lo = 0, hi = 0;
         VOXL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1171,7 +1381,7 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     const bool wrap = cfg_.scenario == Scenario::PeriodicBox;
     const bool zero_copy = cfg_.halo == HaloMode::ZeroCopy;
     const int in = cur_, out = cur_ ^ 1;
-    const int up = decomp_.upper_neighbor(p), low = decomp_.lower_neighbor(p);
+    const int up = links_[std::size_t(p)].first, low = links_[std::size_t(p)].second;
     const unsigned t = unsigned(steps_done_);
     const int par = int(t & 1u), prev = par ^ 1;
     if (!occ_ready_) {
@@ -1233,7 +1443,7 @@ void DenseEngine::launch_step(DiagTarget* diag) {
     const int in = cur_, out = cur_ ^ 1;
     for (int p = 0; p < cfg_.partitions; ++p) {
         if (!local(p)) continue;
-        const int up = decomp_.upper_neighbor(p), low = decomp_.lower_neighbor(p);
+        const int up = links_[std::size_t(p)].first, low = links_[std::size_t(p)].second;
         void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
         void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
         const int n = decomp_.thickness(p);
@@ -1248,10 +1458,204 @@ void DenseEngine::launch_step(DiagTarget* diag) {
 }
 
 void DenseEngine::enqueue_steps(int n) {
+    check_links();
+    if (multi_) {
+        enqueue_multi(n, nullptr, true);
+        return;
+    }
     for (int i = 0; i < n; ++i) launch_step();
 }
 
+// ---- single-process multi-device schedule ----------------------------------------------
+//
+// Partition p runs on devices[p] with two streams, the multi-process OCC
+// schedule (launch_step_distributed) with the step flags replaced by
+// cross-device event waits, since every partition lives in this process:
+//
+//   I_p: after S_p(t-1)                                  -> interior(t)     [planes 1..n-2]
+//   S_p: after I_p(t-1), S_up(t-1), S_low(t-1)           -> shared(t)       [planes 0, n-1]
+//        (+ zero-copy peer stores into the neighbours' halos of the next
+//         buffer, or span copies / NCCL send-recv after it)
+//
+// S_up(t-1)/S_low(t-1) cover both hazards on the neighbours' halos: RAW (they
+// filled ours for step t) and WAR (they finished reading the halo slots of the
+// buffer our shared(t) now stores into). The interior never reads a halo, so it
+// overlaps the whole exchange. A batch of steps forks from the engine stream
+// (ev_fork_) and joins back into it, so the engine stream orders a batch
+// against I/O, probes and the next batch; graph replays capture exactly that
+// fork -> steps -> join shape.
+
+void DenseEngine::launch_step_multi(int step_off, bool first, const DiagTarget* dev_diag, bool capturing) {
+    const bool wrap = cfg_.scenario == Scenario::PeriodicBox;
+    const bool zero_copy = cfg_.halo == HaloMode::ZeroCopy;
+    const int in = cur_, out = cur_ ^ 1;
+    const int par = steps_done_ & 1, prev = par ^ 1;
+    const int step_arg = capturing ? step_off : steps_done_;
+    const int* sb = capturing ? step_base_ : nullptr;
+    const int P = cfg_.partitions;
+    auto ready = [&](int p) { return dev_diag ? dx_[std::size_t(dev_index(parts_[p].device))].ev : ev_fork_; };
+    auto diag_of = [&](int p) -> DiagTarget* {
+        if (!dev_diag) return nullptr;
+        return const_cast<DiagTarget*>(&dev_diag[dev_index(parts_[p].device)]);
+    };
+    for (int p = 0; p < P; ++p) {
+        PartExec& x = px_[std::size_t(p)];
+        DeviceGuard g(parts_[p].device);
+        VOXL_CUDA(cudaStreamWaitEvent(x.interior, first ? ready(p) : x.ev_s[prev], 0));
+        const int n = decomp_.thickness(p);
+        dispatch(cfg_, [&](auto ops) {
+            decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr,
+                                       wrap, step_arg, error_flag_, 1, 1, n - 2, x.interior, false, diag_of(p), sb);
+        });
+        VOXL_CUDA(cudaEventRecord(x.ev_i[par], x.interior));
+    }
+    for (int p = 0; p < P; ++p) {
+        PartExec& x = px_[std::size_t(p)];
+        DeviceGuard g(parts_[p].device);
+        const int up = links_[std::size_t(p)].first, low = links_[std::size_t(p)].second;
+        if (first) {
+            VOXL_CUDA(cudaStreamWaitEvent(x.shared, ready(p), 0));
+        } else {
+            VOXL_CUDA(cudaStreamWaitEvent(x.shared, x.ev_i[prev], 0));
+            if (up >= 0 && up != p) VOXL_CUDA(cudaStreamWaitEvent(x.shared, px_[std::size_t(up)].ev_s[prev], 0));
+            if (low >= 0 && low != p && low != up)
+                VOXL_CUDA(cudaStreamWaitEvent(x.shared, px_[std::size_t(low)].ev_s[prev], 0));
+        }
+        const int n = decomp_.thickness(p);
+        void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
+        void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
+        dispatch(cfg_, [&](auto ops) {
+            decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out,
+                                       wrap, step_arg, error_flag_, 0, n - 1, 2, x.shared, false, diag_of(p), sb);
+        });
+        if (cfg_.halo == HaloMode::Copy)
+            for (const auto& r : ledger_records(0)) {
+                if (r.src != p) continue;
+                char* dst = static_cast<char*>(parts_[r.dst].buf[out]) + r.dst_span.base * esize_;
+                const char* src = static_cast<const char*>(parts_[r.src].buf[out]) + r.src_span.base * esize_;
+                VOXL_CUDA(cudaMemcpyAsync(dst, src, std::size_t(r.elements) * esize_, cudaMemcpyDefault, x.shared));
+            }
+    }
+    if (nccl_) {
+        // every partition's sends and receives in one group (one thread drives
+        // all communicators); records in the reference's order on both sides
+        nccl_->check(nccl_->group_start(), "ncclGroupStart");
+        for (const auto& r : ledger_records(0)) {
+            const std::size_t bytes = std::size_t(r.elements) * esize_;
+            const char* src = static_cast<const char*>(parts_[r.src].buf[out]) + r.src_span.base * esize_;
+            char* dst = static_cast<char*>(parts_[r.dst].buf[out]) + r.dst_span.base * esize_;
+            nccl_->check(nccl_->send(src, bytes, ncclInt8, r.dst, nccl_->comms[std::size_t(r.src)],
+                                     px_[std::size_t(r.src)].shared), "ncclSend");
+            nccl_->check(nccl_->recv(dst, bytes, ncclInt8, r.src, nccl_->comms[std::size_t(r.dst)],
+                                     px_[std::size_t(r.dst)].shared), "ncclRecv");
+        }
+        nccl_->check(nccl_->group_end(), "ncclGroupEnd");
+    }
+    for (int p = 0; p < P; ++p) {
+        DeviceGuard g(parts_[p].device);
+        VOXL_CUDA(cudaEventRecord(px_[std::size_t(p)].ev_s[par], px_[std::size_t(p)].shared));
+    }
+    cur_ = out;
+    ++steps_done_;
+}
+
+void DenseEngine::fork_multi() {
+    VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
+}
+
+void DenseEngine::join_multi() {
+    // the engine stream waits for the last step's two streams of every partition
+    const int last = (steps_done_ - 1) & 1;
+    for (auto& x : px_) {
+        VOXL_CUDA(cudaStreamWaitEvent(stream_, x.ev_i[last], 0));
+        VOXL_CUDA(cudaStreamWaitEvent(stream_, x.ev_s[last], 0));
+    }
+}
+
+void DenseEngine::capture_graph(int parity) {
+    // fork -> graph_steps steps -> join -> step counter += graph_steps, captured
+    // from the engine stream; cross-device waits become graph edges. The host
+    // bookkeeping (parity, step count) advances during capture and is rolled
+    // back: replaying the graph advances it.
+    const int saved_cur = cur_, saved_steps = steps_done_;
+    cur_ = parity;
+    steps_done_ = parity;  // event parity follows the step count
+    cudaGraph_t graph = nullptr;
+    VOXL_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeRelaxed));
+    try {
+        fork_multi();
+        for (int s = 0; s < cfg_.graph_steps; ++s) launch_step_multi(s, s == 0, nullptr, true);
+        join_multi();
+        advance_step_kernel<<<1, 1, 0, stream_>>>(step_base_, cfg_.graph_steps);
+        VOXL_CUDA(cudaGetLastError());
+    } catch (...) {
+        cudaStreamEndCapture(stream_, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        cur_ = saved_cur;
+        steps_done_ = saved_steps;
+        throw;
+    }
+    VOXL_CUDA(cudaStreamEndCapture(stream_, &graph));
+    cur_ = saved_cur;
+    steps_done_ = saved_steps;
+    const cudaError_t e = cudaGraphInstantiate(&graph_[parity], graph, 0);
+    cudaGraphDestroy(graph);
+    VOXL_CUDA(e);
+}
+
+void DenseEngine::enqueue_multi(int n, const DiagTarget* dev_diag, bool use_graph) {
+    if (n <= 0) return;
+    int done = 0;
+    const int G = cfg_.graph_steps;
+    if (use_graph && !dev_diag && !nccl_ && G > 0 && n >= G) {
+        // the graph's kernels report a failing step as *step_base + offset
+        const int base = steps_done_;
+        VOXL_CUDA(cudaMemcpyAsync(step_base_, &base, sizeof(int), cudaMemcpyHostToDevice, stream_));
+        VOXL_CUDA(cudaStreamSynchronize(stream_));  // `base` is a stack value
+        while (n - done >= G) {
+            if (!graph_[cur_]) {
+                try {
+                    capture_graph(cur_);
+                } catch (const CudaError& e) {
+                    // a driver that cannot capture this schedule (e.g. across
+                    // devices) keeps the same launches issued from the host
+                    graph_note_ = e.what();
+                    cfg_.graph_steps = 0;
+                    cudaGetLastError();
+                    break;
+                }
+            }
+            VOXL_CUDA(cudaGraphLaunch(graph_[cur_], stream_));
+            steps_done_ += G;  // G is even: the parity is unchanged
+            done += G;
+        }
+    }
+    if (done == n) return;
+    fork_multi();
+    for (int s = done; s < n; ++s) launch_step_multi(s - done, s == done, nullptr, false);
+    join_multi();
+}
+
 double DenseEngine::timed_steps(int n, double* kernel_ms) {
+    if (multi_) {
+        // one event pair on the engine stream around the whole fork -> steps ->
+        // join batch (the partitions' streams overlap inside it)
+        check_links();
+        cudaEvent_t e0, e1;
+        VOXL_CUDA(cudaEventCreate(&e0));
+        VOXL_CUDA(cudaEventCreate(&e1));
+        VOXL_CUDA(cudaEventRecord(e0, stream_));
+        enqueue_multi(n, nullptr, true);
+        VOXL_CUDA(cudaEventRecord(e1, stream_));
+        VOXL_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        VOXL_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (kernel_ms) *kernel_ms = ms;
+        check_errors();
+        return ms;
+    }
     // CUDA events on the launching stream: one pair around each step (the
     // step's kernels), plus the span from the first to the last event.
     std::vector<cudaEvent_t> ev(2 * std::size_t(n));
@@ -1304,6 +1708,8 @@ int DenseEngine::step_probe_n(int n, DenseDiag* rows, std::string* abort_msg) {
     // with probe_field fused (accumulating into the step's ring slot); one
     // reduction kernel, one copy and one host synchronisation per batch.
     if (n < 0) throw std::invalid_argument("step_probe: n must be >= 0");
+    check_links();
+    if (multi_) return step_probe_n_multi(n, rows, abort_msg);
     if (!ring_) ring_ = std::make_unique<DiagRing>();
     int done = 0;
     while (done < n) {
@@ -1338,6 +1744,75 @@ int DenseEngine::step_probe_n(int n, DenseDiag* rows, std::string* abort_msg) {
         if (fail >= 0) {
             if (abort_msg) *abort_msg = msg;
             last_bad_ = r[fail].bad;
+            return done;
+        }
+    }
+    return done;
+}
+
+int DenseEngine::step_probe_n_multi(int n, DenseDiag* rows, std::string* abort_msg) {
+    // As step_probe_n, with one accumulator ring per device: each device's
+    // kernels commit into their own ring (no cross-device atomics), and the
+    // exact integer sums of the rings add up on the host before the single
+    // rounding to fp64 -- the same row bit for bit as one device would give.
+    for (auto& d : dx_)
+        if (!d.ring) {
+            DeviceGuard g(d.device);
+            d.ring = std::make_unique<DiagRing>();
+        }
+    std::vector<DiagTarget> dt(dx_.size());
+    std::vector<DiagRaw> raw;
+    int done = 0;
+    while (done < n) {
+        const int b = std::min(n - done, kDiagBatch);
+        const int step0 = steps_done_;
+        fork_multi();
+        for (auto& d : dx_) {
+            DeviceGuard g(d.device);
+            if (d.aux != stream_) VOXL_CUDA(cudaStreamWaitEvent(d.aux, ev_fork_, 0));
+            d.ring->begin(b, d.aux);
+            VOXL_CUDA(cudaEventRecord(d.ev, d.aux));
+        }
+        for (int s = 0; s < b; ++s) {
+            for (std::size_t i = 0; i < dx_.size(); ++i) {
+                dt[i].acc = dx_[i].ring->acc(s);
+                dt[i].bad = dx_[i].ring->bad(s);
+            }
+            launch_step_multi(s, s == 0, dt.data(), false);
+        }
+        const int last = (steps_done_ - 1) & 1;
+        for (std::size_t i = 0; i < dx_.size(); ++i) {
+            DevExec& d = dx_[i];
+            DeviceGuard g(d.device);
+            for (int p = 0; p < cfg_.partitions; ++p) {
+                if (parts_[p].device != d.device) continue;
+                VOXL_CUDA(cudaStreamWaitEvent(d.aux, px_[std::size_t(p)].ev_i[last], 0));
+                VOXL_CUDA(cudaStreamWaitEvent(d.aux, px_[std::size_t(p)].ev_s[last], 0));
+            }
+            d.ring->reduce(i == 0 ? error_flag_ : nullptr, d.aux);
+            VOXL_CUDA(cudaEventRecord(d.ev, d.aux));
+            if (i > 0) VOXL_CUDA(cudaStreamWaitEvent(stream_, d.ev, 0));
+        }
+        join_multi();
+        for (auto& d : dx_) VOXL_CUDA(cudaStreamSynchronize(d.aux));
+        raw.assign(dx_[0].ring->raw(), dx_[0].ring->raw() + b);
+        for (std::size_t i = 1; i < dx_.size(); ++i)
+            for (int s = 0; s < b; ++s) diag_accumulate(raw[std::size_t(s)], dx_[i].ring->raw()[s]);
+        std::vector<DiagRow> r(static_cast<std::size_t>(b));
+        for (int s = 0; s < b; ++s) r[std::size_t(s)] = diag_compose(raw[std::size_t(s)]);
+        std::string msg;
+        const int fail = first_failure(r.data(), b, step0, dx_[0].ring->error_flag(), &msg);
+        const int good = fail < 0 ? b : fail;
+        for (int s = 0; s < good; ++s) {
+            DenseDiag& d = rows[done + s];
+            d = DenseDiag{};
+            d.mass = r[std::size_t(s)].mass;
+            d.max_speed = std::sqrt(r[std::size_t(s)].v2);
+        }
+        done += good;
+        if (fail >= 0) {
+            if (abort_msg) *abort_msg = msg;
+            last_bad_ = r[std::size_t(fail)].bad;
             return done;
         }
     }
@@ -1391,6 +1866,12 @@ DenseDiag DenseEngine::probe() {
     return d;
 }
 
-std::vector<TransferRecord> DenseEngine::ledger_records(int step) const { return halo_records(decomp_, maps_, step); }
+std::vector<TransferRecord> DenseEngine::ledger_records(int step) const {
+    // the decomposition's records, less the links a caller cut (set_neighbor_links)
+    std::vector<TransferRecord> out;
+    for (const auto& r : halo_records(decomp_, maps_, step))
+        if (links_[std::size_t(r.src)].first == r.dst || links_[std::size_t(r.src)].second == r.dst) out.push_back(r);
+    return out;
+}
 
 } // namespace voxl_b200

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -29,7 +30,12 @@ class DiagRing;
 
 struct DiagTarget;
 enum class Precision : int { F32 = 0, F64 = 1 };
-enum class HaloMode : int { ZeroCopy = 0, Copy = 1 };
+/// ZeroCopy: the shared-layer kernel stores the crossing populations into the
+/// neighbour's halo (peer memory). Copy: span copies after the shared layers
+/// (halo_update's copies, device to device). Nccl: the same spans moved by
+/// grouped ncclSend/ncclRecv (multi-device engines with one device per
+/// partition; the measured comparison of the paper's zero-copy scheme).
+enum class HaloMode : int { ZeroCopy = 0, Copy = 1, Nccl = 2 };
 enum class Scenario : int { LidDrivenCavity = 0, FlowOverObstacle = 1, PeriodicBox = 2 };
 
 /// The closed operator set behind the step_occ plugin point
@@ -55,6 +61,15 @@ struct DenseConfig {
     int first_partition = 0;
     int local_partitions = -1;
     Operator op = Operator::Lbm;
+    // Single-process multi-device placement: partition p lives on devices[p]
+    // (the reference's in-process PartitionedField, partition.hpp:92-126, over
+    // several GPUs). Empty: every partition on the current device, launched
+    // back to back on one stream. Non-empty (even all equal): the two-stream
+    // OCC schedule per partition with cross-device event ordering.
+    std::vector<int> devices;
+    // Multi-device engines: steps per captured CUDA graph (even, 0 = launch
+    // every step from the host).
+    int graph_steps = 8;
 };
 
 /// Field geometry an operator implies: cardinality, partition axis and the
@@ -159,6 +174,16 @@ public:
     /// Push this engine's shared slabs into the neighbours' halos (peer
     /// copies), for a canonical state loaded in multi-process mode.
     void halo_push();
+    /// PartitionedField::neighbors / set_neighbor_links (partition.hpp:110-113):
+    /// (upper, lower) neighbour of partition p. Links are derived from the
+    /// decomposition; the setter is the reference's fault-injection hook, and
+    /// a step on asymmetric links throws "halo_update: asymmetric neighbor
+    /// links" (partition.cpp:165-171).
+    std::pair<int, int> neighbors(int p) const { return links_.at(std::size_t(p)); }
+    void set_neighbor_links(int p, int upper, int lower);
+    /// Device of partition p.
+    int device_of(int p) const { return parts_.at(std::size_t(p)).device; }
+    bool multi_device() const { return multi_; }
 
 private:
     DenseConfig cfg_;
@@ -196,6 +221,39 @@ private:
     cudaEvent_t ev_fork_ = nullptr;
     bool occ_ready_ = false;
     void join_streams();
+
+    // single-process multi-device schedule (launch_step_multi)
+    struct PartExec {
+        cudaStream_t interior = nullptr;  // planes 1 .. n-2
+        cudaStream_t shared = nullptr;    // planes 0, n-1 + halo transfer (high priority)
+        cudaEvent_t ev_i[2] = {nullptr, nullptr};
+        cudaEvent_t ev_s[2] = {nullptr, nullptr};
+        cudaEvent_t ev_ready = nullptr;   // batch start (fork) on this partition's device
+    };
+    struct DevExec {
+        int device = 0;
+        cudaStream_t aux = nullptr;  // fork / join / diagnostics of this device
+        cudaEvent_t ev = nullptr;
+        std::unique_ptr<DiagRing> ring;
+    };
+    bool multi_ = false;
+    std::vector<PartExec> px_;
+    std::vector<DevExec> dx_;  // distinct devices, dx_[0] = the engine stream's device
+    std::vector<std::pair<int, int>> links_;
+    struct NcclHalo;
+    std::unique_ptr<NcclHalo> nccl_;
+    int* step_base_ = nullptr;  // graph replays: device-side step counter for the error flag
+    cudaGraphExec_t graph_[2] = {nullptr, nullptr};  // per starting parity
+    int dev_index(int device) const;
+    void setup_multi();
+    void check_links() const;
+    std::string graph_note_;  // why graph replay was turned off, if it was
+    void enqueue_multi(int n, const DiagTarget* dev_diag, bool use_graph);
+    void launch_step_multi(int step_off, bool first, const DiagTarget* dev_diag, bool capturing);
+    void fork_multi();
+    void join_multi();
+    void capture_graph(int parity);
+    int step_probe_n_multi(int n, DenseDiag* rows, std::string* abort_msg);
 
     bool local(int p) const {
         return p >= cfg_.first_partition && p < cfg_.first_partition + cfg_.local_partitions;

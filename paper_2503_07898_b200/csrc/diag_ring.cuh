@@ -17,14 +17,18 @@
 // ((canonical voxel << 5) | population, atomicMin: the reference's first
 // offender, voxel-major then population; population kBadDensity = 31 marks a
 // non-positive density, macroscopic's throw). One kernel reduces a whole batch
-// into 32-byte rows, one copy brings them and the engine's error flag home.
+// into 32-byte exact sums, one copy brings them and the engine's error flag
+// home; the host rounds each sum to fp64 once (diag_compose), after adding the
+// sums of every device a multi-device step ran on.
 #pragma once
 
 #include "common.cuh"
 #include "lattice.cuh"
 
 #include <climits>
+#include <cstring>
 #include <string>
+#include <vector>
 
 namespace voxl_b200 {
 
@@ -58,9 +62,17 @@ __device__ __forceinline__ void diag_commit(unsigned long long* acc, unsigned lo
     if (v2 > 0.0) atomicMax(w + 3, (unsigned long long)__double_as_longlong(v2));
 }
 
-/// One CTA per step: exact integer sums over the lanes, composed once into fp64.
+/// A step's exact sums: mass as a 128-bit two's-complement fixed-point number
+/// (64 fraction bits), max |u|^2 as fp64 bits, the first-offender word.
+/// Raw sums from several rings (one per device) add as integers, so a step
+/// split over devices composes to the same row bit for bit.
+struct DiagRaw {
+    unsigned long long lo, hi, vmax, bad;
+};
+
+/// One CTA per step: exact integer sums over the lanes.
 __global__ void __launch_bounds__(256) diag_rows_kernel(const unsigned long long* acc, const unsigned long long* bad,
-                                                        DiagRow* rows) {
+                                                        DiagRaw* rows) {
     const unsigned long long* a = acc + (long long)blockIdx.x * kDiagLanes * kDiagWords;
     unsigned long long w0 = 0, w1 = 0, w2 = 0, vm = 0;
     for (int l = threadIdx.x; l < kDiagLanes; l += 256) {
@@ -88,14 +100,34 @@ __global__ void __launch_bounds__(256) diag_rows_kernel(const unsigned long long
         // T = w2 * 2^64 + w1 * 2^32 + w0 (two's complement, 64 fraction bits)
         const unsigned long long x0 = s0[0], x1 = s1[0];
         const unsigned long long lo = x0 + (x1 << 32);
-        const unsigned long long hi = s2[0] + (x1 >> 32) + (lo < x0 ? 1ull : 0ull);
-        DiagRow r;
-        r.mass = double((long long)hi) + double(lo) * 0x1p-64;
-        r.v2 = __longlong_as_double((long long)sv[0]);
+        DiagRaw r;
+        r.lo = lo;
+        r.hi = s2[0] + (x1 >> 32) + (lo < x0 ? 1ull : 0ull);
+        r.vmax = sv[0];
         r.bad = bad[blockIdx.x];
-        r.pad = 0;
         rows[blockIdx.x] = r;
     }
+}
+
+/// Sum of two rings' raw rows (mod 2^128 fixed point, max, min).
+inline void diag_accumulate(DiagRaw& into, const DiagRaw& x) {
+    const unsigned long long lo = into.lo + x.lo;
+    into.hi += x.hi + (lo < x.lo ? 1ull : 0ull);
+    into.lo = lo;
+    into.vmax = into.vmax > x.vmax ? into.vmax : x.vmax;
+    into.bad = into.bad < x.bad ? into.bad : x.bad;
+}
+
+/// The row of a raw sum: one rounding of the exact fixed-point mass to fp64.
+inline DiagRow diag_compose(const DiagRaw& r) {
+    DiagRow row;
+    row.mass = double((long long)r.hi) + double(r.lo) * 0x1p-64;
+    double v2;
+    std::memcpy(&v2, &r.vmax, sizeof v2);
+    row.v2 = v2;
+    row.bad = r.bad;
+    row.pad = 0;
+    return row;
 }
 
 /// Device accumulators + pinned rows of up to kDiagBatch probed steps.
@@ -107,7 +139,7 @@ public:
     ~DiagRing() {
         if (acc_) cudaFree(acc_);
         if (bad_) cudaFree(bad_);
-        if (rows_) cudaFree(rows_);
+        if (raw_) cudaFree(raw_);
         if (host_) cudaFreeHost(host_);
     }
 
@@ -117,8 +149,8 @@ public:
         if (!acc_) {
             VOXL_CUDA(cudaMalloc(&acc_, std::size_t(kDiagBatch) * kDiagLanes * kDiagWords * 8));
             VOXL_CUDA(cudaMalloc(&bad_, std::size_t(kDiagBatch) * 8));
-            VOXL_CUDA(cudaMalloc(&rows_, std::size_t(kDiagBatch) * sizeof(DiagRow)));
-            VOXL_CUDA(cudaMallocHost(&host_, std::size_t(kDiagBatch) * sizeof(DiagRow) + 16));
+            VOXL_CUDA(cudaMalloc(&raw_, std::size_t(kDiagBatch) * sizeof(DiagRaw)));
+            VOXL_CUDA(cudaMallocHost(&host_, std::size_t(kDiagBatch) * sizeof(DiagRaw) + 16));
         }
         VOXL_CUDA(cudaMemsetAsync(acc_, 0, std::size_t(n) * kDiagLanes * kDiagWords * 8, st));
         VOXL_CUDA(cudaMemsetAsync(bad_, 0xFF, std::size_t(n) * 8, st));
@@ -130,24 +162,31 @@ public:
     /// Enqueue the batch's reduction and the read-back of the rows and of
     /// `error_flag` (the engine's first non-positive-density step) on `st`.
     void reduce(const int* error_flag, cudaStream_t st) {
-        diag_rows_kernel<<<n_, 256, 0, st>>>(acc_, bad_, rows_);
+        diag_rows_kernel<<<n_, 256, 0, st>>>(acc_, bad_, raw_);
         VOXL_CUDA(cudaGetLastError());
-        VOXL_CUDA(cudaMemcpyAsync(host_, rows_, std::size_t(n_) * sizeof(DiagRow), cudaMemcpyDeviceToHost, st));
+        VOXL_CUDA(cudaMemcpyAsync(host_, raw_, std::size_t(n_) * sizeof(DiagRaw), cudaMemcpyDeviceToHost, st));
         if (error_flag)
             VOXL_CUDA(cudaMemcpyAsync(flag_slot(), error_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
         else
             *flag_slot() = INT_MAX;
     }
-    /// After the stream synchronised: the rows and the error flag.
-    const DiagRow* rows() const { return host_; }
+    /// After the stream synchronised: the raw sums and the error flag.
+    const DiagRaw* raw() const { return host_; }
+    /// The composed rows of this ring alone.
+    const DiagRow* rows() {
+        rows_.resize(std::size_t(n_));
+        for (int s = 0; s < n_; ++s) rows_[std::size_t(s)] = diag_compose(host_[s]);
+        return rows_.data();
+    }
     int error_flag() const { return *flag_slot(); }
 
 private:
     int* flag_slot() const { return reinterpret_cast<int*>(host_ + kDiagBatch); }
     unsigned long long* acc_ = nullptr;
     unsigned long long* bad_ = nullptr;
-    DiagRow* rows_ = nullptr;
-    DiagRow* host_ = nullptr;
+    DiagRaw* raw_ = nullptr;
+    DiagRaw* host_ = nullptr;
+    std::vector<DiagRow> rows_;
     int n_ = 0;
 };
 

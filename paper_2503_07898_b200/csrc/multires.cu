@@ -1000,7 +1000,7 @@ void MultiResEngine::launch_stream(int l, bool jump_only, cudaStream_t s) {
         using R = decltype(real);
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
-        auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+        auto A = level_args<L, R, X>(cfg_, V, cfg_.fused ? ahead_step_ : steps_done_, d_error_);
         if (cfg_.fused) {  // post -> nxt, and BGK(nxt) -> the other post buffer
             A.post_ahead = static_cast<R*>(V->post[V->parity ^ 1]);
             launch_pull<L, R, X, E, kStreamAhead>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st);
@@ -1075,7 +1075,7 @@ void MultiResEngine::launch_fused(int l) {
         using R = decltype(real);
         constexpr bool X = decltype(exact)::value;
         constexpr int E = decltype(e)::value;
-        auto A = level_args<L, R, X>(cfg_, V, steps_done_, d_error_);
+        auto A = level_args<L, R, X>(cfg_, V, ahead_step_, d_error_);  // the collision is the next sub-step's
         A.nxt = static_cast<R*>(V->post[V->parity ^ 1]);  // post[p] -> post[p^1]
         launch_pull<L, R, X, E, kFused>(A, 0, V->n_uni, V->n_plain, stream_);
     });
@@ -1148,6 +1148,11 @@ void MultiResEngine::advance(int l) {
     // the side stream in order with the jump-block streams, and the long
     // fused uniform kernels on the engine stream never wait for them.
     if (!cfg_.fused) launch_collide(l, false);
+    if (sub_.size() != lv_.size()) sub_.assign(lv_.size(), 0);
+    const int per = 1 << (int(lv_.size()) - 1 - l);  // advance(l) calls per coarse step
+    const int sub = sub_[std::size_t(l)];
+    sub_[std::size_t(l)] = sub + 1 == per ? 0 : sub + 1;
+    const int ahead = steps_done_ + (sub + 1 == per ? 1 : 0);
     if (l > 0) {
         if (side_transitions_) {
             VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
@@ -1165,6 +1170,7 @@ void MultiResEngine::advance(int l) {
         launch_coalesce(l, side_transitions_ ? side_ : stream_);
     }
     Level* V = lv_[l];
+    ahead_step_ = ahead;
     if (cfg_.fused && V->n_uni > 0 && V->n_jump > 0) {
         // jump stream (side stream, high priority) || fused uniform (engine stream)
         VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
@@ -1190,7 +1196,9 @@ void MultiResEngine::check_errors() {
     int flag = INT_MAX;
     VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     VOXL_CUDA(cudaStreamSynchronize(stream_));
-    if (flag != INT_MAX)
+    // flag == steps_done_: a collide-ahead of a step that has not run yet
+    // (fused mode); it throws once that step has run, as the reference would
+    if (flag < steps_done_)
         throw InstabilityError("run aborted at step " + std::to_string(flag) + ": macroscopic: non-positive density");
 }
 

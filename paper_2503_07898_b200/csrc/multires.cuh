@@ -98,6 +98,13 @@ private:
     std::size_t probe_scratch_len_ = 0;
     std::size_t diag_len_ = 0;
     int steps_done_ = 0;
+    // Fused mode collides ahead: the fused uniform kernel and the jump-block
+    // stream compute the NEXT sub-step's collide_level of their blocks. A
+    // non-positive density found there belongs to that sub-step, which is the
+    // next coarse step after a level's last sub-step of this one (sub_[l]
+    // counts the level's sub-steps within the coarse step).
+    std::vector<int> sub_;
+    int ahead_step_ = 0;
     // timing (events around each launch class) when non-null
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* events_ = nullptr;
 

@@ -22,7 +22,7 @@ Q_OF = {"D2Q9": 9, "D3Q19": 19, "D3Q27": 27}
 LAYOUTS = {"AoS": 0, "SoA": 1, "DisagSoA": 2}
 SCENARIOS = {"lid_driven_cavity": 0, "flow_over_obstacle": 1, "periodic_box": 2}
 PRECISIONS = {"fp32": 0, "fp64": 1}
-HALO_MODES = {"zero_copy": 0, "copy": 1}
+HALO_MODES = {"zero_copy": 0, "copy": 1, "nccl": 2}
 # closed step_occ operator set (partition.hpp:173): the LBM GatherKernel and the
 # reference tests' identity / five-point Jacobi kernels (partition_test.cpp:189, :234)
 OPERATORS = {"lbm": 0, "identity": 1, "jacobi2": 2}
@@ -124,7 +124,11 @@ class DenseEngine:
 
     def __init__(self, lattice="D3Q19", domain=(32, 32, 32), tau=0.56, scenario="lid_driven_cavity",
                  velocity=(0.05, 0.0, 0.0), layout="DisagSoA", partitions=1, precision="fp32",
-                 halo_mode="zero_copy", first_partition=0, local_partitions=-1, op="lbm"):
+                 halo_mode="zero_copy", first_partition=0, local_partitions=-1, op="lbm", devices=None,
+                 graph_steps=8):
+        """``devices``: one CUDA device per partition (the single-process
+        multi-device engine, voxl_dense_create_multi); None keeps every
+        partition on the current device, launched back to back on one stream."""
         d = make_desc(lattice, domain, tau, scenario, velocity, layout, partitions, precision, halo_mode,
                       first_partition, local_partitions, op)
         dom = (d.nx, d.ny, d.nz)
@@ -134,7 +138,13 @@ class DenseEngine:
         self.domain = dom
         self.partitions = partitions
         self._h = C.c_void_p()
-        check(lib.voxl_dense_create(C.byref(d), C.byref(self._h)))
+        if devices is None:
+            check(lib.voxl_dense_create(C.byref(d), C.byref(self._h)))
+        else:
+            devs = (C.c_int * max(partitions, 1))(*[int(x) for x in devices])
+            if len(devices) != partitions:
+                raise ValueError("devices must name one device per partition")
+            check(lib.voxl_dense_create_multi(C.byref(d), devs, graph_steps, C.byref(self._h)))
 
     @property
     def voxels(self) -> int:
@@ -243,6 +253,21 @@ class DenseEngine:
 
     def attach_peer(self, partition: int, buf0: int, buf1: int) -> None:
         check(lib.voxl_dense_attach_peer(self._h, partition, C.c_void_p(buf0), C.c_void_p(buf1)))
+
+    def device(self, partition: int) -> int:
+        d = C.c_int()
+        check(lib.voxl_dense_device(self._h, partition, C.byref(d)))
+        return d.value
+
+    def neighbors(self, partition: int):
+        """PartitionedField::neighbors (partition.hpp:110): (upper, lower)."""
+        u, lo = C.c_int(), C.c_int()
+        check(lib.voxl_dense_neighbors(self._h, partition, C.byref(u), C.byref(lo)))
+        return u.value, lo.value
+
+    def set_neighbor_links(self, partition: int, upper: int, lower: int) -> None:
+        """The reference's fault-injection hook (partition.hpp:111-113)."""
+        check(lib.voxl_dense_set_neighbor_links(self._h, partition, upper, lower))
 
     def close(self) -> None:
         if self._h:

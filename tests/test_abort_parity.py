@@ -7,7 +7,14 @@ canonical state, and on the first failure throws
 macroscopic's "macroscopic: non-positive density" (lattice.cpp:124). A large
 population injected into the initial state drives both kinds; the B200 engines
 must name the same step, voxel and population, and the rows before the
-failure must agree (1e-12 relative).
+failure must agree: max |u| to 1e-12 relative, the mass to the reference's own
+rounding bound. probe_field sums every population into one fp64 accumulator in
+canonical order (lbm.cpp:116-123); recursive summation of n positive terms is
+off the exact sum by up to (n - 1) * 2^-53 * sum (Higham, Accuracy and Stability
+of Numerical Algorithms, eq. 4.4), and it is biased when many equal terms (the
+rest state) are added to a large partial sum -- which the injected populations
+make larger. The B200 rows are exact sums of the per-cell moments rounded to
+2^-64 (diag_ring.cuh).
 """
 import numpy as np
 import pytest
@@ -25,10 +32,11 @@ INJECT_DENSE = [((3 * 64 + 2 * 8 + 1) * 19 + 0, 1e4), ((3 * 64 + 2 * 8 + 1) * 19
                 ((2 * 64 + 2 * 8 + 2) * 19 + 7, -5.0)]
 
 
-def _rows_close(ours, ref):
+def _rows_close(ours, ref, n_terms):
     assert len(ours) == len(ref)
+    tol = max(1e-12, n_terms * 2.0 ** -53)
     for (m, u), (rm, ru) in zip(ours, ref):
-        assert abs(m - rm) <= 1e-12 * abs(rm)
+        assert abs(m - rm) <= tol * abs(rm)
         assert abs(u - ru) <= 1e-12 * max(abs(ru), 1e-300)
 
 
@@ -65,7 +73,7 @@ def test_dense_abort_text_equals_reference(elem, value, parts, layout):
     with pytest.raises(V.VoxlInstability) as info:
         e.step_probe_n(20)
     assert str(info.value) == ref_msg
-    _rows_close([(d.mass, d.max_speed) for d in info.value.rows], ref_rows)
+    _rows_close([(d.mass, d.max_speed) for d in info.value.rows], ref_rows, st.size)
     e.close()
     # one step at a time (run()'s per-step shape)
     e = V.DenseEngine(domain=(8, 8, 8), precision="fp64", partitions=parts, layout=layout)
@@ -73,7 +81,7 @@ def test_dense_abort_text_equals_reference(elem, value, parts, layout):
     rows, msg = _ours_loop(e.step_probe, None, 20)
     e.close()
     assert msg == ref_msg
-    _rows_close(rows, ref_rows)
+    _rows_close(rows, ref_rows, st.size)
 
 
 @pytest.mark.gpu
@@ -96,13 +104,13 @@ def test_sparse_abort_text_equals_reference(elem, value, strategy, edge):
     rows, msg = _ours_loop(e.step_probe, None, 10)
     e.close()
     assert msg == ref_msg
-    _rows_close(rows, ref_rows)
+    _rows_close(rows, ref_rows, st.size)
 
 
 @pytest.mark.gpu
 @needs_ref
 @pytest.mark.parametrize("elem,value", [(100 * 19 + 0, 1e4), (300 * 19 + 5, 1e4), (50 * 19, 3000.0),
-                                        (40000 * 19 + 2, 1e4)])
+                                        (2100 * 19 + 2, 1e4)])  # 2100: a coarse (level-1) cell
 @pytest.mark.parametrize("fused", [True, False])
 def test_multires_abort_text_equals_reference(elem, value, fused):
     dom = (16, 16, 16)
@@ -119,4 +127,4 @@ def test_multires_abort_text_equals_reference(elem, value, fused):
     rows, msg = _ours_loop(lambda: e.step(1), e.probe, 10)
     e.close()
     assert msg == ref_msg
-    _rows_close(rows, ref_rows)
+    _rows_close(rows, ref_rows, st.size)

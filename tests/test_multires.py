@@ -363,15 +363,15 @@ def test_2d_multires_fp32_tolerance():
 # map has no solid cell.
 
 def _level_cells(domain, lm, levels):
-    """Per level: (x, y, z) of its cells in canonical_state order (pack_coord:
-    z, then y, then x)."""
+    """Per level: (x, y, z) of its cells in canonical_state order (sorted by
+    pack_coord, multires.cpp:578-597: x most significant, z fastest)."""
     nx, ny, nz = domain
     m = lm.reshape(nz, ny, nx)
     out = []
     for l in range(levels):
         s = 1 << l
-        sub = m[::s, ::s, ::s]
-        z, y, x = np.nonzero(sub == l)
+        sub = m[::s, ::s, ::s].transpose(2, 1, 0)  # [x, y, z]
+        x, y, z = np.nonzero(sub == l)
         out.append(np.stack([x, y, z], 1))
     return out
 

@@ -62,6 +62,8 @@ extern "C" {
 
 const char* voxl_last_error(void);
 int voxl_version(void);
+/** Visible CUDA devices (the multi-device engine places partitions on them). */
+int voxl_device_count(int* count);
 /** Lattice descriptor as the reference's lattice_to_json (lattice.cpp:140-158). */
 int voxl_lattice_json(int lattice, char* out, int64_t cap, int64_t* len);
 

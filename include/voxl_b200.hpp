@@ -21,7 +21,9 @@
 
 #include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -32,6 +34,11 @@ namespace voxl {
 namespace b200 {
 
 struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+/// ConfigError (solver.hpp:22-25): a configuration that fails validation.
+struct ConfigError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
@@ -56,6 +63,11 @@ struct Diagnostics {  // lbm::Diagnostics (lbm.hpp:137-141)
 class DenseEngine {
 public:
     explicit DenseEngine(const voxl_dense_desc& d) { check(voxl_dense_create(&d, &h_)); }
+    /// Partition p on devices[p] (voxl_dense_create_multi); empty = current device.
+    DenseEngine(const voxl_dense_desc& d, const std::vector<int>& devices, int graph_steps = 8) {
+        if (devices.empty()) check(voxl_dense_create(&d, &h_));
+        else check(voxl_dense_create_multi(&d, devices.data(), graph_steps, &h_));
+    }
     ~DenseEngine() { voxl_dense_destroy(h_); }
     DenseEngine(const DenseEngine&) = delete;
     DenseEngine& operator=(const DenseEngine&) = delete;
@@ -192,12 +204,61 @@ struct SolverConfig {
     double perturbation = 0.0;
     int precision = VOXL_F32;
     int block_edge = 8;
+    // Dense runs: device of partition p (the single-process multi-device
+    // engine). Empty: one partition per visible device when several are
+    // visible (round robin), else every partition on the current device.
+    std::vector<int> devices;
+    int halo_mode = VOXL_HALO_ZERO_COPY;
+    int graph_steps = 8;
 
     int dim() const { return lattice == VOXL_D2Q9 ? 2 : 3; }
     int partition_axis() const { return dim() == 2 ? 1 : 2; }
     std::int64_t volume() const { return std::int64_t(nx) * ny * nz; }
     int q() const { return lattice == VOXL_D2Q9 ? 9 : (lattice == VOXL_D3Q19 ? 19 : 27); }
+    int extent(int axis) const { return axis == 0 ? nx : (axis == 1 ? ny : nz); }
+
+    /// SolverConfig::validate (solver.cpp:27-60): same checks, same message
+    /// ("invalid configuration: " + every failed check), ConfigError.
+    void validate() const {
+        std::string err;
+        const double speed =
+            std::sqrt(velocity[0] * velocity[0] + velocity[1] * velocity[1] + velocity[2] * velocity[2]);
+        if (!(tau > 0.5)) err += "tau must be > 0.5; ";
+        if (speed > 0.1) err += "|velocity| must be <= 0.1 (stability envelope); ";
+        if (steps < 0) err += "steps must be >= 0; ";
+        if (nx < 2 || ny < 2) err += "domain extents must be >= 2; ";
+        if (dim() == 2 && nz != 1) err += "D2Q9 requires nz == 1; ";
+        if (dim() == 3 && nz < 2) err += "3D lattices require nz >= 2; ";
+        if (partitions < 1) err += "partitions must be >= 1; ";
+        if (partitions > 1 && extent(partition_axis()) < 2 * partitions)
+            err += "partition axis too small for the partition count; ";
+        if (levels < 1 || levels > 4) err += "levels must be in [1, 4]; ";
+        if (levels > 1 && scenario != VOXL_CAVITY)
+            err += "multi-level runs support the lid_driven_cavity scenario only; ";
+        if (levels > 1 && partitions > 1) err += "multi-level runs are single-partition; ";
+        if (levels > 1 && levels <= 4) {
+            const int scale = 1 << (levels - 1);
+            if (nx % scale || ny % scale || (dim() == 3 && nz % scale))
+                err += "domain extents must divide the coarsest cell size; ";
+        }
+        if (perturbation < 0.0 || perturbation > 0.5) err += "perturbation must be in [0, 0.5]; ";
+        if (scenario == VOXL_OBSTACLE) {
+            const int min_extent = std::min(nx, std::min(ny, nz));
+            const double r = obstacle_radius > 0.0 ? obstacle_radius : min_extent / 5.0;
+            if (2.0 * r >= min_extent - 4) err += "obstacle does not fit the domain; ";
+        }
+        if (!err.empty()) throw ConfigError("invalid configuration: " + err);
+    }
 };
+
+inline const char* lattice_name(int k) { return k == VOXL_D2Q9 ? "D2Q9" : (k == VOXL_D3Q19 ? "D3Q19" : "D3Q27"); }
+inline const char* layout_name(int s) { return s == VOXL_AOS ? "AoS" : (s == VOXL_SOA ? "SoA" : "DisagSoA"); }
+inline const char* strategy_name(int s) {
+    return s == VOXL_NAIVE ? "naive" : (s == VOXL_DISAG_BITMASK ? "disag_bitmask" : "disag_mem");
+}
+inline const char* scenario_name(int s) {
+    return s == VOXL_CAVITY ? "lid_driven_cavity" : (s == VOXL_OBSTACLE ? "flow_over_obstacle" : "periodic_box");
+}
 
 /// RunResult (solver.hpp:54-74).
 struct RunResult {
@@ -208,11 +269,50 @@ struct RunResult {
         double mass;
         double max_speed;
     };
+    std::string field_header_json;
     std::vector<DiagRow> diagnostics;
     std::vector<voxl_transfer_record> ledger;  // dense partitioned runs
+    struct TraceEvent {                        // TraceLog::Event (partition.hpp:79-84)
+        int step;
+        int stage;
+        std::string phase;
+        int partition;
+    };
+    std::vector<TraceEvent> trace;             // dense runs: the OCC schedule's logical order
     std::string dispatch_json;                 // sparse runs
     std::string graph_dot;                     // multires runs
     std::string distribution;                  // multires runs
+
+    /// RunResult::diagnostics_csv (solver.cpp:137-146).
+    std::string diagnostics_csv() const {
+        std::string out = "step,mass,max_u\n";
+        char buf[80];
+        for (const DiagRow& r : diagnostics) {
+            std::snprintf(buf, sizeof buf, "%d,%.17g,%.17g\n", r.step, r.mass, r.max_speed);
+            out += buf;
+        }
+        return out;
+    }
+    /// TransferLedger::to_csv (partition.cpp:90-97).
+    std::string ledger_csv() const {
+        std::string out = "step,src,dst,base_src,base_dst,elements\n";
+        for (const auto& r : ledger)
+            out += std::to_string(r.step) + "," + std::to_string(r.src) + "," + std::to_string(r.dst) + "," +
+                   std::to_string(r.src_base) + "," + std::to_string(r.dst_base) + "," + std::to_string(r.elements) +
+                   "\n";
+        return out;
+    }
+    /// TraceLog::to_json (partition.cpp:98-109).
+    std::string trace_json() const {
+        std::string out = "[\n";
+        for (std::size_t i = 0; i < trace.size(); ++i) {
+            const TraceEvent& e = trace[i];
+            out += "  {\"step\": " + std::to_string(e.step) + ", \"stage\": " + std::to_string(e.stage) +
+                   ", \"phase\": \"" + e.phase + "\", \"partition\": " + std::to_string(e.partition) + "}" +
+                   (i + 1 < trace.size() ? "," : "") + "\n";
+        }
+        return out + "]\n";
+    }
 };
 
 namespace detail {
@@ -252,11 +352,17 @@ inline RunResult run_dense(const SolverConfig& c) {
     d.layout = c.layout;
     d.partitions = c.partitions;
     d.precision = c.precision;
-    d.halo_mode = VOXL_HALO_ZERO_COPY;
+    d.halo_mode = c.halo_mode;
     d.first_partition = 0;
     d.local_partitions = -1;
     d.op = VOXL_OP_LBM;
-    DenseEngine e(d);
+    // the in-process PartitionedField over several GPUs (partition.hpp:92-126)
+    std::vector<int> devices = c.devices;
+    int visible = 1;
+    check(voxl_device_count(&visible));
+    if (devices.empty() && visible > 1 && c.partitions > 1)
+        for (int p = 0; p < c.partitions; ++p) devices.push_back(p % visible);
+    DenseEngine e(d, devices, c.graph_steps);
     std::vector<double> state(std::size_t(c.volume()) * c.q());
     check(voxl_initial_state(c.lattice, c.scenario, c.nx, c.ny, c.nz, c.seed, c.perturbation, state.data()));
     e.fill_canonical(state);
@@ -270,8 +376,20 @@ inline RunResult run_dense(const SolverConfig& c) {
         const auto recs = e.ledger(step);
         r.ledger.insert(r.ledger.end(), recs.begin(), recs.end());
     }
+    // step_occ's logical schedule per step (partition.hpp:186-213,
+    // partition.cpp:193): halo sends by partition, then private, then shared
+    for (int step = 0; step < done; ++step) {
+        for (int p = 0; p < c.partitions; ++p) r.trace.push_back({step, 1, "halo", p});
+        for (int p = 0; p < c.partitions; ++p) r.trace.push_back({step, 1, "private", p});
+        for (int p = 0; p < c.partitions; ++p) r.trace.push_back({step, 2, "shared", p});
+    }
     check(status);
     r.field = e.to_canonical(state.size());
+    r.field_header_json = "{\"shape\": [" + std::to_string(c.nx) + ", " + std::to_string(c.ny) + ", " +
+                          std::to_string(c.nz) + "], \"lattice\": \"" + lattice_name(c.lattice) +
+                          "\", \"representation\": \"dense\", \"layout\": \"" + layout_name(c.layout) +
+                          "\", \"cardinality\": " + std::to_string(c.q()) +
+                          ", \"order\": \"voxel-major (x fastest), component innermost\"}\n";
     return r;
 }
 
@@ -301,6 +419,12 @@ inline RunResult run_sparse(const SolverConfig& c) {
         r.diagnostics.push_back({step, g.mass, g.max_speed});
     }
     r.field = e.canonical_state(c.q());
+    r.field_header_json = "{\"shape\": [" + std::to_string(c.nx) + ", " + std::to_string(c.ny) + ", " +
+                          std::to_string(c.nz) + "], \"lattice\": \"" + lattice_name(c.lattice) +
+                          "\", \"representation\": \"block_sparse\", \"strategy\": \"" +
+                          strategy_name(c.strategy) + "\", \"cardinality\": " + std::to_string(c.q()) +
+                          ", \"active_voxels\": " + std::to_string(e.num_active()) +
+                          ", \"order\": \"active cells sorted by (z, y, x), component innermost\"}\n";
     voxl_sparse_desc d4 = d;
     d4.block_edge = 4;
     voxl_sparse_plan* plan = nullptr;
@@ -344,8 +468,35 @@ inline RunResult run_multires(const SolverConfig& c) {
         r.diagnostics.push_back({step, g.mass, g.max_speed});
     }
     r.field = e.canonical_state();
-    r.graph_dot = e.graph_dot();
-    r.distribution = e.distribution_report() + "\n";
+    // the execution graph and the distribution at the reference's block
+    // granularity (edge 4, multires.cpp:54-365), whatever edge the engine runs
+    voxl_mres_desc d4 = d;
+    d4.block_edge = 4;
+    d4.reference_tables = 1;
+    d4.precision = VOXL_F64;
+    voxl_mres_plan* plan = nullptr;
+    check(voxl_mres_plan_create(&d4, level_map.data(), &plan));
+    try {
+        std::int64_t n = 0;
+        for (int what : {c.fused ? 0 : 1, 2}) {
+            check(voxl_mres_plan_text(plan, what, nullptr, 0, &n));
+            std::string s(std::size_t(n) + 1, '\0');
+            check(voxl_mres_plan_text(plan, what, &s[0], n + 1, &n));
+            s.resize(std::size_t(n));
+            if (what == 2) r.distribution = s + "\n";
+            else r.graph_dot = s;
+        }
+    } catch (...) {
+        voxl_mres_plan_destroy(plan);
+        throw;
+    }
+    voxl_mres_plan_destroy(plan);
+    r.field_header_json = "{\"shape\": [" + std::to_string(c.nx) + ", " + std::to_string(c.ny) + ", " +
+                          std::to_string(c.nz) + "], \"lattice\": \"" + lattice_name(c.lattice) +
+                          "\", \"representation\": \"multires\", \"levels\": " + std::to_string(c.levels) +
+                          ", \"cardinality\": " + std::to_string(c.q()) +
+                          ", \"order\": \"levels finest to coarsest, cells sorted by (z, y, x), component "
+                          "innermost\"}\n";
     return r;
 }
 
@@ -354,6 +505,7 @@ inline RunResult run_multires(const SolverConfig& c) {
 /// run (solver.cpp:369-375): multires when levels > 1, block-sparse for flow
 /// over an obstacle, the partitioned dense engine otherwise.
 inline RunResult run(const SolverConfig& c) {
+    c.validate();
     if (c.levels > 1) return detail::run_multires(c);
     if (c.scenario == VOXL_OBSTACLE) return detail::run_sparse(c);
     return detail::run_dense(c);

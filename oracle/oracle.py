@@ -37,6 +37,21 @@ def build() -> None:
         subprocess.run(["make", "-s", "-C", HERE, "ref", "-j8"], check=True)
 
 
+def build_dropin() -> None:
+    """The drop-in test driver (reference run() vs voxl::b200::run on the
+    reference's types); needs the reference sources and the built libvoxl_b200."""
+    import subprocess
+
+    if os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-C", HERE, "dropin"], check=True)
+
+
+def dropin_driver():
+    """Path of the prebuilt drop-in driver, or None."""
+    p = os.path.join(REF_DIR, "dropin_reference")
+    return p if os.path.exists(p) else None
+
+
 _port = None
 _ref = None
 

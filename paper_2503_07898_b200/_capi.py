@@ -81,6 +81,7 @@ def _load():
     sigs = {
         "voxl_last_error": ([], cp),
         "voxl_version": ([], C.c_int),
+        "voxl_device_count": ([C.POINTER(C.c_int)], C.c_int),
         "voxl_lattice_json": ([C.c_int, cp, i64, C.POINTER(i64)], C.c_int),
         "voxl_layout_json": ([C.c_int] * 7 + [cp, i64, C.POINTER(i64)], C.c_int),
         "voxl_layout_addresses": ([C.c_int] * 6 + [vp, i64, C.POINTER(i64)], C.c_int),

@@ -46,6 +46,36 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+CLI = os.path.join(LIBDIR, "voxl_b200")
+
+
+def _json_include() -> str:
+    """nlohmann/json (3.11, header-only) as vendored by the image's cudnn
+    frontend -- the JSON library the reference's config parser uses."""
+    import site
+
+    for sp in site.getsitepackages() + [site.getusersitepackages()]:
+        d = os.path.join(sp, "include", "cudnn_frontend", "thirdparty", "nlohmann")
+        if os.path.exists(os.path.join(d, "json.hpp")):
+            return d
+    raise RuntimeError("nlohmann/json.hpp not found (cudnn_frontend thirdparty headers)")
+
+
+def build_cli() -> str:
+    """The C++ driver (csrc/cli/voxl_b200_main.cpp): `voxl_b200 run|verify`,
+    linked against the in-tree library with an $ORIGIN rpath."""
+    src = os.path.join(CSRC, "cli", "voxl_b200_main.cpp")
+    hdr = os.path.join(PKG, "..", "include", "voxl_b200.hpp")
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(x) for x in (src, hdr, LIB)):
+        return CLI
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I" + os.path.join(PKG, "..", "include"), "-I" + _json_include(),
+           src, "-L" + LIBDIR, "-lvoxl_b200", "-Wl,-rpath,$ORIGIN", "-o", CLI]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"voxl_b200 CLI build failed:\n{r.stderr}")
+    return CLI
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
@@ -56,6 +86,7 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    build_cli()
     return LIB
 
 

@@ -77,6 +77,13 @@ const char* voxl_last_error(void) { return g_last_error.c_str(); }
 
 int voxl_version(void) { return 1; }
 
+int voxl_device_count(int* count) {
+    return guarded([&] {
+        require(count != nullptr, "voxl_device_count: null argument");
+        VOXL_CUDA(cudaGetDeviceCount(count));
+    });
+}
+
 int voxl_lattice_json(int lattice, char* out, int64_t cap, int64_t* len) {
     return guarded([&] {
         require(lattice >= 0 && lattice <= 2, "unknown lattice kind");

@@ -43,3 +43,4 @@ def _built():
     import __graft_entry__
 
     __graft_entry__._load_builder().build()
+    oracle.build_dropin()

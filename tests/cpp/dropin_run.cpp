@@ -57,9 +57,17 @@ int main(int argc, char** argv) {
         m2.steps = 3;
         dump(prefix, "multires2d", voxl::b200::run(m2));
 
+        // a configuration that passes validate() and still blows up: the
+        // periodic box at tau -> 1/2 with the largest allowed perturbation
         voxl::b200::SolverConfig bad = c;
-        bad.velocity = {5.0, 0.0, 0.0};  // blows up within a few steps
-        bad.steps = 50;
+        bad.nx = bad.ny = bad.nz = 12;
+        bad.scenario = VOXL_PERIODIC;
+        bad.velocity = {0.0, 0.0, 0.0};
+        bad.tau = 0.5000001;
+        bad.perturbation = 0.5;
+        bad.seed = 3;
+        bad.partitions = 2;
+        bad.steps = 200;
         try {
             voxl::b200::run(bad);
             std::puts("unstable run did not abort");

@@ -267,6 +267,10 @@ int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out);
 /** One SparseLbmEngine::step with probe_field fused into the step kernels:
  *  run_sparse's per-step diagnostics row (solver.cpp:287-291). */
 int voxl_sparse_step_probe(voxl_sparse* h, voxl_diag* out);
+/** n x (step + probe_field), run_sparse's per-step loop (solver.cpp:287-291),
+ *  rows accumulated on the device (one host synchronisation per 256 steps).
+ *  Same contract as voxl_dense_step_probe_n. */
+int voxl_sparse_step_probe_n(voxl_sparse* h, int n, voxl_diag* rows, int* completed);
 /** dispatch_plan(...).to_json() (sparse.cpp:199-225; Table 2). */
 int voxl_dispatch_plan_json(int strategy, int64_t n_b, int64_t n_nb, int q, int block_size, int s_w, int s_i,
                             int naive_full_domain_storage, char* out, int64_t cap, int64_t* len);
@@ -311,6 +315,13 @@ int voxl_mres_digest(voxl_mres* h, uint64_t* out2);
 int voxl_mres_set_equilibrium(voxl_mres* h, double rho, const double* u);
 /** probe_field over canonical_state (solver.cpp:345). */
 int voxl_mres_probe(voxl_mres* h, voxl_diag* out);
+/** n x (coarse_step + probe_field), run_multires's per-step loop (solver.cpp:343-345),
+ *  with the probe fused into each level's last sub-step kernels and the rows
+ *  accumulated on the device (one host synchronisation per 256 steps). Same
+ *  contract as voxl_dense_step_probe_n: rows[s] = diagnostics of the s-th step;
+ *  VOXL_INSTABILITY with run()'s text at the first failing step, *completed =
+ *  the rows filled. */
+int voxl_mres_step_probe_n(voxl_mres* h, int n, voxl_diag* rows, int* completed);
 /** total_mass (multires.cpp:600-609): per-level sums weighted by 8^l. */
 int voxl_mres_total_mass(voxl_mres* h, double* mass);
 /** what: 0 = execution graph DOT, 1 = distribution report. */

@@ -317,16 +317,6 @@ struct RunResult {
 
 namespace detail {
 
-inline void abort_if_unstable(const voxl_diag& d, int step) {
-    if (!d.unstable) return;
-    const std::string head = "run aborted at step " + std::to_string(step) + ": ";
-    if (d.bad_population == VOXL_BAD_DENSITY)  // macroscopic's throw inside probe_field (lattice.cpp:124)
-        throw std::runtime_error(head + "macroscopic: non-positive density");
-    // probe_field's throw (lbm.cpp:124-128), rewrapped as run() does (solver.cpp:251-254)
-    throw std::runtime_error(head + "instability at step " + std::to_string(step) + ", voxel " +
-                             std::to_string(d.bad_voxel) + ", population " + std::to_string(d.bad_population));
-}
-
 inline std::string text_of(int (*get)(void*, char*, std::int64_t, std::int64_t*), void* h) {
     std::int64_t n = 0;
     check(get(h, nullptr, 0, &n));
@@ -412,12 +402,14 @@ inline RunResult run_sparse(const SolverConfig& c) {
     d.strategy = c.strategy;
     d.precision = c.precision;
     SparseLbmEngine e(d, mask);
-    for (int step = 0; step < c.steps; ++step) {
-        voxl_diag g{};
-        check(voxl_sparse_step_probe(e.handle(), &g));  // step + probe_field, fused on the device
-        abort_if_unstable(g, step);
-        r.diagnostics.push_back({step, g.mass, g.max_speed});
-    }
+    // step + probe_field per step, fused on the device; the rows come back
+    // once per batch and the first failing step aborts with run()'s text
+    std::vector<voxl_diag> rows(std::size_t(std::max(c.steps, 0)));
+    int done = 0;
+    const int status = voxl_sparse_step_probe_n(e.handle(), c.steps, rows.data(), &done);
+    for (int step = 0; step < done; ++step)
+        r.diagnostics.push_back({step, rows[std::size_t(step)].mass, rows[std::size_t(step)].max_speed});
+    check(status);
     r.field = e.canonical_state(c.q());
     r.field_header_json = "{\"shape\": [" + std::to_string(c.nx) + ", " + std::to_string(c.ny) + ", " +
                           std::to_string(c.nz) + "], \"lattice\": \"" + lattice_name(c.lattice) +
@@ -460,13 +452,14 @@ inline RunResult run_multires(const SolverConfig& c) {
     d.precision = c.precision;
     d.block_edge = c.block_edge;
     MultiResLbm e(d, level_map);
-    for (int step = 0; step < c.steps; ++step) {
-        e.coarse_step();
-        voxl_diag g{};
-        check(voxl_mres_probe(e.handle(), &g));
-        abort_if_unstable(g, step);
-        r.diagnostics.push_back({step, g.mass, g.max_speed});
-    }
+    // coarse_step + probe_field per step, the probe fused into each level's
+    // last sub-step; rows once per batch, run()'s text at the first failure
+    std::vector<voxl_diag> rows(std::size_t(std::max(c.steps, 0)));
+    int done = 0;
+    const int status = voxl_mres_step_probe_n(e.handle(), c.steps, rows.data(), &done);
+    for (int step = 0; step < done; ++step)
+        r.diagnostics.push_back({step, rows[std::size_t(step)].mass, rows[std::size_t(step)].max_speed});
+    check(status);
     r.field = e.canonical_state();
     // the execution graph and the distribution at the reference's block
     // granularity (edge 4, multires.cpp:54-365), whatever edge the engine runs

@@ -145,6 +145,7 @@ def _load():
                                      C.POINTER(C.c_double)], C.c_int),
         "voxl_sparse_probe": ([vp, C.POINTER(Diag)], C.c_int),
         "voxl_sparse_step_probe": ([vp, C.POINTER(Diag)], C.c_int),
+        "voxl_sparse_step_probe_n": ([vp, C.c_int, C.POINTER(Diag), C.POINTER(C.c_int)], C.c_int),
         "voxl_dispatch_plan_json": ([C.c_int, i64, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, cp, i64,
                                      C.POINTER(i64)], C.c_int),
         "voxl_band_level_map": ([C.c_int] * 5 + [vp], C.c_int),
@@ -159,6 +160,7 @@ def _load():
         "voxl_mres_set_state": ([vp, vp], C.c_int),
         "voxl_mres_set_equilibrium": ([vp, C.c_double, C.POINTER(C.c_double)], C.c_int),
         "voxl_mres_probe": ([vp, C.POINTER(Diag)], C.c_int),
+        "voxl_mres_step_probe_n": ([vp, C.c_int, C.POINTER(Diag), C.POINTER(C.c_int)], C.c_int),
         "voxl_mres_total_mass": ([vp, C.POINTER(C.c_double)], C.c_int),
         "voxl_mres_text": ([vp, C.c_int, cp, i64, C.POINTER(i64)], C.c_int),
         "voxl_mres_level_info": ([vp, C.c_int, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(i64),
@@ -192,6 +194,23 @@ def check(status: int) -> None:
     if status != OK:
         msg = lib.voxl_last_error().decode()
         raise _EXC.get(status, VoxlError)(msg)
+
+
+def probe_rows(fn, h, n: int):
+    """n probed steps through a voxl_*_step_probe_n entry point: the list of
+    diagnostics rows. On the first failing step raises VoxlInstability with
+    run()'s text; `.rows` holds the rows of the steps before it."""
+    rows = (Diag * max(n, 1))()
+    done = C.c_int()
+    st = fn(h, n, rows, C.byref(done))
+    out = [rows[i] for i in range(done.value)]
+    if st != OK:
+        try:
+            check(st)
+        except VoxlError as e:
+            e.rows = out
+            raise
+    return out
 
 
 def text(fn, *args) -> str:

@@ -328,6 +328,19 @@ int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out) {
     });
 }
 
+namespace {
+/// The healthy rows of a probed batch in the C-ABI's row type.
+void fill_rows(const DenseDiag* r, int done, voxl_diag* rows) {
+    for (int s = 0; s < done; ++s) {
+        rows[s] = voxl_diag{};
+        rows[s].mass = r[s].mass;
+        rows[s].max_speed = r[s].max_speed;
+        rows[s].bad_population = -1;
+        rows[s].bad_voxel = -1;
+    }
+}
+} // namespace
+
 int voxl_dense_step_probe_n(voxl_dense* h, int n, voxl_diag* rows, int* completed) {
     if (completed) *completed = 0;
     return guarded([&] {
@@ -336,13 +349,7 @@ int voxl_dense_step_probe_n(voxl_dense* h, int n, voxl_diag* rows, int* complete
         std::vector<DenseDiag> r(std::size_t(std::max(n, 0)));
         std::string msg;
         const int done = h->eng->step_probe_n(n, r.data(), &msg);
-        for (int s = 0; s < done; ++s) {
-            rows[s] = voxl_diag{};
-            rows[s].mass = r[s].mass;
-            rows[s].max_speed = r[s].max_speed;
-            rows[s].bad_population = -1;
-            rows[s].bad_voxel = -1;
-        }
+        fill_rows(r.data(), done, rows);
         if (completed) *completed = done;
         if (done < n) throw InstabilityError(msg);
     });
@@ -666,6 +673,20 @@ int voxl_sparse_probe(voxl_sparse* h, voxl_diag* out) {
     });
 }
 
+int voxl_sparse_step_probe_n(voxl_sparse* h, int n, voxl_diag* rows, int* completed) {
+    if (completed) *completed = 0;
+    return guarded([&] {
+        need("voxl_sparse_step_probe_n", h);
+        if (n > 0) need("voxl_sparse_step_probe_n", rows);
+        std::vector<DenseDiag> r(std::size_t(std::max(n, 0)));
+        std::string msg;
+        const int done = SP(h)->step_probe_n(n, r.data(), &msg);
+        fill_rows(r.data(), done, rows);
+        if (completed) *completed = done;
+        if (done < n) throw InstabilityError(msg);
+    });
+}
+
 int voxl_sparse_step_probe(voxl_sparse* h, voxl_diag* out) {
     return guarded([&] {
         need("voxl_sparse_step_probe", h, out);
@@ -840,6 +861,20 @@ int voxl_mres_probe(voxl_mres* h, voxl_diag* out) {
         out->unstable = d.unstable;
         out->bad_population = d.bad_population;
         out->bad_voxel = d.bad_voxel;
+    });
+}
+
+int voxl_mres_step_probe_n(voxl_mres* h, int n, voxl_diag* rows, int* completed) {
+    if (completed) *completed = 0;
+    return guarded([&] {
+        need("voxl_mres_step_probe_n", h);
+        if (n > 0) need("voxl_mres_step_probe_n", rows);
+        std::vector<DenseDiag> r(std::size_t(std::max(n, 0)));
+        std::string msg;
+        const int done = MR(h)->step_probe_n(n, r.data(), &msg);
+        fill_rows(r.data(), done, rows);
+        if (completed) *completed = done;
+        if (done < n) throw InstabilityError(msg);
     });
 }
 

@@ -26,12 +26,6 @@
 
 namespace voxl_b200 {
 
-/// Where a step launch writes its fused-probe partials.
-struct DiagTarget {
-    unsigned long long* acc = nullptr;  // the step's accumulator lanes (diag_ring.cuh)
-    unsigned long long* bad = nullptr;  // the step's first-offender word
-};
-
 namespace {
 
 #ifndef VOXL_DENSE_BLOCK

@@ -36,6 +36,12 @@ constexpr int kDiagLanes = 1024;  // power of two
 constexpr int kDiagWords = 4;     // fraction bits [0,32) | fraction bits [32,64) | integer part | max |u|^2 bits
 constexpr int kDiagBatch = 256;   // steps per read-back (8 MB of accumulators)
 
+/// Where a step launch writes its fused-probe terms.
+struct DiagTarget {
+    unsigned long long* acc = nullptr;  // the step's accumulator lanes
+    unsigned long long* bad = nullptr;  // the step's first-offender word
+};
+
 struct DiagRow {
     double mass;
     double v2;                // max |u|^2 (the host takes the square root)
@@ -43,23 +49,53 @@ struct DiagRow {
     long long pad;
 };
 
-__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+/// red.add with an L2 evict_last policy: the accumulator lines are hit by
+/// every CTA of the step while the step streams its whole state through L2;
+/// a normal-priority line gets evicted between hits, and each miss costs a
+/// DRAM fill plus a write-back (ncu: 5.5 M missed red sectors, +0.2 GB of
+/// DRAM writes per 512^3 step with one reduction per warp).
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v, unsigned long long pol) {
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+/// A warp partial as accumulator words: fraction bits [0,32), fraction bits
+/// [32,64), integer part (two's complement), max |u|^2 as fp64 bits. A
+/// non-finite partial contributes nothing (its bad voxel is reported by the
+/// step's bad word).
+__device__ __forceinline__ void diag_words(double mass, double v2, unsigned long long (&w)[kDiagWords]) {
+    w[0] = w[1] = w[2] = 0;
+    if (fabs(mass) < 4.0e18) {
+        const double ip = floor(mass);
+        const unsigned long long frac = (unsigned long long)((mass - ip) * 18446744073709551616.0);
+        w[0] = frac & 0xffffffffull;
+        w[1] = frac >> 32;
+        w[2] = (unsigned long long)(long long)ip;
+    }
+    w[3] = v2 > 0.0 ? (unsigned long long)__double_as_longlong(v2) : 0ull;
 }
 
 /// One warp's contribution (called by a single lane). `warp_id` only spreads
-/// the accumulators over lanes; any mapping gives the same sums.
+/// the accumulators over lanes; any mapping gives the same sums. No CTA
+/// barrier: a per-CTA pre-reduction through shared memory was measured
+/// slower (512^3 dense step_probe 3.53 vs 3.30 ms under ncu: warps parked at
+/// the barrier hold their CTA's slot while the step is HBM-bound).
 __device__ __forceinline__ void diag_commit(unsigned long long* acc, unsigned long long warp_id, double mass,
                                             double v2) {
-    unsigned long long* w = acc + (warp_id & (kDiagLanes - 1)) * kDiagWords;
-    if (fabs(mass) < 4.0e18) {  // a non-finite partial has a bad voxel, which the bad word reports
-        const double ip = floor(mass);
-        const unsigned long long frac = (unsigned long long)((mass - ip) * 18446744073709551616.0);
-        red_add_u64(w + 0, frac & 0xffffffffull);
-        red_add_u64(w + 1, frac >> 32);
-        red_add_u64(w + 2, (unsigned long long)(long long)ip);
-    }
-    if (v2 > 0.0) atomicMax(w + 3, (unsigned long long)__double_as_longlong(v2));
+    unsigned long long w[kDiagWords];
+    diag_words(mass, v2, w);
+    unsigned long long* lane = acc + (warp_id & (kDiagLanes - 1)) * kDiagWords;
+    const unsigned long long pol = l2_evict_last_policy();
+    if (w[0]) red_add_u64(lane + 0, w[0], pol);
+    if (w[1]) red_add_u64(lane + 1, w[1], pol);
+    if (w[2]) red_add_u64(lane + 2, w[2], pol);
+    if (w[3]) atomicMax(lane + 3, w[3]);
 }
 
 /// A step's exact sums: mass as a 128-bit two's-complement fixed-point number
@@ -71,7 +107,7 @@ struct DiagRaw {
 };
 
 /// One CTA per step: exact integer sums over the lanes.
-__global__ void __launch_bounds__(256) diag_rows_kernel(const unsigned long long* acc, const unsigned long long* bad,
+__global__ inline void __launch_bounds__(256) diag_rows_kernel(const unsigned long long* acc, const unsigned long long* bad,
                                                         DiagRaw* rows) {
     const unsigned long long* a = acc + (long long)blockIdx.x * kDiagLanes * kDiagWords;
     unsigned long long w0 = 0, w1 = 0, w2 = 0, vm = 0;

@@ -4,11 +4,13 @@
 #include "digest.cuh"
 #include "canon_io.cuh"
 #include "block_probe.cuh"
+#include "diag_ring.cuh"
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 namespace voxl_b200 {
 
@@ -40,6 +42,14 @@ struct MresArgs {
     int has_lid;
     int step;
     int* error_flag;
+    // fused probe_field of run_multires (DIAG kernels, a level's last
+    // sub-step of the coarse step): accumulator lanes and first-offender word
+    // of the step (diag_ring.cuh); canon[slot] = the cell's index in the
+    // level's canonical order, cell0 = the level's first canonical cell
+    unsigned long long* diag_acc;
+    unsigned long long* diag_bad;
+    const std::int32_t* canon;
+    long long cell0;
 };
 
 template <int E>
@@ -117,9 +127,18 @@ struct ProbeAcc {
     bool bad = false;
 };
 
-template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID>
+/// DIAG: the probe_field terms of one pulled cell (probe_first_bad /
+/// probe_moments, lattice.cuh) in the precision the collision forms them.
+template <class R, bool Exact>
+struct DiagCell {
+    using P = std::conditional_t<Exact || sizeof(R) == 8, double, float>;
+    P m = P(0), v = P(0);
+    int bad = -1;
+};
+
+template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID, bool DIAG = false>
 __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src,
-                                               ProbeAcc* acc = nullptr);
+                                               ProbeAcc* acc = nullptr, DiagCell<R, Exact>* dc = nullptr);
 
 /// CTAs per block: 8^3 blocks are split over two 256-thread CTAs (6 CTAs / SM
 /// at 40 registers), so each CTA's metadata prologue hides behind five others.
@@ -128,7 +147,7 @@ constexpr int kSplit = E == 8 ? 2 : 1;
 
 /// SOLID: the level has obstacle cells (a separate instantiation, so grids
 /// without them keep the register budget of the plain kernel).
-template <class L, class R, bool Exact, int E, int MODE, bool SOLID>
+template <class L, class R, bool Exact, int E, int MODE, bool SOLID, bool DIAG = false>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4) ? block_min_ctas(L::Q) : 1)
     mres_pull_kernel(const __grid_constant__ MresArgs<L::Q, R> A) {
     constexpr int Q = L::Q, BV = E * E * E, W = BlockGeom<E>::W, S = kSplit<E>;
@@ -154,7 +173,35 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
     }
     __syncthreads();
     const bool active = s_full || ((A.amask[(long long)b * W + (t >> 6)] >> (t & 63)) & 1ull);
-    if constexpr (MODE != kProbe) {
+    if constexpr (MODE != kProbe && DIAG) {
+        // fused probe_field: every thread reaches the warp reduction; the
+        // warp's mass and max |u|^2 go into the step's accumulator lanes
+        // (order-independent integer sums, diag_ring.cuh), the first
+        // offender into the step's bad word by canonical index
+        DiagCell<R, Exact> dc;
+        if (active) {
+            if (SOLID && s_solid) mres_pull_body<L, R, Exact, E, MODE, false, SOLID, true>(A, b, t, s_src, nullptr, &dc);
+            else if (s_inner) mres_pull_body<L, R, Exact, E, MODE, true, false, true>(A, b, t, s_src, nullptr, &dc);
+            else mres_pull_body<L, R, Exact, E, MODE, false, false, true>(A, b, t, s_src, nullptr, &dc);
+            if (dc.bad >= 0) {
+                const long long canon = A.cell0 + A.canon[(long long)b * (E * E * E) + t];
+                atomicMin(A.diag_bad, ((unsigned long long)canon << 5) | (unsigned long long)dc.bad);
+            }
+        }
+        using P = typename DiagCell<R, Exact>::P;
+        P pm = dc.m, pv = dc.v;
+        for (int o = 16; o > 0; o >>= 1) {
+            pm += __shfl_xor_sync(0xffffffffu, pm, o);
+            pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
+        }
+        const unsigned live = __ballot_sync(0xffffffffu, active);
+        if ((tid & 31) == 0 && live) {
+            double mass = double(pm);
+            if constexpr (std::is_same_v<P, float>) mass += double(__popc(live));
+            diag_commit(A.diag_acc, (unsigned long long)blockIdx.x * (E * E * E / S / 32) + (tid >> 5), mass,
+                        double(pv));
+        }
+    } else if constexpr (MODE != kProbe) {
         if (!active) return;
         if constexpr (SOLID) {
             if (s_solid) {
@@ -197,7 +244,7 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
 /// Pull over blocks [begin, begin + count): the part below `n_plain` (blocks
 /// that cannot see a solid cell) runs the plain kernel, the rest the
 /// solid-aware one when the level has obstacle cells.
-template <class L, class R, bool Exact, int E, int MODE>
+template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
 void launch_pull(MresArgs<L::Q, R> A, int begin, int count, int n_plain, cudaStream_t st) {
     const dim3 block(E * E * E / kSplit<E>);
     const int split = std::min(begin + count, std::max(begin, n_plain));
@@ -205,19 +252,34 @@ void launch_pull(MresArgs<L::Q, R> A, int begin, int count, int n_plain, cudaStr
     if (split > begin) {
         A.block_begin = begin;
         A.nsolid = nullptr;
-        mres_pull_kernel<L, R, Exact, E, MODE, false><<<(split - begin) * kSplit<E>, block, 0, st>>>(A);
+        mres_pull_kernel<L, R, Exact, E, MODE, false, DIAG><<<(split - begin) * kSplit<E>, block, 0, st>>>(A);
     }
     if (begin + count > split) {
         A.block_begin = split;
         A.nsolid = ns;
-        if (ns) mres_pull_kernel<L, R, Exact, E, MODE, true><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
-        else mres_pull_kernel<L, R, Exact, E, MODE, false><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
+        if (ns)
+            mres_pull_kernel<L, R, Exact, E, MODE, true, DIAG><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
+        else
+            mres_pull_kernel<L, R, Exact, E, MODE, false, DIAG><<<(begin + count - split) * kSplit<E>, block, 0, st>>>(A);
     }
 }
 
-template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID>
+/// launch_pull with the fused probe when `diag` is set (run_multires's
+/// per-step row, taken by a level's last sub-step of the coarse step).
+template <class L, class R, bool Exact, int E, int MODE>
+void launch_pull_diag(MresArgs<L::Q, R> A, int begin, int count, int n_plain, cudaStream_t st,
+                      const DiagTarget* diag, const std::int32_t* canon, long long cell0) {
+    if (!diag) return launch_pull<L, R, Exact, E, MODE>(A, begin, count, n_plain, st);
+    A.diag_acc = diag->acc;
+    A.diag_bad = diag->bad;
+    A.canon = canon;
+    A.cell0 = cell0;
+    launch_pull<L, R, Exact, E, MODE, true>(A, begin, count, n_plain, st);
+}
+
+template <class L, class R, bool Exact, int E, int MODE, bool INNER, bool SOLID, bool DIAG>
 __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b, int t, const R* const* s_src,
-                                               ProbeAcc* acc) {
+                                               ProbeAcc* acc, DiagCell<R, Exact>* dc) {
     constexpr int Q = L::Q, BV = E * E * E;
     using Ar = Arith<R, Exact>;
     constexpr int LOG = BlockGeom<E>::LOG;
@@ -285,12 +347,23 @@ __device__ __forceinline__ void mres_pull_body(const MresArgs<L::Q, R>& A, int b
         }
         return;
     }
+    // DIAG: g is the level's cur after this sub-step (the reference's state
+    // that probe_field reads): the population test runs before the
+    // collision overwrites g, the moments come from the collision
+    int dbad = -1;
+    if constexpr (DIAG) dbad = probe_first_bad<L, R, Exact>(g);
+    if constexpr (DIAG && MODE == kStream) {
+        R rho, dr, u[3];
+        pulled_moments<L, R, Exact>(g, rho, dr, u);
+        probe_moments<L, R, Exact>(dbad, rho, dr, u, dc->m, dc->v, dc->bad);
+    }
     auto collide = [&] {
         bool ok = true;
-        R rho, u[3];
+        R rho, u[3], dr = R(0);
         if constexpr (Exact) bgk_relax<L, R, true>(g, A.omega, A.keep, rho, u, ok);
-        else bgk_relax_shifted<L, R>(g, A.omega, A.keep, rho, u, ok);
+        else bgk_relax_shifted<L, R>(g, A.omega, A.keep, rho, u, ok, DIAG ? &dr : nullptr);
         if (!ok) atomicMin(A.error_flag, A.step);
+        if constexpr (DIAG && MODE != kStream) probe_moments<L, R, Exact>(dbad, rho, dr, u, dc->m, dc->v, dc->bad);
     };
     if constexpr (MODE == kFused) collide();
     const long long cell = (long long)b * Q * BV + t;
@@ -535,6 +608,8 @@ struct MultiResEngine::Level {
     int n_ring = 0;
     std::int64_t* slots = nullptr;
     std::int64_t n_active = 0;
+    std::int32_t* canon = nullptr;  // slot -> canonical index in the level (built by the first probed step)
+    long long cell0 = 0;            // canonical index of the level's first cell (levels finest first)
     double inv_tau = 1.0;
     std::int64_t slot(int x, int y, int z) const {
         const int e = ext.edge();
@@ -815,6 +890,7 @@ MultiResEngine::~MultiResEngine() {
         cudaFree(V->coal_dst);
         cudaFree(V->coal_child);
         cudaFree(V->slots);
+        cudaFree(V->canon);
         delete V;
     }
     cudaFree(d_error_);
@@ -988,7 +1064,7 @@ void MultiResEngine::launch_collide(int l, bool jump_only) {
     mark_end(kTCollide, b);
 }
 
-void MultiResEngine::launch_stream(int l, bool jump_only, cudaStream_t s) {
+void MultiResEngine::launch_stream(int l, bool jump_only, cudaStream_t s, const DiagTarget* diag) {
     Level* V = lv_[l];
     const int nb = jump_only ? V->n_jump : V->n_all;
     if (nb == 0) return;
@@ -1003,9 +1079,11 @@ void MultiResEngine::launch_stream(int l, bool jump_only, cudaStream_t s) {
         auto A = level_args<L, R, X>(cfg_, V, cfg_.fused ? ahead_step_ : steps_done_, d_error_);
         if (cfg_.fused) {  // post -> nxt, and BGK(nxt) -> the other post buffer
             A.post_ahead = static_cast<R*>(V->post[V->parity ^ 1]);
-            launch_pull<L, R, X, E, kStreamAhead>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st);
-        } else {
-            launch_pull<L, R, X, E, kStream>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st);  // post -> nxt
+            launch_pull_diag<L, R, X, E, kStreamAhead>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st, diag,
+                                                       V->canon, V->cell0);
+        } else {  // post -> nxt
+            launch_pull_diag<L, R, X, E, kStream>(A, jump_only ? V->n_uni : 0, nb, V->n_plain, st, diag, V->canon,
+                                                  V->cell0);
         }
     });
     VOXL_CUDA(cudaGetLastError());
@@ -1065,7 +1143,7 @@ void MultiResEngine::load_uniform_post() {
     cur_valid_ = true;
 }
 
-void MultiResEngine::launch_fused(int l) {
+void MultiResEngine::launch_fused(int l, const DiagTarget* diag) {
     Level* V = lv_[l];
     if (V->n_uni == 0) return;
     cudaEvent_t b{};
@@ -1077,7 +1155,7 @@ void MultiResEngine::launch_fused(int l) {
         constexpr int E = decltype(e)::value;
         auto A = level_args<L, R, X>(cfg_, V, ahead_step_, d_error_);  // the collision is the next sub-step's
         A.nxt = static_cast<R*>(V->post[V->parity ^ 1]);  // post[p] -> post[p^1]
-        launch_pull<L, R, X, E, kFused>(A, 0, V->n_uni, V->n_plain, stream_);
+        launch_pull_diag<L, R, X, E, kFused>(A, 0, V->n_uni, V->n_plain, stream_, diag, V->canon, V->cell0);
     });
     VOXL_CUDA(cudaGetLastError());
     mark_end(kTFused, b);
@@ -1171,12 +1249,15 @@ void MultiResEngine::advance(int l) {
     }
     Level* V = lv_[l];
     ahead_step_ = ahead;
+    // run_multires probes the state after the coarse step: each level's
+    // cur after its last sub-step, i.e. what this sub-step's pull computes
+    const DiagTarget* dg = sub + 1 == per ? diag_ : nullptr;
     if (cfg_.fused && V->n_uni > 0 && V->n_jump > 0) {
         // jump stream (side stream, high priority) || fused uniform (engine stream)
         VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
         VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-        launch_stream(l, true, side_);
-        launch_fused(l);
+        launch_stream(l, true, side_, dg);
+        launch_fused(l, dg);
         VOXL_CUDA(cudaEventRecord(ev_join_, side_));
         VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
     } else {
@@ -1184,8 +1265,8 @@ void MultiResEngine::advance(int l) {
             VOXL_CUDA(cudaEventRecord(ev_join_, side_));
             VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
         }
-        if (cfg_.fused) launch_fused(l);
-        launch_stream(l, cfg_.fused);
+        if (cfg_.fused) launch_fused(l, dg);
+        launch_stream(l, cfg_.fused, nullptr, dg);
     }
     std::swap(V->cur, V->nxt);
     if (cfg_.fused) V->parity ^= 1;
@@ -1350,6 +1431,78 @@ void MultiResEngine::device_probe(double out[3], DenseDiag* d) {
     d->unstable = 1;
     d->bad_voxel = std::int64_t(b >> 5);
     d->bad_population = int(b & 31u);
+}
+
+namespace {
+__global__ void mres_canon_kernel(const std::int64_t* slots, long long n, std::int32_t* canon) {
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
+        canon[slots[v]] = std::int32_t(v);
+}
+} // namespace
+
+void MultiResEngine::build_canon_maps() {
+    long long cell0 = 0;
+    for (Level* V : lv_) {
+        V->cell0 = cell0;
+        cell0 += V->n_active;
+        if (V->canon || V->n_active == 0) continue;
+        const std::size_t n = std::size_t(V->ext.num_blocks()) * std::size_t(V->ext.block_volume());
+        VOXL_CUDA(cudaMalloc(&V->canon, n * sizeof(std::int32_t)));
+        VOXL_CUDA(cudaMemsetAsync(V->canon, 0xFF, n * sizeof(std::int32_t), stream_));
+        mres_canon_kernel<<<kMresProbeBlocks, 256, 0, stream_>>>(V->slots, V->n_active, V->canon);
+        VOXL_CUDA(cudaGetLastError());
+    }
+}
+
+int MultiResEngine::step_probe_n(int n, DenseDiag* rows, std::string* abort_msg) {
+    // Batches of up to kDiagBatch coarse steps. Each level's last sub-step
+    // kernels (fused uniform + jump stream, or the staged stream) pull the
+    // level's cur of the coarse step's end and fold probe_field's terms into
+    // the step's accumulator lanes before colliding it; one reduction kernel,
+    // one copy and one host synchronisation per batch (the reference probes
+    // canonical_state after every coarse_step, solver.cpp:343-345).
+    if (n < 0) throw std::invalid_argument("step_probe: n must be >= 0");
+    if (!ring_) ring_ = std::make_unique<DiagRing>();
+    build_canon_maps();
+    int done = 0;
+    while (done < n) {
+        const int b = std::min(n - done, kDiagBatch);
+        const int step0 = steps_done_;
+        ring_->begin(b, stream_);  // every side-stream launch forks from the engine stream after this
+        DiagTarget dt;
+        for (int s = 0; s < b; ++s) {
+            dt.acc = ring_->acc(s);
+            dt.bad = ring_->bad(s);
+            diag_ = &dt;
+            advance(grid_.num_levels() - 1);
+            ++steps_done_;
+        }
+        diag_ = nullptr;
+        if (side_) {
+            VOXL_CUDA(cudaEventRecord(ev_join_, side_));
+            VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+        }
+        ring_->reduce(d_error_, stream_);
+        VOXL_CUDA(cudaStreamSynchronize(stream_));
+        const DiagRow* r = ring_->rows();
+        std::string msg;
+        // a collide-ahead error of step steps_done_ (not run yet) stays
+        // pending: first_failure only reports steps of this batch
+        const int fail = first_failure(r, b, step0, ring_->error_flag(), &msg);
+        const int good = fail < 0 ? b : fail;
+        for (int s = 0; s < good; ++s) {
+            DenseDiag& d = rows[done + s];
+            d = DenseDiag{};
+            d.mass = r[s].mass;
+            d.max_speed = std::sqrt(r[s].v2);
+        }
+        done += good;
+        if (fail >= 0) {
+            if (abort_msg) *abort_msg = msg;
+            return done;
+        }
+    }
+    return done;
 }
 
 DenseDiag MultiResEngine::probe() {

@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "multires_grid.hpp"
+#include "diag_ring.cuh"
 
 namespace voxl_b200 {
 
@@ -67,6 +68,12 @@ public:
     void coarse_step(int n);
     MresTimes timed_steps(int n);
     DenseDiag probe();
+    /// n x (coarse_step + probe_field), run_multires's per-step loop
+    /// (solver.cpp:343-345), with the probe fused into each level's last
+    /// sub-step kernels and the rows accumulated on the device (diag_ring.cuh):
+    /// one host synchronisation per kDiagBatch steps. Returns the rows filled;
+    /// on the first failing step *abort_msg = run()'s text.
+    int step_probe_n(int n, DenseDiag* rows, std::string* abort_msg);
     double total_mass();
     std::string graph_dot() const;
     /// Device-grid (uniform, jump) block counts per level.
@@ -93,6 +100,8 @@ private:
     cudaStream_t side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     int* d_error_ = nullptr;
+    std::unique_ptr<DiagRing> ring_;     // step_probe_n's accumulators
+    const DiagTarget* diag_ = nullptr;   // the probed step's target while step_probe_n enqueues it
     double* d_diag_ = nullptr;
     double* probe_scratch_ = nullptr;  // fused-mode pull probe: per-CTA partials of the uniform blocks
     std::size_t probe_scratch_len_ = 0;
@@ -116,8 +125,9 @@ private:
     void sync_state();         // cur of every cell valid (fused mode gathers uniform cells)
     void load_uniform_post();  // uniform cells' post = BGK(cur) after a host-side state change
     void launch_collide(int l, bool jump_only);
-    void launch_stream(int l, bool jump_only, cudaStream_t s = nullptr);
-    void launch_fused(int l);
+    void launch_stream(int l, bool jump_only, cudaStream_t s = nullptr, const DiagTarget* diag = nullptr);
+    void launch_fused(int l, const DiagTarget* diag = nullptr);
+    void build_canon_maps();   // Level::canon (slot -> canonical index), for the fused probe's offender
     void launch_explode(int coarse, cudaStream_t st);
     void launch_coalesce(int coarse, cudaStream_t st);
     void mark_begin(int cls, cudaEvent_t* b, cudaStream_t s = nullptr);

@@ -14,6 +14,7 @@
 #include "digest.cuh"
 #include "canon_io.cuh"
 #include "block_probe.cuh"
+#include "diag_ring.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -40,6 +41,7 @@ struct SparseArgs {
     int block_begin;
     const std::uint8_t* bitmask;  // DisagBitmask: skip blocks whose bit != want
     int bitmask_want;
+    int scan_blocks;              // > 0: persistent grid striding over this many blocks (bitmask sweep)
     int vel_source;
     const std::int32_t* meta_index;  // per slot (DisagBitmask)
     const R* compact_meta;           // 3 per boundary voxel (DisagBitmask)
@@ -50,11 +52,12 @@ struct SparseArgs {
     double shift[Q];  // w_i for shifted fp32 storage
     int step;
     int* error_flag;
-    // fused probe_field (DIAG kernels): per-warp (mass, |u|^2) partials at
-    // slot (diag_offset + CTA) * warps + warp; any unstable cell sets *diag_bad
-    double* diag_partial;
-    long long diag_offset;
-    unsigned int* diag_bad;
+    // fused probe_field (DIAG kernels): the step's accumulator lanes and
+    // first-offender word (diag_ring.cuh); canon[slot] = the voxel's index in
+    // canonical_state order (read for an unstable voxel only)
+    unsigned long long* diag_acc;
+    unsigned long long* diag_bad;
+    const std::int32_t* canon;
 };
 
 /// equilibrium (lattice.cpp:104-113) at given (rho, u), reference op order.
@@ -92,7 +95,7 @@ __device__ __forceinline__ bool regularized_dev(int sign, const R (&ubc)[3], R (
     });
     R rho;
     if constexpr (Exact) rho = A::add(sum0, A::mul(R(2), sum_in)) / A::sub(R(1), u_n);
-    else rho = (sum0 + R(2) * sum_in) / (R(1) - u_n);
+    else rho = fma_rn(R(2), sum_in, sum0) / A::sub(R(1), u_n);  // FMA spelled out (Arith<float, false>)
     R feq[L::Q];
     equilibrium_dev<L, R, Exact>(rho, ubc, feq);
     R fneq[L::Q];
@@ -153,21 +156,43 @@ constexpr int kSplit = E == 8 ? 2 : 1;
 #ifndef VOXL_HEAVY_MINB
 #define VOXL_HEAVY_MINB 4
 #endif
+template <class L, class R, bool Exact, int E, int MODE, bool DIAG>
+__device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b, int half);
+
 template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 ? (MODE == 0 ? block_min_ctas(L::Q) : VOXL_HEAVY_MINB) : 1)
     sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
+    constexpr int S = kSplit<E>;
+    if (A.scan_blocks > 0) {
+        // DisagBitmask sweep (sparse.cpp:369-380): every block is visited and
+        // skipped unless its bit matches. A CTA per block would spend most of
+        // the boundary sweep dispatching CTAs that exit at once (0.44 of
+        // 0.66 ms at 512^3), so this sweep strides a persistent grid over the
+        // blocks and skips with one broadcast byte load.
+        for (int b = A.block_begin + int(blockIdx.x) / S; b < A.block_begin + A.scan_blocks; b += int(gridDim.x) / S) {
+            if (int(A.bitmask[b]) != A.bitmask_want) continue;  // CTA-uniform
+            sparse_block<L, R, Exact, E, MODE, DIAG>(A, b, int(blockIdx.x) % S);
+            __syncthreads();  // shared neighbourhood tables are rewritten by the next block
+        }
+        return;
+    }
+    const int b = A.block_begin + int(blockIdx.x) / S;
+    if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip
+    sparse_block<L, R, Exact, E, MODE, DIAG>(A, b, int(blockIdx.x) % S);
+}
+
+template <class L, class R, bool Exact, int E, int MODE, bool DIAG>
+__device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b, int half) {
     constexpr int Q = L::Q;
     constexpr int BV = E * E * E;
     constexpr int W = BV >= 64 ? BV / 64 : 1;
     constexpr int S = kSplit<E>;
-    const int b = A.block_begin + int(blockIdx.x) / S;
-    if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip (DIAG: partials pre-zeroed)
     __shared__ const R* s_ptr[27];  // component-0 plane of neighbour block d (own block if absent)
     __shared__ int s_nbr[27];
     __shared__ unsigned long long s_mask[27][W];
     __shared__ int s_full;
     const int tid = threadIdx.x;
-    const int t = tid + (int(blockIdx.x) % S) * (BV / S);  // local voxel index in the block
+    const int t = tid + half * (BV / S);  // local voxel index in the block
     if (tid < 27) {
         const int nb = A.nbr[(long long)b * 27 + tid];
         s_nbr[tid] = nb;
@@ -273,23 +298,24 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 
     });
     }();
 
-    // Fused probe_field (lbm.cpp:116-138): per-warp partials (fixed slots,
-    // fixed-order reduction later); an unstable cell only raises a flag --
-    // the engine names it with the canonical-order probe (rare path).
+    // Fused probe_field (lbm.cpp:116-138): the warp's mass and max |u|^2 go
+    // into the step's accumulator lanes (order-independent integer sums,
+    // diag_ring.cuh); an unstable voxel names itself by canonical index.
     if constexpr (DIAG) {
-        if (live && dg_bad >= 0) atomicOr(A.diag_bad, 1u);
+        if (live && dg_bad >= 0)
+            atomicMin(A.diag_bad, ((unsigned long long)A.canon[(long long)b * BV + t] << 5) |
+                                      (unsigned long long)dg_bad);
         P pm = dg_mass, pv = dg_bad >= 0 ? P(0) : dg_v2;
         for (int o = 16; o > 0; o >>= 1) {
             pm += __shfl_xor_sync(0xffffffffu, pm, o);
             pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
         }
-        double mass = double(pm);
-        if constexpr (std::is_same_v<P, float>) mass += double(__popc(__ballot_sync(0xffffffffu, live)));
-        if ((tid & 31) == 0) {
+        const unsigned lanes = __ballot_sync(0xffffffffu, live);
+        if ((tid & 31) == 0 && lanes) {
+            double mass = double(pm);
+            if constexpr (std::is_same_v<P, float>) mass += double(__popc(lanes));
             constexpr int kWarps = (BV / S + 31) / 32;
-            const long long slot = (A.diag_offset + (long long)blockIdx.x) * kWarps + (tid >> 5);
-            A.diag_partial[2 * slot] = mass;
-            A.diag_partial[2 * slot + 1] = double(pv);
+            diag_commit(A.diag_acc, ((unsigned long long)b * S + half) * kWarps + (tid >> 5), mass, double(pv));
         }
     }
 }
@@ -370,27 +396,37 @@ struct SparseOps {
         return A;
     }
 
+    /// Resident CTAs of a kernel on the whole GPU (the persistent scan grid).
+    template <class K>
+    static int resident_ctas(K kernel, int threads) {
+        int dev = 0, sms = 0;
+        VOXL_CUDA(cudaGetDevice(&dev));
+        VOXL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        int per = 0;
+        VOXL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0));
+        return std::max(1, per) * sms;
+    }
+
     template <int E>
     static void launch_e(SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
         if (nblocks <= 0) return;
         constexpr int S = kSplit<E>;
-        const dim3 grid(nblocks * S), block(E * E * E / S);
-        if (A.diag_partial) {
+        dim3 grid(nblocks * S);
+        const dim3 block(E * E * E / S);
+        if (A.scan_blocks > 0) {  // persistent grid over the bitmask sweep's blocks
+            const int r = A.diag_acc ? resident_ctas(sparse_step_kernel<L, R, Exact, E, kHeavy, true>, block.x)
+                                     : resident_ctas(sparse_step_kernel<L, R, Exact, E, kHeavy, false>, block.x);
+            A.scan_blocks = nblocks;
+            grid = dim3(std::min(nblocks, r / S) * S);
+        }
+        if (A.diag_acc) {
             if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy, true><<<grid, block, 0, st>>>(A);
             else sparse_step_kernel<L, R, Exact, E, kLight, true><<<grid, block, 0, st>>>(A);
-            A.diag_offset += (long long)nblocks * S;
         } else {
             if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy><<<grid, block, 0, st>>>(A);
             else sparse_step_kernel<L, R, Exact, E, kLight><<<grid, block, 0, st>>>(A);
         }
         VOXL_CUDA(cudaGetLastError());
-    }
-
-    /// fused-probe partial slots (one per warp) of `nblocks` blocks
-    static long long diag_slots(int edge, long long nblocks) {
-        const int s = edge == 8 ? kSplit<8> : kSplit<4>;
-        const int threads = edge * edge * edge / s;
-        return nblocks * s * ((threads + 31) / 32);
     }
 
     static void launch(int edge, SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
@@ -528,7 +564,7 @@ SparseEngine::~SparseEngine() {
     cudaFree(d_slots_);
     cudaFree(d_error_);
     cudaFree(d_diag_);
-    cudaFree(diag_partials_);
+    cudaFree(d_canon_);
     if (side_) {
         cudaStreamSynchronize(side_);
         cudaEventDestroy(ev_fork_);
@@ -607,16 +643,17 @@ void SparseEngine::digest(unsigned long long out[2]) {
     VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, double* diag_partial,
-                          unsigned int* diag_bad) {
+void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, const DiagTarget* diag) {
     // sweep / step (sparse.cpp:359-394) as real kernels.
     sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
         using Ops = decltype(ops);
         auto A = Ops::base_args(cfg_);
         using R = std::remove_pointer_t<decltype(A.nxt)>;
-        A.diag_partial = diag_partial;  // fused probe_field (step_probe)
-        A.diag_bad = diag_bad;
-        A.diag_offset = 0;
+        if (diag) {  // fused probe_field (step_probe_n)
+            A.diag_acc = diag->acc;
+            A.diag_bad = diag->bad;
+            A.canon = d_canon_;
+        }
         A.cur = static_cast<const R*>(buf_[cur_]);
         A.nxt = static_cast<R*>(buf_[cur_ ^ 1]);
         A.nbr = d_nbr_;
@@ -642,19 +679,36 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, d
                     VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
                 }
                 break;
-            case Strategy::DisagBitmask:
+            case Strategy::DisagBitmask: {
+                // both sweeps scan every block and skip the other class's
+                // blocks by bitmask (sparse.cpp:369-380); they write disjoint
+                // blocks, so the heavy sweep runs on the side stream
+                // concurrently with the light one, as in DisagMem
                 A.vel_source = kVelIndirect;
                 A.block_begin = 0;
                 A.bitmask = d_bitmask_;
+                const bool split = classes_.n_boundary > 0 && classes_.n_boundary < nb;
+                cudaStream_t hs = split ? side_ : stream_;
+                if (split) {
+                    VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
+                    VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+                }
                 A.bitmask_want = 1;
-                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], stream_));
-                Ops::launch(edge, A, kHeavy, nb, stream_);
-                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], stream_));
+                A.scan_blocks = 1;  // persistent strided sweep (launch_e sizes it)
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], hs));
+                Ops::launch(edge, A, kHeavy, nb, hs);
+                if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], hs));
+                A.scan_blocks = 0;
                 A.bitmask_want = 0;
                 if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
                 Ops::launch(edge, A, kLight, nb, stream_);
                 if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
+                if (split) {
+                    VOXL_CUDA(cudaEventRecord(ev_join_, side_));
+                    VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+                }
                 break;
+            }
             case Strategy::DisagMem: {
                 A.vel_source = kVelConst;
                 // boundary blocks [0, n_b) with the heavy kernel on the side
@@ -700,42 +754,73 @@ void SparseEngine::step(int n) {
     check_errors();
 }
 
-DenseDiag SparseEngine::step_probe() {
-    // One step with probe_field fused into the step kernels (run_sparse's
-    // per-step row, solver.cpp:287-291): per-warp partials, a fixed-order
-    // two-stage reduction and one 32-byte row back to the host.
-    long long slots = 0;
-    sparse_dispatch(cfg_.lattice, cfg_.precision, [&](auto ops) {
-        slots = decltype(ops)::diag_slots(grid_.edge(), grid_.num_blocks());
-    });
-    if (cfg_.strategy == Strategy::DisagBitmask) slots *= 2;  // both sweeps visit every block
-    if (diag_partials_len_ < std::size_t(2 * slots)) {
-        cudaFree(diag_partials_);
-        VOXL_CUDA(cudaMalloc(&diag_partials_, 2 * slots * sizeof(double)));
-        diag_partials_len_ = std::size_t(2 * slots);
+namespace {
+__global__ void sparse_canon_kernel(const std::int64_t* slots, long long n, std::int32_t* canon) {
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
+        canon[slots[v]] = std::int32_t(v);
+}
+} // namespace
+
+int SparseEngine::step_probe_n(int n, DenseDiag* rows, std::string* abort_msg) {
+    // Batches of up to kDiagBatch steps (run_sparse's per-step loop,
+    // solver.cpp:287-291): each step's kernels fold probe_field's terms into
+    // the step's accumulator lanes and name an unstable voxel by canonical
+    // index; one reduction kernel, one copy and one host synchronisation per
+    // batch.
+    if (n < 0) throw std::invalid_argument("step_probe: n must be >= 0");
+    if (!ring_) ring_ = std::make_unique<DiagRing>();
+    if (!d_canon_) {
+        ensure_slots();
+        const std::size_t ns = std::size_t(grid_.num_blocks()) * std::size_t(grid_.block_volume());
+        VOXL_CUDA(cudaMalloc(&d_canon_, ns * sizeof(std::int32_t)));
+        VOXL_CUDA(cudaMemsetAsync(d_canon_, 0xFF, ns * sizeof(std::int32_t), stream_));
+        sparse_canon_kernel<<<kSpProbeBlocks, 256, 0, stream_>>>(d_slots_, grid_.num_active(), d_canon_);
+        VOXL_CUDA(cudaGetLastError());
     }
-    double* stage = d_diag_;
-    double* out = d_diag_ + 2 * kSpProbeBlocks;
-    auto* bad_any = reinterpret_cast<unsigned int*>(out + 3);
-    VOXL_CUDA(cudaMemsetAsync(diag_partials_, 0, 2 * slots * sizeof(double), stream_));  // skipped CTAs add 0
-    VOXL_CUDA(cudaMemsetAsync(out, 0, 4 * sizeof(double), stream_));
-    launch(0, nullptr, nullptr, diag_partials_, bad_any);
-    partials_reduce_kernel<<<kSpProbeBlocks, 256, 0, stream_>>>(diag_partials_, slots, stage);
-    block_probe_final<<<1, 32, 0, stream_>>>(stage, kSpProbeBlocks, out);
-    VOXL_CUDA(cudaGetLastError());
-    double row[4];
-    int flag = INT_MAX;
-    VOXL_CUDA(cudaMemcpyAsync(row, out, sizeof row, cudaMemcpyDeviceToHost, stream_));
-    VOXL_CUDA(cudaMemcpyAsync(&flag, d_error_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-    VOXL_CUDA(cudaStreamSynchronize(stream_));
-    if (flag != INT_MAX)
-        throw InstabilityError("run aborted at step " + std::to_string(flag) + ": macroscopic: non-positive density");
-    unsigned int any;
-    std::memcpy(&any, &row[3], sizeof any);
-    if (any) return probe();  // names the first unstable cell in canonical order
+    int done = 0;
+    while (done < n) {
+        const int b = std::min(n - done, kDiagBatch);
+        const int step0 = steps_done_;
+        ring_->begin(b, stream_);  // side-stream sweeps fork from the engine stream after this
+        for (int s = 0; s < b; ++s) {
+            DiagTarget dt;
+            dt.acc = ring_->acc(s);
+            dt.bad = ring_->bad(s);
+            launch(0, nullptr, nullptr, &dt);
+        }
+        ring_->reduce(d_error_, stream_);
+        VOXL_CUDA(cudaStreamSynchronize(stream_));
+        const DiagRow* r = ring_->rows();
+        std::string msg;
+        const int fail = first_failure(r, b, step0, ring_->error_flag(), &msg);
+        const int good = fail < 0 ? b : fail;
+        for (int s = 0; s < good; ++s) {
+            DenseDiag& d = rows[done + s];
+            d = DenseDiag{};
+            d.mass = r[s].mass;
+            d.max_speed = std::sqrt(r[s].v2);
+        }
+        done += good;
+        if (fail >= 0) {
+            if (abort_msg) *abort_msg = msg;
+            last_bad_ = r[fail].bad;
+            return done;
+        }
+    }
+    return done;
+}
+
+DenseDiag SparseEngine::step_probe() {
+    // One probed step; a probe_field instability comes back in the row (the
+    // caller composes run()'s text), a non-positive density throws.
     DenseDiag d;
-    d.mass = row[0];
-    d.max_speed = std::sqrt(row[1]);
+    std::string msg;
+    if (step_probe_n(1, &d, &msg) == 1) return d;
+    if (msg.find("macroscopic") != std::string::npos) throw InstabilityError(msg);
+    d = DenseDiag{};
+    d.unstable = 1;
+    d.bad_voxel = std::int64_t(last_bad_ >> 5);
+    d.bad_population = int(last_bad_ & 31u);
     return d;
 }
 

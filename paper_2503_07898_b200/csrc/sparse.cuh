@@ -18,11 +18,14 @@
 
 #include <array>
 #include <cstdint>
+#include <memory>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
 #include "dense.cuh"
 #include "sparse_grid.hpp"
+#include "diag_ring.cuh"
 
 namespace voxl_b200 {
 
@@ -66,6 +69,11 @@ public:
     double timed_steps(int n, double* boundary_ms, double* light_ms);
     DenseDiag probe();
     DenseDiag step_probe();  // one step with probe_field fused into the step kernels
+    /// n x (step + probe_field), run_sparse's per-step loop (solver.cpp:287-291),
+    /// rows accumulated on the device (diag_ring.cuh), one host
+    /// synchronisation per kDiagBatch steps. Returns the rows filled; on the
+    /// first failing step *abort_msg = run()'s text.
+    int step_probe_n(int n, DenseDiag* rows, std::string* abort_msg);
     void check_errors();
 
 private:
@@ -98,10 +106,10 @@ private:
     cudaStream_t side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
 
-    void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l, double* diag_partial = nullptr,
-                unsigned int* diag_bad = nullptr);
-    double* diag_partials_ = nullptr;  // fused-probe per-warp partials (step_probe)
-    std::size_t diag_partials_len_ = 0;
+    void launch(int which, cudaEvent_t* ev_b, cudaEvent_t* ev_l, const DiagTarget* diag = nullptr);
+    std::unique_ptr<DiagRing> ring_;       // step_probe_n's accumulators
+    std::int32_t* d_canon_ = nullptr;      // slot -> canonical index (the fused probe's offender)
+    unsigned long long last_bad_ = ~0ull;  // first-offender word of the last failing probed step
     void ensure_slots();
     void transfer(double* host, bool to_device, unsigned long long* digest);
 };

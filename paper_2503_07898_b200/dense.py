@@ -222,17 +222,7 @@ class DenseEngine:
         256 steps: the list of n diagnostics rows. On the first failing step
         raises VoxlInstability with run()'s text; `.rows` holds the rows of
         the steps before it."""
-        rows = (_capi.Diag * max(n, 1))()
-        done = C.c_int()
-        st = lib.voxl_dense_step_probe_n(self._h, n, rows, C.byref(done))
-        out = [rows[i] for i in range(done.value)]
-        if st != _capi.OK:
-            try:
-                check(st)
-            except _capi.VoxlError as e:
-                e.rows = out
-                raise
-        return out
+        return _capi.probe_rows(lib.voxl_dense_step_probe_n, self._h, n)
 
     def ledger(self, step: int):
         return _records(lib.voxl_dense_ledger, self._h, step)

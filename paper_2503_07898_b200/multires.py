@@ -176,6 +176,13 @@ class MultiResEngine:
         check(lib.voxl_mres_probe(self._h, C.byref(d)))
         return d
 
+    def step_probe_n(self, n: int):
+        """n coarse steps with probe_field fused into each level's last
+        sub-step (run_multires's per-step rows), one host synchronisation per
+        256 steps. Raises VoxlInstability with run()'s text at the first
+        failing step (`.rows` = the rows before it)."""
+        return _capi.probe_rows(lib.voxl_mres_step_probe_n, self._h, n)
+
     def total_mass(self):
         m = C.c_double()
         check(lib.voxl_mres_total_mass(self._h, C.byref(m)))

@@ -205,12 +205,22 @@ BAD_DENSITY = 31  # voxl_diag.bad_population of a non-positive density (VOXL_BAD
 
 
 def _unstable(d, step):
+    """run()'s abort for one probe row (the per-step loop shape)."""
     if not d.unstable:
         return
     if d.bad_population == BAD_DENSITY:  # macroscopic's throw inside probe_field (lattice.cpp:124)
         raise RuntimeError(f"run aborted at step {step}: macroscopic: non-positive density")
     raise RuntimeError(f"run aborted at step {step}: instability at step {step}, voxel {d.bad_voxel}, "
                        f"population {d.bad_population}")
+
+
+def _probed_rows(eng, steps):
+    """n probed steps through the engine's fused step_probe_n: (rows, error)
+    -- the rows of the steps that completed and run()'s abort text, if any."""
+    try:
+        return eng.step_probe_n(steps), None
+    except VoxlInstability as e:
+        return e.rows, e
 
 
 def run_dense(c: SolverConfig) -> RunResult:
@@ -224,12 +234,7 @@ def run_dense(c: SolverConfig) -> RunResult:
     eng.set_canonical(initial_canonical_state(c))
     # step_occ + probe_field per step, fused on the device; rows read back per
     # batch, the first failing step raises run()'s text
-    try:
-        rows = eng.step_probe_n(c.steps)
-    except VoxlInstability as e:
-        rows, err = e.rows, e
-    else:
-        err = None
+    rows, err = _probed_rows(eng, c.steps)
     for step, d in enumerate(rows):
         r.diagnostics.append((step, d.mass, d.max_speed))
         r.ledger += plan_ledger(step, lattice=c.lattice, domain=c.domain, layout=c.layout, partitions=c.partitions,
@@ -257,10 +262,11 @@ def run_sparse(c: SolverConfig) -> RunResult:
     act = obstacle_mask(c.domain, c.obstacle_radius)
     eng = SparseEngine(c.domain, act, tau=c.tau, u_bc=c.velocity, block_edge=c.block_edge, strategy=c.strategy,
                        precision=c.precision, lattice=c.lattice)
-    for step in range(c.steps):
-        d = eng.step_probe()  # step + probe_field, fused on the device
-        _unstable(d, step)
-        r.diagnostics.append((step, d.mass, d.max_speed))
+    rows, err = _probed_rows(eng, c.steps)  # step + probe_field, fused on the device
+    r.diagnostics = [(step, d.mass, d.max_speed) for step, d in enumerate(rows)]
+    if err is not None:
+        eng.close()
+        raise RuntimeError(str(err))
     r.field = eng.get_state()
     # The report is the reference's (edge-4 tables); the engine's own blocks may be 8^3.
     from .sparse import SparsePlan
@@ -284,11 +290,12 @@ def run_multires(c: SolverConfig) -> RunResult:
     lm = band_level_map(c.domain, c.levels, c.partition_axis())
     eng = MultiResEngine(c.domain, c.levels, level_map=lm, tau=c.tau, lid_u=c.velocity, fused=c.fused,
                          precision=c.precision, block_edge=c.block_edge, lattice=c.lattice)
-    for step in range(c.steps):
-        eng.step(1)
-        d = eng.probe()
-        _unstable(d, step)
-        r.diagnostics.append((step, d.mass, d.max_speed))
+    # coarse_step + probe_field, the probe fused into each level's last sub-step
+    rows, err = _probed_rows(eng, c.steps)
+    r.diagnostics = [(step, d.mass, d.max_speed) for step, d in enumerate(rows)]
+    if err is not None:
+        eng.close()
+        raise RuntimeError(str(err))
     r.field = eng.get_state()
     plan = MultiResPlan(c.domain, c.levels, level_map=lm, tau=c.tau, lattice=c.lattice)
     r.graph_dot = plan.graph_dot(fused=c.fused)

@@ -197,6 +197,13 @@ class SparseEngine:
         check(lib.voxl_sparse_step_probe(self._h, C.byref(d)))
         return d
 
+    def step_probe_n(self, n: int):
+        """n steps with probe_field fused into the step kernels (run_sparse's
+        per-step rows), one host synchronisation per 256 steps. Raises
+        VoxlInstability with run()'s text at the first failing step (`.rows`
+        = the rows before it)."""
+        return _capi.probe_rows(lib.voxl_sparse_step_probe_n, self._h, n)
+
     def close(self):
         if self._h:
             check(lib.voxl_sparse_destroy(self._h))

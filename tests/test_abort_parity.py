@@ -105,6 +105,15 @@ def test_sparse_abort_text_equals_reference(elem, value, strategy, edge):
     e.close()
     assert msg == ref_msg
     _rows_close(rows, ref_rows, st.size)
+    # batched rows (run_sparse's loop, one read-back per batch)
+    e = V.SparseEngine(dom, V.obstacle_mask(dom), tau=0.7, u_bc=(0.04, 0, 0), block_edge=edge, strategy=strategy,
+                       precision="fp64")
+    e.set_state(st)
+    with pytest.raises(V.VoxlInstability) as info:
+        e.step_probe_n(10)
+    e.close()
+    assert str(info.value) == ref_msg
+    _rows_close([(d.mass, d.max_speed) for d in info.value.rows], ref_rows, st.size)
 
 
 @pytest.mark.gpu
@@ -128,3 +137,12 @@ def test_multires_abort_text_equals_reference(elem, value, fused):
     e.close()
     assert msg == ref_msg
     _rows_close(rows, ref_rows, st.size)
+    # the probe fused into each level's last sub-step, rows once per batch
+    for edge in (8, 4):
+        e = V.MultiResEngine(dom, 2, fused=fused, precision="fp64", block_edge=edge)
+        e.set_state(st)
+        with pytest.raises(V.VoxlInstability) as info:
+            e.step_probe_n(10)
+        e.close()
+        assert str(info.value) == ref_msg
+        _rows_close([(d.mass, d.max_speed) for d in info.value.rows], ref_rows, st.size)

@@ -472,3 +472,53 @@ def test_fused_probe_path_vs_host_sums(edge, solid):
         base += len(c)
     ref_tm = math.fsum(weighted)
     assert abs(tm - ref_tm) <= 1e-12 * ref_tm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("precision,edge,solid,levels", [("fp64", 8, False, 3), ("fp64", 4, False, 2),
+                                                         ("fp64", 8, True, 3), ("fp32", 8, False, 3),
+                                                         ("fp32", 4, True, 3)])
+def test_step_probe_n_equals_step_plus_probe(fused, precision, edge, solid, levels):
+    """run_multires's rows with the probe fused into each level's last
+    sub-step (step_probe_n) against coarse_step + probe() on a twin engine:
+    fields bitwise, mass to summation order (fp64) / fp32 moment rounding,
+    max |u| likewise."""
+    dom = (32, 32, 32)
+    lm = obstacle_band_level_map(dom, levels) if solid else None
+    kw = dict(level_map=lm, fused=fused, precision=precision, block_edge=edge, solid_cells=solid)
+    a = V.MultiResEngine(dom, levels, **kw)
+    b = V.MultiResEngine(dom, levels, **kw)
+    tol_m, tol_u = (1e-12, 1e-12) if precision == "fp64" else (1e-9, 1e-6)
+    rows = a.step_probe_n(3) + a.step_probe_n(4)  # two batches
+    for k in range(7):
+        b.step(1)
+        db = b.probe()
+        assert rows[k].unstable == 0 and db.unstable == 0
+        assert abs(rows[k].mass - db.mass) <= tol_m * db.mass
+        assert abs(rows[k].max_speed - db.max_speed) <= tol_u * db.max_speed + 1e-15
+    assert np.array_equal(a.get_state(), b.get_state())
+    a.close()
+    b.close()
+
+
+@pytest.mark.gpu
+def test_step_probe_n_2d_and_batch_boundary():
+    """D2Q9 multires (z = 0 layer of the blocks) and a run longer than one
+    device batch (256 steps): rows equal step + probe() every 37th step."""
+    dom = (32, 48, 1)
+    lm = V.band_level_map(dom, 3, axis=1)
+    kw = dict(level_map=lm, tau=0.6, fused=True, precision="fp64", block_edge=8, lattice="D2Q9")
+    a = V.MultiResEngine(dom, 3, **kw)
+    b = V.MultiResEngine(dom, 3, **kw)
+    rows = a.step_probe_n(300)
+    assert len(rows) == 300
+    for k in range(300):
+        b.step(1)
+        if k % 37 == 0 or k == 299:
+            db = b.probe()
+            assert abs(rows[k].mass - db.mass) <= 1e-12 * db.mass
+            assert abs(rows[k].max_speed - db.max_speed) <= 1e-12 * db.max_speed + 1e-15
+    assert np.array_equal(a.get_state(), b.get_state())
+    a.close()
+    b.close()

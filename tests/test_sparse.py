@@ -272,3 +272,27 @@ def test_step_probe_equals_step_plus_probe(strategy, precision, edge):
     assert np.array_equal(a.get_state(), b.get_state())
     a.close()
     b.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["naive", "disag_bitmask", "disag_mem"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_step_probe_n_batches(strategy, precision):
+    """run_sparse's rows accumulated on the device over a run longer than one
+    batch (256 steps) against step + probe() on a twin engine, fields bitwise."""
+    dom = (24, 16, 16)
+    a = V.SparseEngine(dom, block_edge=8, strategy=strategy, precision=precision)
+    b = V.SparseEngine(dom, block_edge=8, strategy=strategy, precision=precision)
+    tol_m, tol_u = (1e-12, 1e-12) if precision == "fp64" else (1e-9, 1e-6)
+    rows = a.step_probe_n(270)
+    assert len(rows) == 270
+    for k in range(270):
+        b.step(1)
+        if k % 53 == 0 or k == 269:
+            db = b.probe()
+            assert rows[k].unstable == 0 and db.unstable == 0
+            assert abs(rows[k].mass - db.mass) <= tol_m * db.mass
+            assert abs(rows[k].max_speed - db.max_speed) <= tol_u * db.max_speed + 1e-12
+    assert np.array_equal(a.get_state(), b.get_state())
+    a.close()
+    b.close()

@@ -281,6 +281,238 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
     }
 }
 
+// ---- AoS step through shared-memory plane tiles (fp32, 3D) --------------------------
+//
+// The AoS layout keeps a voxel's Q populations in one 4Q-byte record. The
+// one-voxel-per-thread kernel above pulls population i of record (x - e_i):
+// a warp's load then touches 32 records 4Q bytes apart (Q sectors for 128
+// useful bytes), and the x/y/z neighbourhood of a warp (~34 x 9 records) is
+// far more than L1 holds per warp at full occupancy, so every pull goes to L2
+// at Q-fold sector amplification (21 % of copy bandwidth measured).
+//
+// This kernel stages records instead of populations. A CTA owns a 32 x 8
+// (x, y) column of the slab and marches it along z through a ring of plane
+// tiles (34 x 10 records with the x/y halo) in shared memory. Each tile row
+// is one contiguous span of global memory (the records of consecutive x are
+// adjacent) and is filled by 16-byte cp.async (TMA-free async copies; the
+// smem row is shifted so that it shares the global span's 16-byte phase),
+// one plane ahead of the plane being computed. A voxel's pulls are then
+// shared-memory reads (record stride Q words, odd for Q = 19 / 27: bank-
+// conflict free), the collision is the same bgk_relax_shifted as every
+// other fp32 kernel (bitwise equal results), and the outputs go back through
+// the ring slot the plane k-1 tile just vacated, so each output row is again
+// one contiguous span of 16-byte stores. Traffic: every record is read once
+// per plane pass plus the tile halo (34 x 10 / 256 = 1.33x from L2, mostly
+// hits) and written once.
+#ifndef VOXL_AOS_TY
+#define VOXL_AOS_TY 8
+#endif
+#ifndef VOXL_AOS_CHUNK
+#define VOXL_AOS_CHUNK 64
+#endif
+#ifndef VOXL_AOS_SLOTS19
+#define VOXL_AOS_SLOTS19 4
+#endif
+#ifndef VOXL_AOS_MINB
+#define VOXL_AOS_MINB 2
+#endif
+constexpr int kAosTX = 32, kAosTY = VOXL_AOS_TY, kAosChunk = VOXL_AOS_CHUNK;
+constexpr int kAosThreads = kAosTX * kAosTY;
+
+/// Tile geometry in words: row pitch (a multiple of 4, so every row has the
+/// same 16-byte phase), plane slot size (one pitch of phase slack), slots.
+template <int Q>
+struct AosTile {
+    static constexpr int RX = kAosTX + 2, RY = kAosTY + 2;
+    static constexpr int pitch = (RX * Q + 3) / 4 * 4;
+    static constexpr int slot_words = RY * pitch + 4;
+    static constexpr int slots = Q <= 19 ? VOXL_AOS_SLOTS19 : 3;  // 2 CTAs per SM either way
+    static constexpr int smem_bytes = slots * slot_words * 4;
+};
+
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+/// A warp copies one contiguous row of `nw` words global -> shared (cp.async):
+/// 16-byte chunks where both sides share the 16-byte phase, single words for
+/// the unaligned head and tail (never outside the row).
+__device__ __forceinline__ void aos_row_load(float* sm, const float* g, int nw, int lane) {
+    const int head = int((4 - ((reinterpret_cast<std::uintptr_t>(g) >> 2) & 3)) & 3);
+    const bool same_phase = ((reinterpret_cast<std::uintptr_t>(g) ^ reinterpret_cast<std::uintptr_t>(sm)) & 15) == 0;
+    if (!same_phase || nw < head + 4) {
+        for (int o = lane; o < nw; o += 32) cp_async4(sm + o, g + o);
+        return;
+    }
+    const int chunks = (nw - head) >> 2, body_end = head + 4 * chunks;
+    if (lane < head) cp_async4(sm + lane, g + lane);
+    if (lane < nw - body_end) cp_async4(sm + body_end + lane, g + body_end + lane);
+    for (int c = lane; c < chunks; c += 32) cp_async16(sm + head + 4 * c, g + head + 4 * c);
+}
+
+/// A warp stores one contiguous row of `nw` words shared -> global.
+__device__ __forceinline__ void aos_row_store(float* g, const float* sm, int nw, int lane) {
+    const int head = int((4 - ((reinterpret_cast<std::uintptr_t>(g) >> 2) & 3)) & 3);
+    const bool same_phase = ((reinterpret_cast<std::uintptr_t>(g) ^ reinterpret_cast<std::uintptr_t>(sm)) & 15) == 0;
+    if (!same_phase || nw < head + 4) {
+        for (int o = lane; o < nw; o += 32) g[o] = sm[o];
+        return;
+    }
+    const int chunks = (nw - head) >> 2, body_end = head + 4 * chunks;
+    if (lane < head) g[lane] = sm[lane];
+    if (lane < nw - body_end) g[body_end + lane] = sm[body_end + lane];
+    for (int c = lane; c < chunks; c += 32)
+        *reinterpret_cast<float4*>(g + head + 4 * c) = *reinterpret_cast<const float4*>(sm + head + 4 * c);
+}
+
+/// Plane kk (local, -1..n) of the CTA's tile into a ring slot: rows b0-1 ..
+/// b0+TY, records a0-1 .. a0+TX, clipped to the slab (walls never read
+/// outside it; the k = -1 / n planes are the partition halos). One warp per
+/// row.
+template <int Q>
+__device__ __forceinline__ void aos_load_plane(const StepArgs<Q, float>& A, float* tile, int kk, int a0, int b0) {
+    using T = AosTile<Q>;
+    const int a_lo = max(a0 - 1, 0), a_hi = min(a0 + kAosTX, A.na - 1);
+    const int b_lo = max(b0 - 1, 0), b_hi = min(b0 + kAosTY, A.nb - 1);
+    const int nw = (a_hi - a_lo + 1) * Q;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    for (int bb = b_lo + warp; bb <= b_hi; bb += kAosThreads / 32) {
+        const float* g = A.in + ((long long)(kk + 1) * A.s + (long long)bb * A.na + a_lo) * Q;
+        float* sm = tile + (bb - (b0 - 1)) * T::pitch + (a_lo - (a0 - 1)) * Q;
+        aos_row_load(sm, g, nw, lane);
+    }
+}
+
+template <class L, bool DIAG>
+__global__ void __launch_bounds__(kAosThreads, VOXL_AOS_MINB)
+    dense_aos_tiled_kernel(const __grid_constant__ StepArgs<L::Q, float> A, int k_base, int z_stride, int chunk,
+                           int k_end) {
+    constexpr int Q = L::Q;
+    using T = AosTile<Q>;
+    constexpr int NS = T::slots;
+    using R = float;
+    extern __shared__ __align__(16) float aos_smem[];
+    const int tx = threadIdx.x & (kAosTX - 1), ty = threadIdx.x / kAosTX;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    const int a0 = blockIdx.x * kAosTX, b0 = blockIdx.y * kAosTY;
+    const int a = a0 + tx, b = b0 + ty;
+    const bool live = a < A.na && b < A.nb;
+    const int kb = k_base + int(blockIdx.z) * z_stride;
+    const int ke = min(kb + chunk, k_end);
+    // the tiles start `phase` words into their slots so that tile rows share
+    // the 16-byte phase of their global spans (the same for every row and
+    // plane when na * Q is a multiple of 4; otherwise rows fall back to words)
+    const int a_lo = max(a0 - 1, 0);
+    const int phase = int(((long long)a_lo * Q - (long long)(a_lo - (a0 - 1)) * Q) & 3);
+    auto tile = [&](int kk) { return aos_smem + ((kk + 1) % NS) * T::slot_words + phase; };  // kk >= -1
+    // prologue: planes kb-1, kb, kb+1, and kb+2 ahead when the ring has room
+    for (int kk = kb - 1; kk <= kb + 1; ++kk) aos_load_plane<Q>(A, tile(kk), kk, a0, b0);
+    cp_async_commit();
+    if (NS == 4 && kb + 2 <= ke) aos_load_plane<Q>(A, tile(kb + 2), kb + 2, a0, b0);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const bool a_lo_w = A.wall_a && a == 0, a_hi_w = A.wall_a && a == A.na - 1;
+    const bool b_lo_w = A.wall_b && b == 0, b_hi_w = A.wall_b && b == A.nb - 1;
+    const int own = (ty + 1) * T::pitch + (tx + 1) * Q;
+    for (int k = kb; k < ke; ++k) {
+        const int kg = A.kg0 + k;
+        using P = float;
+        P dg_mass = P(0), dg_v2 = P(0);
+        int dg_bad = -1;
+        R f[Q];
+        if (live) {
+            const bool k_lo = A.wall_k && kg == 0, k_hi = A.wall_k && kg == A.nk - 1;
+            const float* pm = tile(k - 1);
+            const float* p0 = tile(k);
+            const float* pp = tile(k + 1);
+            static_for<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr int ex = L::e(i, 0), ey = L::e(i, 1), ez = L::e(i, 2);
+                bool oob = false;
+                if constexpr (ex > 0) oob = oob || a_lo_w;
+                if constexpr (ex < 0) oob = oob || a_hi_w;
+                if constexpr (ey > 0) oob = oob || b_lo_w;
+                if constexpr (ey < 0) oob = oob || b_hi_w;
+                if constexpr (ez > 0) oob = oob || k_lo;
+                if constexpr (ez < 0) oob = oob || k_hi;
+                const float* plane = ez > 0 ? pm : (ez < 0 ? pp : p0);
+                constexpr int shift = -ey * T::pitch - ex * Q + i;
+                R v = oob ? p0[own + L::opp(i)] : plane[own + shift];
+                if constexpr (ez < 0) {
+                    if (A.has_lid && k_hi) v = Arith<R, false>::add(v, A.lid[i]);
+                }
+                f[i] = v;
+            });
+            bool ok = true;
+            R rho, u[3], dr = R(0);
+            bgk_relax_shifted<L, R>(f, A.omega, A.keep, rho, u, ok, DIAG ? &dr : nullptr);
+            if (!ok) atomicMin(A.error_flag, A.step_base ? *A.step_base + A.step : A.step);
+            if constexpr (DIAG) probe_voxel<L, R, false, P>(f, rho, dr, u, dg_mass, dg_v2, dg_bad);
+        }
+        if constexpr (DIAG) {
+            if (live && dg_bad >= 0) {
+                const unsigned long long canon = (unsigned long long)kg * A.s + (unsigned long long)b * A.na + a;
+                atomicMin(A.diag_bad, (canon << 5) | (unsigned long long)dg_bad);
+            }
+            P pm = dg_mass, pv = dg_v2;
+            const unsigned lanes = __ballot_sync(0xffffffffu, live);
+            for (int o = 16; o > 0; o >>= 1) {
+                pm += __shfl_xor_sync(0xffffffffu, pm, o);
+                pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
+            }
+            if (lane == 0 && lanes) {
+                const double mass = double(pm) + double(__popc(lanes));
+                const unsigned long long row =
+                    ((unsigned long long)kg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+                diag_commit(A.diag_acc, row * kAosTY + ty, mass, double(pv));
+            }
+        }
+        // the output records go through the slot of plane k-1 (read by no
+        // one after this barrier), 32 records x Q words per row, 16-byte phase 0
+        float* out_s = aos_smem + ((k + NS) % NS) * T::slot_words;
+        __syncthreads();
+        if (live) {
+            static_for<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                out_s[threadIdx.x * Q + i] = f[i];
+            });
+        }
+        __syncthreads();
+        {
+            // output rows: contiguous spans of (records x Q) words; the shared
+            // layers also store them into the neighbour's halo plane
+            // (zero-copy halo: AoS sends every population)
+            const int nw = min(kAosTX, A.na - a0) * Q;
+            const int bb = b0 + warp;
+            if (bb < A.nb) {
+                const long long cross = ((long long)bb * A.na + a0) * Q;
+                const float* src = out_s + warp * kAosTX * Q;
+                aos_row_store(A.out + (long long)(k + 1) * A.s * Q + cross, src, nw, lane);
+                if (k == 0 && A.up_out) aos_row_store(A.up_out + A.up_plane[0] + cross, src, nw, lane);
+                if (k == A.n - 1 && A.low_out) aos_row_store(A.low_out + A.low_plane[0] + cross, src, nw, lane);
+                if (A.remote_fence && ((k == 0 && A.up_out) || (k == A.n - 1 && A.low_out))) __threadfence_system();
+            }
+        }
+        __syncthreads();  // the staging slot is free: the next plane goes there
+        const int next = k + NS - 1;  // k+3 (4 slots, k+2 already in flight) or k+2 (3 slots)
+        if (next <= ke && next <= A.n) aos_load_plane<Q>(A, tile(next), next, a0, b0);
+        cp_async_commit();
+        if constexpr (NS == 4) cp_async_wait<1>();  // plane k+2 landed (k+3 may be in flight)
+        else cp_async_wait<0>();
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+}
+
 constexpr int kOpIdentity = int(Operator::Identity);
 constexpr int kOpJacobi2 = int(Operator::Jacobi2);
 
@@ -693,12 +925,37 @@ struct DenseOps {
         const dim3 grid((g.na + kBlock - 1) / kBlock, g.nb, k_count);
         A.diag_acc = diag ? diag->acc : nullptr;
         A.diag_bad = diag ? diag->bad : nullptr;
+        using T = std::true_type;
+        using F = std::false_type;
+        if constexpr (std::is_same_v<R, float> && L::dim == 3) {
+            // AoS fp32 3D without periodic wrap: the plane-tile kernel
+            if (aos && !wrap && g.na >= 1) {
+                constexpr int smem = AosTile<Q>::smem_bytes;
+                auto launch = [&](auto kern) {
+                    // opt in to the large dynamic shared memory (per kernel and device; a host-side call)
+                    VOXL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                    int kb = k_first, zs = kAosChunk, chunk = kAosChunk, ke = k_first + k_count, zc;
+                    if (k_step != 1 && k_count > 1) {  // the shared layers: one plane per CTA
+                        zs = k_step;
+                        chunk = 1;
+                        ke = k_first + (k_count - 1) * k_step + 1;
+                        zc = k_count;
+                    } else {
+                        zc = (k_count + kAosChunk - 1) / kAosChunk;
+                    }
+                    const dim3 tg((g.na + kAosTX - 1) / kAosTX, (g.nb + kAosTY - 1) / kAosTY, zc);
+                    kern<<<tg, kAosThreads, smem, st>>>(A, kb, zs, chunk, ke);
+                };
+                if (diag) launch(dense_aos_tiled_kernel<L, true>);
+                else launch(dense_aos_tiled_kernel<L, false>);
+                VOXL_CUDA(cudaGetLastError());
+                return;
+            }
+        }
         auto go = [&](auto aos_c, auto wrap_c, auto diag_c) {
             dense_step_kernel<L, R, Exact, decltype(aos_c)::value, AXIS, decltype(wrap_c)::value,
                               decltype(diag_c)::value><<<grid, kBlock, 0, st>>>(A);
         };
-        using T = std::true_type;
-        using F = std::false_type;
         auto with_diag = [&](auto a_c, auto w_c) { diag ? go(a_c, w_c, T{}) : go(a_c, w_c, F{}); };
         if (aos) wrap ? with_diag(T{}, T{}) : with_diag(T{}, F{});
         else wrap ? with_diag(F{}, T{}) : with_diag(F{}, F{});

@@ -396,15 +396,11 @@ struct SparseOps {
         return A;
     }
 
-    /// Resident CTAs of a kernel on the whole GPU (the persistent scan grid).
-    template <class K>
-    static int resident_ctas(K kernel, int threads) {
+    static int sm_count() {
         int dev = 0, sms = 0;
         VOXL_CUDA(cudaGetDevice(&dev));
         VOXL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        int per = 0;
-        VOXL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0));
-        return std::max(1, per) * sms;
+        return sms;
     }
 
     template <int E>
@@ -413,11 +409,14 @@ struct SparseOps {
         constexpr int S = kSplit<E>;
         dim3 grid(nblocks * S);
         const dim3 block(E * E * E / S);
-        if (A.scan_blocks > 0) {  // persistent grid over the bitmask sweep's blocks
-            const int r = A.diag_acc ? resident_ctas(sparse_step_kernel<L, R, Exact, E, kHeavy, true>, block.x)
-                                     : resident_ctas(sparse_step_kernel<L, R, Exact, E, kHeavy, false>, block.x);
+        if (A.scan_blocks > 0) {
+            // persistent grid over the bitmask sweep's blocks: one CTA per SM.
+            // A full resident grid (4 x 64-register CTAs per SM) would take
+            // every register of the GPU for the sweep's whole life and push
+            // the concurrent light sweep behind it (3.53 ms per 512^3 step
+            // measured, against 3.20 for DisagMem).
             A.scan_blocks = nblocks;
-            grid = dim3(std::min(nblocks, r / S) * S);
+            grid = dim3(std::min(nblocks * S, std::max(S, sm_count() / S * S)));
         }
         if (A.diag_acc) {
             if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy, true><<<grid, block, 0, st>>>(A);

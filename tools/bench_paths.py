@@ -91,7 +91,10 @@ def dense(args):
 
     n = args.n
     cases = [("D3Q19", "fp32", "DisagSoA", 1), ("D3Q19", "fp32", "SoA", 1), ("D3Q19", "fp32", "AoS", 1),
-             ("D3Q19", "fp32", "DisagSoA", 8), ("D3Q27", "fp32", "DisagSoA", 1), ("D3Q19", "fp64", "DisagSoA", 1)]
+             ("D3Q19", "fp32", "DisagSoA", 8), ("D3Q19", "fp32", "AoS", 8), ("D3Q27", "fp32", "DisagSoA", 1),
+             ("D3Q27", "fp32", "AoS", 1), ("D3Q19", "fp64", "DisagSoA", 1)]
+    if args.layouts:
+        cases = [c for c in cases if c[2] in args.layouts.split(",")]
     for lat, prec, layout, parts in cases:
         q = 19 if lat == "D3Q19" else 27
         bpl = 2 * q * (4 if prec == "fp32" else 8)
@@ -117,5 +120,6 @@ if __name__ == "__main__":
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--lattice", default="D3Q19", choices=["D3Q19", "D3Q27"], help="sparse / multires lattice")
+    ap.add_argument("--layouts", default="", help="dense: only these layouts (comma-separated)")
     a = ap.parse_args()
     {"sparse": sparse, "multires": multires, "dense": dense}[a.path](a)

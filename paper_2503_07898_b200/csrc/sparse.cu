@@ -41,7 +41,8 @@ struct SparseArgs {
     int block_begin;
     const std::uint8_t* bitmask;  // DisagBitmask: skip blocks whose bit != want
     int bitmask_want;
-    int scan_blocks;              // > 0: persistent grid striding over this many blocks (bitmask sweep)
+    int scan_span;                // > 0 (bitmask sweep): each CTA pair walks this many consecutive blocks
+    int scan_blocks;              //   of the sweep's scan_blocks
     int vel_source;
     const std::int32_t* meta_index;  // per slot (DisagBitmask)
     const R* compact_meta;           // 3 per boundary voxel (DisagBitmask)
@@ -163,13 +164,17 @@ template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 ? (MODE == 0 ? block_min_ctas(L::Q) : VOXL_HEAVY_MINB) : 1)
     sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
     constexpr int S = kSplit<E>;
-    if (A.scan_blocks > 0) {
+    if (A.scan_span > 0) {
         // DisagBitmask sweep (sparse.cpp:369-380): every block is visited and
         // skipped unless its bit matches. A CTA per block would spend most of
         // the boundary sweep dispatching CTAs that exit at once (0.44 of
-        // 0.66 ms at 512^3), so this sweep strides a persistent grid over the
-        // blocks and skips with one broadcast byte load.
-        for (int b = A.block_begin + int(blockIdx.x) / S; b < A.block_begin + A.scan_blocks; b += int(gridDim.x) / S) {
+        // 0.66 ms at 512^3), so each CTA walks a span of consecutive blocks
+        // and skips with one broadcast byte load per block. (A persistent
+        // grid was measured worse: its resident 64-register CTAs starve the
+        // concurrent light sweep for the whole step.)
+        const int lo = A.block_begin + int(blockIdx.x) / S * A.scan_span;
+        const int hi = min(lo + A.scan_span, A.block_begin + A.scan_blocks);
+        for (int b = lo; b < hi; ++b) {
             if (int(A.bitmask[b]) != A.bitmask_want) continue;  // CTA-uniform
             sparse_block<L, R, Exact, E, MODE, DIAG>(A, b, int(blockIdx.x) % S);
             __syncthreads();  // shared neighbourhood tables are rewritten by the next block
@@ -380,6 +385,10 @@ __global__ void sparse_probe_kernel(const R* buf, const std::int64_t* slots, lon
 }
 
 constexpr int kSpProbeBlocks = 592;
+#ifndef VOXL_BITMASK_SPAN
+#define VOXL_BITMASK_SPAN 64
+#endif
+constexpr int kBitmaskSpan = VOXL_BITMASK_SPAN;  // blocks per CTA pair of the bitmask boundary sweep
 
 template <class L, class R, bool Exact>
 struct SparseOps {
@@ -396,12 +405,6 @@ struct SparseOps {
         return A;
     }
 
-    static int sm_count() {
-        int dev = 0, sms = 0;
-        VOXL_CUDA(cudaGetDevice(&dev));
-        VOXL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        return sms;
-    }
 
     template <int E>
     static void launch_e(SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
@@ -409,14 +412,9 @@ struct SparseOps {
         constexpr int S = kSplit<E>;
         dim3 grid(nblocks * S);
         const dim3 block(E * E * E / S);
-        if (A.scan_blocks > 0) {
-            // persistent grid over the bitmask sweep's blocks: one CTA per SM.
-            // A full resident grid (4 x 64-register CTAs per SM) would take
-            // every register of the GPU for the sweep's whole life and push
-            // the concurrent light sweep behind it (3.53 ms per 512^3 step
-            // measured, against 3.20 for DisagMem).
+        if (A.scan_span > 0) {  // bitmask sweep: one CTA pair per span of blocks
             A.scan_blocks = nblocks;
-            grid = dim3(std::min(nblocks * S, std::max(S, sm_count() / S * S)));
+            grid = dim3((nblocks + A.scan_span - 1) / A.scan_span * S);
         }
         if (A.diag_acc) {
             if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy, true><<<grid, block, 0, st>>>(A);
@@ -681,8 +679,9 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
             case Strategy::DisagBitmask: {
                 // both sweeps scan every block and skip the other class's
                 // blocks by bitmask (sparse.cpp:369-380); they write disjoint
-                // blocks, so the heavy sweep runs on the side stream
-                // concurrently with the light one, as in DisagMem
+                // blocks, so the boundary sweep (spans of blocks per CTA,
+                // kBitmaskSpan) runs on the high-priority side stream
+                // concurrently with the light sweep, as in DisagMem
                 A.vel_source = kVelIndirect;
                 A.block_begin = 0;
                 A.bitmask = d_bitmask_;
@@ -693,11 +692,11 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
                     VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
                 }
                 A.bitmask_want = 1;
-                A.scan_blocks = 1;  // persistent strided sweep (launch_e sizes it)
+                A.scan_span = kBitmaskSpan;
                 if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], hs));
                 Ops::launch(edge, A, kHeavy, nb, hs);
                 if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], hs));
-                A.scan_blocks = 0;
+                A.scan_span = 0;
                 A.bitmask_want = 0;
                 if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
                 Ops::launch(edge, A, kLight, nb, stream_);

@@ -178,6 +178,16 @@ int voxl_dense_step_probe(voxl_dense* h, voxl_diag* out);
  *  macroscopic: non-positive density" / "... instability at step N, voxel V,
  *  population I", N = the engine's step index) and *completed = the rows filled. */
 int voxl_dense_step_probe_n(voxl_dense* h, int n, voxl_diag* rows, int* completed);
+/** Observed counterpart of TraceLog (partition.hpp:76-90): while enabled, every
+ *  phase the engine launches (per partition: "step", or "interior" + "shared" on
+ *  two streams in the multi-device / multi-process schedules, "halo_copy" in copy
+ *  mode) is bracketed by CUDA events; disabling clears the record. NVTX ranges
+ *  name every phase launch regardless. */
+int voxl_dense_trace_enable(voxl_dense* h, int on);
+/** The record as JSON: [{"step", "stage", "phase", "partition", "device", "stream",
+ *  "begin_ms", "end_ms"}, ...] in launch order, times from the first event on the
+ *  same device (waits for the recorded steps). */
+int voxl_dense_trace_json(voxl_dense* h, char* out, int64_t cap, int64_t* len);
 /** Ledger records of one step in the reference's order (partition.cpp:163-206). */
 int voxl_dense_ledger(voxl_dense* h, int step, voxl_transfer_record* out, int cap, int* count);
 /** The same records from a descriptor alone (no device needed). */

@@ -106,6 +106,8 @@ def _load():
         "voxl_dense_probe": ([vp, C.POINTER(Diag)], C.c_int),
         "voxl_dense_step_probe": ([vp, C.POINTER(Diag)], C.c_int),
         "voxl_dense_step_probe_n": ([vp, C.c_int, C.POINTER(Diag), C.POINTER(C.c_int)], C.c_int),
+        "voxl_dense_trace_enable": ([vp, C.c_int], C.c_int),
+        "voxl_dense_trace_json": ([vp, cp, i64, C.POINTER(i64)], C.c_int),
         "voxl_dense_ledger": ([vp, C.c_int, vp, C.c_int, C.POINTER(C.c_int)], C.c_int),
         "voxl_dense_plan_ledger": ([C.POINTER(DenseDesc), C.c_int, vp, C.c_int, C.POINTER(C.c_int)], C.c_int),
         "voxl_dense_layout_json": ([vp, C.c_int, cp, i64, C.POINTER(i64)], C.c_int),

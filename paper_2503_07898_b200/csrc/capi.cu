@@ -355,6 +355,20 @@ int voxl_dense_step_probe_n(voxl_dense* h, int n, voxl_diag* rows, int* complete
     });
 }
 
+int voxl_dense_trace_enable(voxl_dense* h, int on) {
+    return guarded([&] {
+        need("voxl_dense_trace_enable", h);
+        h->eng->trace_enable(on != 0);
+    });
+}
+
+int voxl_dense_trace_json(voxl_dense* h, char* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        need("voxl_dense_trace_json", h);
+        put_text(h->eng->trace_json(), out, cap, len);
+    });
+}
+
 int voxl_dense_probe(voxl_dense* h, voxl_diag* out) {
     return guarded([&] {
         need("voxl_dense_probe", h, out);

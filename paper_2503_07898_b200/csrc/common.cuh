@@ -45,7 +45,8 @@ inline int log2_exact(long long v) {
 /// Resident 256-thread CTAs per SM requested from ptxas for the fp32 8^3-block
 /// kernels (block-sparse light kernel, multires pull kernel): 6 caps D3Q19 at
 /// 40 registers. D3Q27 (27 live populations) spills at 40; measured at 512^3
-/// (tools/gpu_q27_variants.sh, GLUPS sparse disag_mem / multires fused):
+/// (a -DVOXL_BLOCK_MINB27 sweep, tools/build_lib_variant.sh + gpu_lib_variants.sh;
+/// GLUPS sparse disag_mem / multires fused):
 /// 6 CTAs 26.1 / 27.1, 5 CTAs 27.9 / 27.8, 4 CTAs 25.9 / 27.7.
 #ifndef VOXL_BLOCK_MINB19
 #define VOXL_BLOCK_MINB19 6

@@ -34,7 +34,7 @@ namespace {
 #ifndef VOXL_DENSE_MINB
 #define VOXL_DENSE_MINB 0
 #endif
-// D3Q27 fp32 at 512^3 (tools/gpu_q27_dense_variants.sh, ms per step / per
+// D3Q27 fp32 at 512^3 (-DVOXL_DENSE_MINB27 sweep, ms per step / per
 // step_probe): plain step unconstrained (54 registers, 4 CTAs/SM) 4.58, with
 // 5 CTAs/SM 4.72, 4 CTAs/SM at 48 registers 4.73-4.74; fused-probe step with
 // 6 CTAs/SM (40 registers, 100 B spill) 5.17, with 5 CTAs/SM 4.77.
@@ -45,7 +45,7 @@ namespace {
 #define VOXL_DIAG_MINB27 5
 #endif
 // 256-thread CTAs: +4 % DRAM throughput over 128 on B200 (tools/micro/membw.cu).
-// Sweep at 512^3 (tools/gpu_dense_variants.sh, GLUPS): 256 threads 42.70-42.82,
+// Sweep at 512^3 (-DVOXL_DENSE_BLOCK / MINB sweep, GLUPS): 256 threads 42.70-42.82,
 // 512 42.54-42.66, 512 with 3 CTAs/SM 42.66, 1024 28.2, 256 with 5 CTAs/SM 41.68.
 constexpr int kBlock = VOXL_DENSE_BLOCK;
 #ifndef VOXL_DIAG_MINB
@@ -92,7 +92,7 @@ __device__ __forceinline__ int group_of(int k, int n) {
     return k == -1 ? 0 : (k == 0 ? 1 : (k == n - 1 ? 3 : (k == n ? 4 : 2)));
 }
 
-// Cache hints on the fast path, measured at 512^3 (tools/gpu_dense_hints.sh,
+// Cache hints on the fast path, measured at 512^3 (-DVOXL_LD_HINT / ST_HINT sweep,
 // GLUPS): plain 42.90, st.global.cs stores 42.29, ld.global.lu loads 40.46,
 // both 38.7 -- the x-shifted pulls reuse lines through L2, so plain wins.
 #ifndef VOXL_ST_HINT  // fast-path stores: 0 plain st.global, 1 st.global.cs (evict-first streaming)
@@ -1645,10 +1645,12 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     const int n = decomp_.thickness(p);
     // I: interior(t)
     VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_shared_[prev], 0));
-    dispatch(cfg_, [&](auto ops) {
-        using Ops = decltype(ops);
-        Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr, wrap,
-                         steps_done_, error_flag_, 1, 1, n - 2, stream_, false, diag);
+    trace_.phase(steps_done_, 1, "interior", p, cur_device(), "interior", stream_, [&] {
+        dispatch(cfg_, [&](auto ops) {
+            using Ops = decltype(ops);
+            Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr, wrap,
+                             steps_done_, error_flag_, 1, 1, n - 2, stream_, false, diag);
+        });
     });
     VOXL_CUDA(cudaEventRecord(ev_interior_[par], stream_));
     // S: wait -> shared(t) -> signal
@@ -1659,10 +1661,12 @@ void DenseEngine::launch_step_distributed(DiagTarget* diag) {
     }
     void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
     void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
-    dispatch(cfg_, [&](auto ops) {
-        using Ops = decltype(ops);
-        Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out, wrap,
-                         steps_done_, error_flag_, 0, n - 1, 2, shared_stream_, true, diag);
+    trace_.phase(steps_done_, 2, "shared", p, cur_device(), "shared", shared_stream_, [&] {
+        dispatch(cfg_, [&](auto ops) {
+            using Ops = decltype(ops);
+            Ops::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out, wrap,
+                             steps_done_, error_flag_, 0, n - 1, 2, shared_stream_, true, diag);
+        });
     });
     if (zero_copy) {
         signal_flags_kernel<<<1, 32, 0, shared_stream_>>>(remote_flag_up_, remote_flag_low_, t + 1);
@@ -1698,13 +1702,17 @@ void DenseEngine::launch_step(DiagTarget* diag) {
         void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
         void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
         const int n = decomp_.thickness(p);
-        dispatch(cfg_, [&](auto ops) {
-            decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out,
-                                       low_out, wrap, steps_done_, error_flag_, 0, 1, n, stream_, false, diag);
+        // one kernel per partition: every plane, the shared layers storing
+        // their crossing populations into the neighbours' halos (zero copy)
+        trace_.phase(steps_done_, 1, "step", p, cur_device(), "engine", stream_, [&] {
+            dispatch(cfg_, [&](auto ops) {
+                decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out,
+                                           low_out, wrap, steps_done_, error_flag_, 0, 1, n, stream_, false, diag);
+            });
         });
     }
     cur_ = out;
-    if (!zero_copy) halo_copy(0);
+    if (!zero_copy) trace_.phase(steps_done_, 2, "halo_copy", -1, cur_device(), "engine", stream_, [&] { halo_copy(0); });
     ++steps_done_;
 }
 
@@ -1754,9 +1762,12 @@ void DenseEngine::launch_step_multi(int step_off, bool first, const DiagTarget* 
         DeviceGuard g(parts_[p].device);
         VOXL_CUDA(cudaStreamWaitEvent(x.interior, first ? ready(p) : x.ev_s[prev], 0));
         const int n = decomp_.thickness(p);
-        dispatch(cfg_, [&](auto ops) {
-            decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr, nullptr,
-                                       wrap, step_arg, error_flag_, 1, 1, n - 2, x.interior, false, diag_of(p), sb);
+        trace_.phase(steps_done_, 1, "interior", p, parts_[p].device, "interior", x.interior, [&] {
+            dispatch(cfg_, [&](auto ops) {
+                decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], nullptr,
+                                           nullptr, wrap, step_arg, error_flag_, 1, 1, n - 2, x.interior, false,
+                                           diag_of(p), sb);
+            });
         });
         VOXL_CUDA(cudaEventRecord(x.ev_i[par], x.interior));
     }
@@ -1775,17 +1786,23 @@ void DenseEngine::launch_step_multi(int step_off, bool first, const DiagTarget* 
         const int n = decomp_.thickness(p);
         void* up_out = (zero_copy && up >= 0) ? parts_[up].buf[out] : nullptr;
         void* low_out = (zero_copy && low >= 0) ? parts_[low].buf[out] : nullptr;
-        dispatch(cfg_, [&](auto ops) {
-            decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out, low_out,
-                                       wrap, step_arg, error_flag_, 0, n - 1, 2, x.shared, false, diag_of(p), sb);
+        trace_.phase(steps_done_, 2, "shared", p, parts_[p].device, "shared", x.shared, [&] {
+            dispatch(cfg_, [&](auto ops) {
+                decltype(ops)::launch_step(cfg_, decomp_, maps_, p, parts_[p].buf[in], parts_[p].buf[out], up_out,
+                                           low_out, wrap, step_arg, error_flag_, 0, n - 1, 2, x.shared, false,
+                                           diag_of(p), sb);
+            });
         });
         if (cfg_.halo == HaloMode::Copy)
-            for (const auto& r : ledger_records(0)) {
-                if (r.src != p) continue;
-                char* dst = static_cast<char*>(parts_[r.dst].buf[out]) + r.dst_span.base * esize_;
-                const char* src = static_cast<const char*>(parts_[r.src].buf[out]) + r.src_span.base * esize_;
-                VOXL_CUDA(cudaMemcpyAsync(dst, src, std::size_t(r.elements) * esize_, cudaMemcpyDefault, x.shared));
-            }
+            trace_.phase(steps_done_, 2, "halo_copy", p, parts_[p].device, "shared", x.shared, [&] {
+                for (const auto& r : ledger_records(0)) {
+                    if (r.src != p) continue;
+                    char* dst = static_cast<char*>(parts_[r.dst].buf[out]) + r.dst_span.base * esize_;
+                    const char* src = static_cast<const char*>(parts_[r.src].buf[out]) + r.src_span.base * esize_;
+                    VOXL_CUDA(
+                        cudaMemcpyAsync(dst, src, std::size_t(r.elements) * esize_, cudaMemcpyDefault, x.shared));
+                }
+            });
     }
     if (nccl_) {
         // every partition's sends and receives in one group (one thread drives
@@ -1858,7 +1875,7 @@ void DenseEngine::enqueue_multi(int n, const DiagTarget* dev_diag, bool use_grap
     if (n <= 0) return;
     int done = 0;
     const int G = cfg_.graph_steps;
-    if (use_graph && !dev_diag && !nccl_ && G > 0 && n >= G) {
+    if (use_graph && !dev_diag && !nccl_ && !trace_.enabled() && G > 0 && n >= G) {
         // the graph's kernels report a failing step as *step_base + offset
         const int base = steps_done_;
         VOXL_CUDA(cudaMemcpyAsync(step_base_, &base, sizeof(int), cudaMemcpyHostToDevice, stream_));

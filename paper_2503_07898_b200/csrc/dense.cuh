@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "grid.hpp"
+#include "phase_trace.cuh"
 
 namespace voxl_b200 {
 
@@ -105,6 +106,10 @@ public:
     int q() const { return q_; }
     std::int64_t owned_voxels() const;  // voxels of the locally owned partitions
     int steps_done() const { return steps_done_; }
+    /// The executed schedule (phase_trace.cuh): record phases of the steps
+    /// enqueued while enabled; json() waits for them.
+    void trace_enable(bool on) { trace_.enable(on); }
+    std::string trace_json() { return trace_.json(); }
 
     /// Canonical fp64 state (x fastest, component innermost) for the whole
     /// domain (fill_canonical / to_canonical, partition.cpp:123-161). With a
@@ -186,6 +191,12 @@ public:
     bool multi_device() const { return multi_; }
 
 private:
+    PhaseTrace trace_;
+    static int cur_device() {
+        int d = 0;
+        VOXL_CUDA(cudaGetDevice(&d));
+        return d;
+    }
     DenseConfig cfg_;
     int q_ = 19;
     int axis_ = 2;

@@ -5,6 +5,7 @@
 #include "canon_io.cuh"
 #include "block_probe.cuh"
 #include "diag_ring.cuh"
+#include "phase_trace.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -999,13 +1000,18 @@ void MultiResEngine::transfer(double* host, bool to_device, unsigned long long* 
     VOXL_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void MultiResEngine::mark_begin(int, cudaEvent_t* b, cudaStream_t s) {
+void MultiResEngine::mark_begin(int cls, cudaEvent_t* b, cudaStream_t s) {
+    // NVTX range per launch class (phase_trace.cuh), closed by mark_end
+    static const char* const kNames[] = {"voxl mres collide", "voxl mres stream", "voxl mres fused",
+                                         "voxl mres transition"};
+    nvtxRangePushA(kNames[cls & 3]);
     if (!events_) return;
     VOXL_CUDA(cudaEventCreate(b));
     VOXL_CUDA(cudaEventRecord(*b, s ? s : stream_));
 }
 
 void MultiResEngine::mark_end(int cls, cudaEvent_t b, cudaStream_t s) {
+    nvtxRangePop();
     if (!events_) return;
     cudaEvent_t e;
     VOXL_CUDA(cudaEventCreate(&e));

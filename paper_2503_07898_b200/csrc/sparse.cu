@@ -15,6 +15,7 @@
 #include "canon_io.cuh"
 #include "block_probe.cuh"
 #include "diag_ring.cuh"
+#include "phase_trace.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -151,7 +152,7 @@ constexpr int kSplit = E == 8 ? 2 : 1;
 
 // Heavy (regularized) kernel: 4 resident 256-thread CTAs per SM (64
 // registers, no spill for D3Q19) instead of the unconstrained 72 registers /
-// 3 CTAs. Measured at 512^3 disag_mem (tools/gpu_heavy_variants.sh): D3Q19
+// 3 CTAs. Measured at 512^3 disag_mem (-DVOXL_HEAVY_MINB sweep): D3Q19
 // 40.88 -> 41.21 GLUPS, D3Q27 28.01 -> 28.69 (the boundary kernel shares the
 // GPU with the light one, so its occupancy sets how much it slows it).
 #ifndef VOXL_HEAVY_MINB
@@ -427,6 +428,8 @@ struct SparseOps {
     }
 
     static void launch(int edge, SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
+        NvtxRange r(mode == kHeavy ? (A.scan_span ? "voxl sparse boundary sweep" : "voxl sparse boundary")
+                                   : (A.bitmask ? "voxl sparse light sweep" : "voxl sparse light"));
         switch (edge) {
             case 4: launch_e<4>(A, mode, nblocks, st); break;
             case 8: launch_e<8>(A, mode, nblocks, st); break;

@@ -224,6 +224,15 @@ class DenseEngine:
         the steps before it."""
         return _capi.probe_rows(lib.voxl_dense_step_probe_n, self._h, n)
 
+    def trace(self, on: bool = True) -> None:
+        """Record the executed schedule of the steps enqueued from now on
+        (CUDA-event-timed phases); trace(False) stops and clears it."""
+        check(lib.voxl_dense_trace_enable(self._h, 1 if on else 0))
+
+    def trace_json(self) -> str:
+        """The recorded phases as JSON (see voxl_dense_trace_json)."""
+        return _capi.text(lib.voxl_dense_trace_json, self._h)
+
     def ledger(self, step: int):
         return _records(lib.voxl_dense_ledger, self._h, step)
 

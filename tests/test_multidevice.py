@@ -156,3 +156,50 @@ def test_two_devices_bitwise(halo):
     ref = O.port_dense_run("D3Q19", dom, 0.56, "lid_driven_cavity", (0.05, 0, 0), 20)
     out = _run(20, init, dom, precision="fp64", partitions=parts, halo_mode=halo, devices=list(range(parts)))
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("devices,halo", [(None, "zero_copy"), (None, "copy"), ([0, 0, 0], "zero_copy"),
+                                          ([0, 0, 0], "copy")])
+def test_observed_trace_lists_the_executed_schedule(devices, halo):
+    """The observed TraceLog (voxl_dense_trace_json): one record per launched
+    phase, in launch order, with device-measured, ordered times -- the
+    single-stream schedule launches one "step" kernel per partition (plus a
+    "halo_copy" phase in copy mode), the multi-device OCC schedule "interior"
+    and "shared" kernels per partition on their two streams."""
+    import json
+
+    dom = (16, 12, 24)
+    kw = dict(devices=devices) if devices else {}
+    e = V.DenseEngine("D3Q19", dom, 0.6, "lid_driven_cavity", (0.05, 0, 0), partitions=3, halo_mode=halo, **kw)
+    e.set_equilibrium(1.0, (0.0, 0.0, 0.0))
+    e.trace(True)
+    e.step(2)
+    rec = json.loads(e.trace_json())
+    e.trace(False)
+    assert json.loads(e.trace_json()) == []
+    e.close()
+    if devices is None:
+        want = []
+        for s in range(2):
+            want += [(s, 1, "step", p) for p in range(3)]
+            if halo == "copy":
+                want.append((s, 2, "halo_copy", -1))
+    else:
+        want = []
+        for s in range(2):
+            want += [(s, 1, "interior", p) for p in range(3)]
+            for p in range(3):
+                want.append((s, 2, "shared", p))
+                if halo == "copy":
+                    want.append((s, 2, "halo_copy", p))
+    assert [(r["step"], r["stage"], r["phase"], r["partition"]) for r in rec] == want
+    for r in rec:
+        assert 0.0 <= r["begin_ms"] <= r["end_ms"]
+        assert r["device"] == 0
+    # a partition's step s+1 work starts after its step s work ended (same stream order)
+    by = {}
+    for r in rec:
+        by.setdefault((r["phase"], r["partition"]), []).append(r)
+    for rs in by.values():
+        for a, b in zip(rs, rs[1:]):
+            assert b["begin_ms"] >= a["end_ms"] - 1e-3

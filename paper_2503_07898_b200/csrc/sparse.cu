@@ -16,11 +16,13 @@
 #include "block_probe.cuh"
 #include "diag_ring.cuh"
 #include "phase_trace.cuh"
+#include "tma.cuh"
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 namespace voxl_b200 {
 
@@ -42,6 +44,7 @@ struct SparseArgs {
     int block_begin;
     const std::uint8_t* bitmask;  // DisagBitmask: skip blocks whose bit != want
     int bitmask_want;
+    int tma;                      // host: one block per CTA staged by a bulk copy (sparse_tma_kernel)
     int scan_span;                // > 0 (bitmask sweep): each CTA pair walks this many consecutive blocks
     int scan_blocks;              //   of the sweep's scan_blocks
     int vel_source;
@@ -158,8 +161,9 @@ constexpr int kSplit = E == 8 ? 2 : 1;
 #ifndef VOXL_HEAVY_MINB
 #define VOXL_HEAVY_MINB 4
 #endif
-template <class L, class R, bool Exact, int E, int MODE, bool DIAG>
-__device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b, int half);
+template <class L, class R, bool Exact, int E, int MODE, bool DIAG, bool TMA = false>
+__device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b, int half, const R* s_own = nullptr,
+                                             unsigned long long* bar = nullptr, unsigned parity = 0);
 
 template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 ? (MODE == 0 ? block_min_ctas(L::Q) : VOXL_HEAVY_MINB) : 1)
@@ -187,8 +191,47 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 
     sparse_block<L, R, Exact, E, MODE, DIAG>(A, b, int(blockIdx.x) % S);
 }
 
+/// Bulk-copy block staging (opt-in, VOXL_SPARSE_TMA=1): one block per CTA
+/// (E^3 threads); the block's Q population planes -- one contiguous span of
+/// Q * E^3 values (BlockField layout) -- land in shared memory by a single
+/// cp.async.bulk (tma.cuh) that overlaps the CTA's metadata prologue, and
+/// own-block pulls (all but the face-crossing ones: 81 % at E = 8, D3Q19)
+/// read shared memory. Same arithmetic as sparse_step_kernel (bitwise equal
+/// results). Measured slower than the register-pull kernel at 512^3 (light
+/// kernel under ncu 3.20 vs 2.94 ms; a persistent, double-buffered variant
+/// 4.10 ms): a CTA idles for its copy's full latency before it computes, and
+/// 3 x 512-thread CTAs per SM hide that worse than 6 x 256-thread CTAs with
+/// 19 loads each in flight. Kept as the measured alternative.
+#ifndef VOXL_TMA_MINB_LIGHT
+#define VOXL_TMA_MINB_LIGHT 3
+#endif
+#ifndef VOXL_TMA_MINB_HEAVY
+#define VOXL_TMA_MINB_HEAVY 2
+#endif
 template <class L, class R, bool Exact, int E, int MODE, bool DIAG>
-__device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b, int half) {
+__global__ void __launch_bounds__(E* E* E, MODE == kHeavy ? VOXL_TMA_MINB_HEAVY : (L::Q == 27 ? 2 : VOXL_TMA_MINB_LIGHT))
+    sparse_tma_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
+    constexpr int Q = L::Q, BV = E * E * E;
+    extern __shared__ __align__(128) unsigned char sp_tma_smem[];
+    R* s_own = reinterpret_cast<R*>(sp_tma_smem);
+    __shared__ __align__(8) unsigned long long s_bar;
+    const int b = A.block_begin + int(blockIdx.x);
+    if (A.bitmask && int(A.bitmask[b]) != A.bitmask_want) return;  // CTA-uniform skip, before any copy
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        mbar_arrive_expect_tx(&s_bar, unsigned(Q * BV * sizeof(R)));
+        tma_bulk_g2s(s_own, A.cur + (long long)b * Q * BV, unsigned(Q * BV * sizeof(R)), &s_bar);
+    }
+    // sparse_block's first __syncthreads publishes the initialised barrier
+    sparse_block<L, R, Exact, E, MODE, DIAG, true>(A, b, 0, s_own, &s_bar, 0u);
+    // the copy must complete before the CTA (and its shared memory) retires,
+    // also when every thread of the block returned early
+    if (threadIdx.x == 0) mbar_wait(&s_bar, 0);
+}
+
+template <class L, class R, bool Exact, int E, int MODE, bool DIAG, bool TMA>
+__device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b, int half, const R* s_own,
+                                             unsigned long long* bar, unsigned parity) {
     constexpr int Q = L::Q;
     constexpr int BV = E * E * E;
     constexpr int W = BV >= 64 ? BV / 64 : 1;
@@ -222,6 +265,7 @@ __device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b
             if (!live) return;  // inactive slot
         }
     }
+    if constexpr (TMA) mbar_wait(bar, parity);  // the block's own populations have landed in shared memory
     // fused probe_field terms of this cell (DIAG)
     using P = std::conditional_t<Exact || sizeof(R) == 8, double, float>;
     P dg_mass = P(0), dg_v2 = P(0);
@@ -250,12 +294,21 @@ __device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b
         if constexpr (ey < 0) d += 3 * yhi;
         if constexpr (ez > 0) d -= 9 * zlo;
         if constexpr (ez < 0) d += 9 * zhi;
-        const R* src = s_ptr[d] + (i * BV + sl);
-        if (!full) {
-            const bool solid = !((s_mask[d][sl >> 6] >> (sl & 63)) & 1ull);
-            if (solid) src = A.cur + self_base + (oi * BV + t);
+        if constexpr (TMA) {
+            // own-block pulls from the shared-memory copy, face pulls from
+            // the neighbour blocks in global memory (L2)
+            const bool solid = !full && !((s_mask[d][sl >> 6] >> (sl & 63)) & 1ull);
+            if (solid) g[i] = s_own[oi * BV + t];
+            else if (d == 13) g[i] = s_own[i * BV + sl];
+            else g[i] = __ldg(s_ptr[d] + (i * BV + sl));
+        } else {
+            const R* src = s_ptr[d] + (i * BV + sl);
+            if (!full) {
+                const bool solid = !((s_mask[d][sl >> 6] >> (sl & 63)) & 1ull);
+                if (solid) src = A.cur + self_base + (oi * BV + t);
+            }
+            g[i] = __ldg(src);
         }
-        g[i] = __ldg(src);
     });
 
     bool ok = true;
@@ -416,6 +469,23 @@ struct SparseOps {
         if (A.scan_span > 0) {  // bitmask sweep: one CTA pair per span of blocks
             A.scan_blocks = nblocks;
             grid = dim3((nblocks + A.scan_span - 1) / A.scan_span * S);
+        } else if constexpr (E == 8 && std::is_same_v<R, float>) {
+            if (A.tma) {  // one CTA per block, the block staged by a bulk copy
+                constexpr int smem = Q * E * E * E * int(sizeof(R));
+                auto go = [&](auto kern) {
+                    VOXL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                    kern<<<nblocks, E * E * E, smem, st>>>(A);
+                };
+                if (A.diag_acc) {
+                    if (mode == kHeavy) go(sparse_tma_kernel<L, R, Exact, E, kHeavy, true>);
+                    else go(sparse_tma_kernel<L, R, Exact, E, kLight, true>);
+                } else {
+                    if (mode == kHeavy) go(sparse_tma_kernel<L, R, Exact, E, kHeavy, false>);
+                    else go(sparse_tma_kernel<L, R, Exact, E, kLight, false>);
+                }
+                VOXL_CUDA(cudaGetLastError());
+                return;
+            }
         }
         if (A.diag_acc) {
             if (mode == kHeavy) sparse_step_kernel<L, R, Exact, E, kHeavy, true><<<grid, block, 0, st>>>(A);
@@ -464,6 +534,8 @@ SparseEngine::SparseEngine(const SparseConfig& cfg, const std::uint8_t* active)
     esize_ = cfg_.precision == Precision::F64 ? 8 : 4;
     T_ = SparseTables::build(cfg_.domain, active, cfg_.edge, cfg_.strategy, q_);
 
+    // bulk-copy block staging (sparse_tma_kernel, measured slower): VOXL_SPARSE_TMA=1
+    if (const char* e = std::getenv("VOXL_SPARSE_TMA")) tma_ = std::atoi(e) != 0;
     VOXL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     {
         int lo = 0, hi = 0;
@@ -656,6 +728,7 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
         }
         A.cur = static_cast<const R*>(buf_[cur_]);
         A.nxt = static_cast<R*>(buf_[cur_ ^ 1]);
+        A.tma = tma_ ? 1 : 0;
         A.nbr = d_nbr_;
         A.masks = d_masks_;
         A.full = d_full_;

@@ -296,3 +296,41 @@ def test_step_probe_n_batches(strategy, precision):
     assert np.array_equal(a.get_state(), b.get_state())
     a.close()
     b.close()
+
+
+def _sparse_run(dom, strategy, lattice, steps, tma, probe=False):
+    import os
+
+    old = os.environ.get("VOXL_SPARSE_TMA")
+    os.environ["VOXL_SPARSE_TMA"] = "1" if tma else "0"
+    try:
+        e = V.SparseEngine(dom, block_edge=8, strategy=strategy, precision="fp32", lattice=lattice)
+    finally:
+        if old is None:
+            del os.environ["VOXL_SPARSE_TMA"]
+        else:
+            os.environ["VOXL_SPARSE_TMA"] = old
+    rows = [(d.mass, d.max_speed) for d in e.step_probe_n(steps)] if probe else None
+    if not probe:
+        e.step(steps)
+    out = e.get_state()
+    e.close()
+    return out, rows
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["naive", "disag_bitmask", "disag_mem"])
+@pytest.mark.parametrize("lattice", ["D3Q19", "D3Q27"])
+@pytest.mark.parametrize("probe", [False, True])
+def test_tma_block_staging_bitwise(strategy, lattice, probe):
+    """The bulk-copy staged kernel (one block per CTA, own populations from
+    shared memory) against the register-pull kernel: fields bitwise equal,
+    probe rows too (same warps' per-cell terms)."""
+    dom = (40, 32, 24)
+    a, ra = _sparse_run(dom, strategy, lattice, 25, True, probe)
+    b, rb = _sparse_run(dom, strategy, lattice, 25, False, probe)
+    assert np.array_equal(a, b)
+    if probe:
+        assert len(ra) == len(rb) == 25
+        for (m1, u1), (m2, u2) in zip(ra, rb):
+            assert abs(m1 - m2) <= 1e-12 * m2 and abs(u1 - u2) <= 1e-12 * u2

@@ -260,23 +260,26 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
     // the first offender into the step's bad word.
     if constexpr (DIAG) {
         P pm = dg_mass, pv = dg_v2;
-        if (live && dg_bad >= 0) {
+        // the voxel's coordinates are re-derived from the special registers
+        // here rather than kept live through the step (register budget)
+        if (dg_bad >= 0) {
             const unsigned long long canon =
                 (unsigned long long)(A.kg0 + A.k_first + int(blockIdx.z) * A.k_step) * A.s +
-                (unsigned long long)(blockIdx.y * A.na + a);
+                (unsigned long long)(blockIdx.y * A.na + blockIdx.x * kBlock + threadIdx.x);
             atomicMin(A.diag_bad, (canon << 5) | (unsigned long long)dg_bad);
         }
-        const unsigned live_lanes = __ballot_sync(0xffffffffu, live);
-        for (int o = 16; o > 0; o >>= 1) {
-            pm += __shfl_xor_sync(0xffffffffu, pm, o);
-            pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
-        }
-        if ((threadIdx.x & 31) == 0 && live_lanes) {
-            double mass = double(pm);
-            if constexpr (std::is_same_v<P, float>) mass += double(__popc(live_lanes));
-            const unsigned long long blk =
-                ((unsigned long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-            diag_commit(A.diag_acc, blk * (kBlock / 32) + (threadIdx.x >> 5), mass, double(pv));
+        const unsigned live_lanes = __ballot_sync(0xffffffffu, int(blockIdx.x * kBlock + threadIdx.x) < A.na);
+        const unsigned long long warp_id =
+            (((unsigned long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (kBlock / 32) +
+            (threadIdx.x >> 5);
+        if constexpr (std::is_same_v<P, float>) {
+            diag_warp_commit_f32(A.diag_acc, warp_id, pm, pv, live_lanes);
+        } else {
+            for (int o = 16; o > 0; o >>= 1) {
+                pm += __shfl_xor_sync(0xffffffffu, pm, o);
+                pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
+            }
+            if ((threadIdx.x & 31) == 0 && live_lanes) diag_commit(A.diag_acc, warp_id, double(pm), double(pv));
         }
     }
 }
@@ -463,18 +466,9 @@ __global__ void __launch_bounds__(kAosThreads, VOXL_AOS_MINB)
                 const unsigned long long canon = (unsigned long long)kg * A.s + (unsigned long long)b * A.na + a;
                 atomicMin(A.diag_bad, (canon << 5) | (unsigned long long)dg_bad);
             }
-            P pm = dg_mass, pv = dg_v2;
             const unsigned lanes = __ballot_sync(0xffffffffu, live);
-            for (int o = 16; o > 0; o >>= 1) {
-                pm += __shfl_xor_sync(0xffffffffu, pm, o);
-                pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
-            }
-            if (lane == 0 && lanes) {
-                const double mass = double(pm) + double(__popc(lanes));
-                const unsigned long long row =
-                    ((unsigned long long)kg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-                diag_commit(A.diag_acc, row * kAosTY + ty, mass, double(pv));
-            }
+            const unsigned long long row = ((unsigned long long)kg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            diag_warp_commit_f32(A.diag_acc, row * kAosTY + ty, dg_mass, dg_v2, lanes);
         }
         // the output records go through the slot of plane k-1 (read by no
         // one after this barrier), 32 records x Q words per row, 16-byte phase 0

@@ -98,6 +98,41 @@ __device__ __forceinline__ void diag_commit(unsigned long long* acc, unsigned lo
     if (w[3]) atomicMax(lane + 3, w[3]);
 }
 
+/// A warp's probe terms for the fp32 (shifted-storage) kernels, every lane
+/// calling with its voxel's dr = rho - 1 and |u|^2 (zeros for a dead or
+/// unstable lane; `live` = the warp's live lanes). Each lane's dr becomes a
+/// fixed-point integer in 2^-40 units (|dr| < 2^15 for any voxel that passes
+/// probe_field's |f_i| <= 1e3 test; larger or non-finite terms only occur on a
+/// step the bad word already fails), summed exactly across the warp in three
+/// 21-bit chunks by redux.sync; max |u|^2 is a redux.sync max of the fp32 bit
+/// patterns (non-negative floats order like their bits). Lane 0 adds the
+/// live count (the 1 of each rho) and commits the warp's words. Half the
+/// instructions of a shuffle tree plus an fp64 fixed-point conversion, and
+/// the per-lane rounding (2^-41) is finer than an fp32 warp sum's.
+__device__ __forceinline__ void diag_warp_commit_f32(unsigned long long* acc, unsigned long long warp_id, float dr,
+                                                     float v2, unsigned live) {
+    long long fx = 0;
+    if (fabsf(dr) < 32768.0f) fx = __float2ll_rn(dr * 1099511627776.0f);  // x 2^40 (exact scaling)
+    const unsigned c0 = unsigned(fx) & 0x1FFFFFu, c1 = unsigned(fx >> 21) & 0x1FFFFFu;
+    const int c2 = int(fx >> 42);
+    const unsigned s0 = __reduce_add_sync(0xffffffffu, c0), s1 = __reduce_add_sync(0xffffffffu, c1);
+    const int s2 = __reduce_add_sync(0xffffffffu, c2);
+    const unsigned vb = __reduce_max_sync(0xffffffffu, __float_as_uint(v2));
+    if ((threadIdx.x & 31) != 0 || !live) return;
+    // T = sum of the lanes in 2^-40 units, plus 2^40 per live voxel
+    const long long T = ((long long)s2 << 42) + ((long long)s1 << 21) + (long long)s0 +
+                        ((long long)__popc(live) << 40);
+    const unsigned long long frac40 = (unsigned long long)T & ((1ull << 40) - 1);
+    unsigned long long* lane = acc + (warp_id & (kDiagLanes - 1)) * kDiagWords;
+    const unsigned long long pol = l2_evict_last_policy();
+    const unsigned long long w0 = (frac40 & 0xffull) << 24, w1 = frac40 >> 8,
+                             w2 = (unsigned long long)(T >> 40);  // 64 fraction bits: frac40 << 24
+    if (w0) red_add_u64(lane + 0, w0, pol);
+    if (w1) red_add_u64(lane + 1, w1, pol);
+    if (w2) red_add_u64(lane + 2, w2, pol);
+    if (vb) atomicMax(lane + 3, (unsigned long long)__double_as_longlong(double(__uint_as_float(vb))));
+}
+
 /// A step's exact sums: mass as a 128-bit two's-complement fixed-point number
 /// (64 fraction bits), max |u|^2 as fp64 bits, the first-offender word.
 /// Raw sums from several rings (one per device) add as integers, so a step

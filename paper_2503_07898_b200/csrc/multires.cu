@@ -191,16 +191,16 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
         }
         using P = typename DiagCell<R, Exact>::P;
         P pm = dc.m, pv = dc.v;
-        for (int o = 16; o > 0; o >>= 1) {
-            pm += __shfl_xor_sync(0xffffffffu, pm, o);
-            pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
-        }
         const unsigned live = __ballot_sync(0xffffffffu, active);
-        if ((tid & 31) == 0 && live) {
-            double mass = double(pm);
-            if constexpr (std::is_same_v<P, float>) mass += double(__popc(live));
-            diag_commit(A.diag_acc, (unsigned long long)blockIdx.x * (E * E * E / S / 32) + (tid >> 5), mass,
-                        double(pv));
+        const unsigned long long warp_id = (unsigned long long)blockIdx.x * (E * E * E / S / 32) + (tid >> 5);
+        if constexpr (std::is_same_v<P, float>) {
+            diag_warp_commit_f32(A.diag_acc, warp_id, pm, pv, live);
+        } else {
+            for (int o = 16; o > 0; o >>= 1) {
+                pm += __shfl_xor_sync(0xffffffffu, pm, o);
+                pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
+            }
+            if ((tid & 31) == 0 && live) diag_commit(A.diag_acc, warp_id, double(pm), double(pv));
         }
     } else if constexpr (MODE != kProbe) {
         if (!active) return;

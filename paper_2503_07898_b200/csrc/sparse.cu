@@ -365,16 +365,17 @@ __device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b
             atomicMin(A.diag_bad, ((unsigned long long)A.canon[(long long)b * BV + t] << 5) |
                                       (unsigned long long)dg_bad);
         P pm = dg_mass, pv = dg_bad >= 0 ? P(0) : dg_v2;
-        for (int o = 16; o > 0; o >>= 1) {
-            pm += __shfl_xor_sync(0xffffffffu, pm, o);
-            pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
-        }
         const unsigned lanes = __ballot_sync(0xffffffffu, live);
-        if ((tid & 31) == 0 && lanes) {
-            double mass = double(pm);
-            if constexpr (std::is_same_v<P, float>) mass += double(__popc(lanes));
-            constexpr int kWarps = (BV / S + 31) / 32;
-            diag_commit(A.diag_acc, ((unsigned long long)b * S + half) * kWarps + (tid >> 5), mass, double(pv));
+        constexpr int kWarps = (BV / S + 31) / 32;
+        const unsigned long long warp_id = ((unsigned long long)b * S + half) * kWarps + (tid >> 5);
+        if constexpr (std::is_same_v<P, float>) {
+            diag_warp_commit_f32(A.diag_acc, warp_id, pm, pv, lanes);
+        } else {
+            for (int o = 16; o > 0; o >>= 1) {
+                pm += __shfl_xor_sync(0xffffffffu, pm, o);
+                pv = max(pv, __shfl_xor_sync(0xffffffffu, pv, o));
+            }
+            if ((tid & 31) == 0 && lanes) diag_commit(A.diag_acc, warp_id, double(pm), double(pv));
         }
     }
 }

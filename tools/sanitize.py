@@ -1,8 +1,11 @@
 #!/usr/bin/env python
 """Small runs of every engine kernel family for compute-sanitizer
-(memcheck / racecheck / synccheck): dense (3 layouts, 3 partitions, both halo
-modes, D3Q27, fp32/fp64, fused probe), block-sparse (3 strategies, edge 4/8,
-step_probe), multires (fused/staged, obstacle), canonical I/O both ways.
+(memcheck / racecheck / synccheck): dense (3 layouts incl. the fp32 AoS
+plane-tile kernel, 3 partitions, both halo modes, D3Q27, fp32/fp64, fused
+probe, multi-device schedule with graph replay and the observed trace),
+block-sparse (3 strategies, edge 4/8, fused probe, the bulk-copy staging
+kernel), multires (fused/staged, obstacle, fused probe), canonical I/O both
+ways.
 
     compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize.py
 """
@@ -24,6 +27,7 @@ for lat in ("D3Q19", "D3Q27"):
                 e.set_equilibrium()
                 e.step(3)
                 e.step_probe()
+                e.step_probe_n(3)
                 st = e.get_canonical()
                 e.set_canonical(st)
                 e.probe()
@@ -35,6 +39,7 @@ for lat in ("D3Q19", "D3Q27"):
                 s = V.SparseEngine((40, 24, 24), block_edge=edge, strategy=strategy, precision=prec, lattice=lat)
                 s.step(2)
                 s.step_probe()
+                s.step_probe_n(2)
                 st = s.get_state()
                 s.set_state(st)
                 s.probe()
@@ -48,6 +53,7 @@ for prec in ("fp32", "fp64"):
         m.set_state(st)
         m.step(1)
         m.probe()
+        m.step_probe_n(2)
         m.close()
         m = V.MultiResEngine(dom, 3, level_map=obstacle_band_level_map(dom, 3), fused=fused, precision=prec,
                              solid_cells=True)
@@ -62,4 +68,23 @@ for fused in (True, False):  # D2Q9 multires: z = 0 layer of the E^3 blocks
         m.set_state(m.get_state())
         m.probe()
         m.close()
+# multi-device schedule (all partitions on device 0), graph replay, observed trace
+e = V.DenseEngine("D3Q19", (16, 12, 24), 0.6, "lid_driven_cavity", (0.05, 0, 0), partitions=3, devices=[0, 0, 0],
+                  graph_steps=2, precision="fp32")
+e.set_equilibrium()
+e.step(4)
+e.step_probe_n(2)
+e.trace(True)
+e.step(1)
+e.trace_json()
+e.close()
+# block-sparse bulk-copy (TMA) staging kernel
+os.environ["VOXL_SPARSE_TMA"] = "1"
+for lat in ("D3Q19", "D3Q27"):
+    for strategy in ("naive", "disag_bitmask", "disag_mem"):
+        s = V.SparseEngine((40, 24, 24), block_edge=8, strategy=strategy, precision="fp32", lattice=lat)
+        s.step(2)
+        s.step_probe_n(2)
+        s.close()
+del os.environ["VOXL_SPARSE_TMA"]
 print("sanitize run ok")

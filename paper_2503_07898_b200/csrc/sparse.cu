@@ -444,6 +444,10 @@ constexpr int kSpProbeBlocks = 592;
 #define VOXL_BITMASK_SPAN 64
 #endif
 constexpr int kBitmaskSpan = VOXL_BITMASK_SPAN;  // blocks per CTA pair of the bitmask boundary sweep
+#ifndef VOXL_HEAVY_LOW_PRIO
+#define VOXL_HEAVY_LOW_PRIO 0
+#endif
+constexpr bool kHeavyLowPrio = VOXL_HEAVY_LOW_PRIO != 0;
 
 template <class L, class R, bool Exact>
 struct SparseOps {
@@ -763,7 +767,10 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
                 A.block_begin = 0;
                 A.bitmask = d_bitmask_;
                 const bool split = classes_.n_boundary > 0 && classes_.n_boundary < nb;
-                cudaStream_t hs = split ? side_ : stream_;
+                // VOXL_HEAVY_LOW_PRIO: the light sweep on the high-priority
+                // stream, the boundary sweep behind it on the engine stream
+                cudaStream_t hs = split ? (kHeavyLowPrio ? stream_ : side_) : stream_;
+                cudaStream_t ls = split ? (kHeavyLowPrio ? side_ : stream_) : stream_;
                 if (split) {
                     VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
                     VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
@@ -775,9 +782,9 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
                 if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], hs));
                 A.scan_span = 0;
                 A.bitmask_want = 0;
-                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
-                Ops::launch(edge, A, kLight, nb, stream_);
-                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], ls));
+                Ops::launch(edge, A, kLight, nb, ls);
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], ls));
                 if (split) {
                     VOXL_CUDA(cudaEventRecord(ev_join_, side_));
                     VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
@@ -791,7 +798,8 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
                 // stream, concurrently; joined before the next step.
                 const int n_b = int(classes_.n_boundary);
                 const bool split = n_b > 0 && n_b < nb;
-                cudaStream_t hs = split ? side_ : stream_;
+                cudaStream_t hs = split ? (kHeavyLowPrio ? stream_ : side_) : stream_;
+                cudaStream_t ls = split ? (kHeavyLowPrio ? side_ : stream_) : stream_;
                 if (split) {
                     VOXL_CUDA(cudaEventRecord(ev_fork_, stream_));
                     VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
@@ -801,9 +809,9 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
                 if (n_b > 0) Ops::launch(edge, A, kHeavy, n_b, hs);
                 if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], hs));
                 A.block_begin = n_b;
-                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], stream_));
-                if (nb > n_b) Ops::launch(edge, A, kLight, nb - n_b, stream_);
-                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], stream_));
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], ls));
+                if (nb > n_b) Ops::launch(edge, A, kLight, nb - n_b, ls);
+                if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[1], ls));
                 if (split) {
                     VOXL_CUDA(cudaEventRecord(ev_join_, side_));
                     VOXL_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));

@@ -203,3 +203,17 @@ def test_observed_trace_lists_the_executed_schedule(devices, halo):
     for rs in by.values():
         for a, b in zip(rs, rs[1:]):
             assert b["begin_ms"] >= a["end_ms"] - 1e-3
+
+
+@pytest.mark.parametrize("layout", ["AoS", "DisagSoA"])
+@pytest.mark.parametrize("halo", ["zero_copy", "copy"])
+def test_multi_schedule_fp32_aos_tile_bitwise(layout, halo):
+    """fp32 through the multi-device schedule (interior / shared-layer
+    launches of the AoS plane-tile kernel on their two streams, graph replay)
+    against the one-stream SoA engine: bitwise (same collision arithmetic)."""
+    dom = (40, 18, 36)
+    init = O.port_initial_state("D3Q19", dom)
+    ref = _run(17, init, dom, precision="fp32", layout="SoA", partitions=1)
+    out = _run(17, init, dom, precision="fp32", layout=layout, partitions=3, halo_mode=halo, devices=[0, 0, 0],
+               graph_steps=4)
+    assert np.array_equal(out, ref)

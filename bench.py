@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-size", type=int, default=0, help="domain edge of the e2e run (default: --size)")
+    ap.add_argument("--e2e-steps", type=int, default=1000,
+                    help="steps of the e2e run() (default 1000: BASELINE configs[0]'s run length); a second e2e "
+                         "run at --steps is reported beside it")
     ap.add_argument("--no-paths", action="store_true", help="skip the block-sparse / multires lines (configs[3-4])")
     return ap.parse_args()
 
@@ -435,10 +438,12 @@ def secondary_paths(args, V, peak):
 
 
 def e2e_run(args, V, np):
-    """The same metric through the reference-facing API with host buffers:
-    fill_canonical from a pinned fp64 canonical host array, K steps each
-    followed by probe_field (diagnostics row D2H, as voxl::run does per step,
-    solver.cpp:245-255), and to_canonical of the final field."""
+    """The same metric through the reference-facing API with host buffers, in
+    run()'s shape (solver.cpp:225-266): fill_canonical from a pinned fp64
+    canonical host array, K steps each followed by probe_field (fused into the
+    step kernel, rows read back once per 256 steps), and to_canonical of the
+    final field. K = --e2e-steps (default 1000, the run length of BASELINE
+    configs[0]); the same run at --steps is reported as `short_run`."""
     import torch
 
     n = args.e2e_size or args.size
@@ -450,24 +455,34 @@ def e2e_run(args, V, np):
     # rest-equilibrium canonical input (initial_canonical_state, solver.cpp:165-187)
     w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
     host_in.reshape(vox, Q)[:] = w
-    steps = args.steps
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    eng.set_canonical(host_in)
-    rows = eng.step_probe_n(steps)  # run()'s loop: step + fused probe_field, rows read back per 256-step batch
-    eng.get_canonical(host_out)
-    dt = time.perf_counter() - t0
+
+    def one(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.set_canonical(host_in)
+        t1 = time.perf_counter()
+        rows = eng.step_probe_n(steps)  # run()'s loop: step + fused probe_field
+        t2 = time.perf_counter()
+        eng.get_canonical(host_out)
+        t3 = time.perf_counter()
+        # the fp32 engine moves its storage format over PCIe (canon_io.cuh):
+        # the host converts fp64 <-> fp32 wire buffers, which are what is copied
+        wire_in = vox * Q * 4
+        wire_out = vox * Q * 4 + ((steps + 255) // 256) * 256 * 32
+        return {"value": round(vox * steps / (t3 - t0) / 1e6, 1), "unit": "MLUPS", "steps": steps,
+                "h2d_bytes_per_step": int(wire_in / steps), "d2h_bytes_per_step": int(wire_out / steps),
+                "seconds": round(t3 - t0, 3), "set_s": round(t1 - t0, 3), "steps_s": round(t2 - t1, 3),
+                "get_s": round(t3 - t2, 3), "final_mass": rows[-1].mass if rows else None}
+
+    main = one(args.e2e_steps)
+    short = one(args.steps) if args.steps != args.e2e_steps else None
     eng.close()
-    # the fp32 engine moves its storage format over PCIe (canon_io.cuh): the
-    # host converts fp64 <-> fp32 wire buffers, which are what is copied
-    wire_in = vox * Q * 4
-    wire_out = vox * Q * 4 + ((steps + 255) // 256) * 256 * 32
-    return {"value": round(vox * steps / dt / 1e6, 1), "unit": "MLUPS",
-            "h2d_bytes_per_step": int(wire_in / steps), "d2h_bytes_per_step": int(wire_out / steps),
-            "canonical_fp64_bytes": vox * Q * 8, "domain": list(dom), "seconds": round(dt, 3),
-            "final_mass": rows[-1].mass if rows else None,
-            "path": "DenseEngine.set_canonical(host fp64 -> fp32 wire) + step_probe_n(steps) (fused probe, rows D2H "
-                    "per 256-step batch) + get_canonical(fp32 wire -> host fp64)"}
+    main.update({"canonical_fp64_bytes": vox * Q * 8, "domain": list(dom),
+                 "path": "DenseEngine.set_canonical(host fp64 -> fp32 wire) + step_probe_n(steps) (fused probe, rows "
+                         "D2H per 256-step batch) + get_canonical(fp32 wire -> host fp64)"})
+    if short:
+        main["short_run"] = {k: short[k] for k in ("steps", "value", "seconds", "set_s", "steps_s", "get_s")}
+    return main
 
 
 def e2e_run_dist(args, eng, dist, voxels_total, share, np):

@@ -167,7 +167,8 @@ def test_bench_line_contract_small():
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--size", "64", "--no-cpu"],
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--size", "64", "--no-cpu",
+                        "--e2e-steps", "10"],
                        capture_output=True, text=True, cwd=root, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
@@ -179,7 +180,8 @@ def test_bench_line_contract_small():
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["value"] > 0 and d["gpu_launches"] == 5
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["achieved"] > 0
     # the copied tensors are the fp32 wire buffers (the host converts fp64 canonical <-> fp32)
-    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 64 ** 3 * 19 * 4 // 5
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 64 ** 3 * 19 * 4 // 10
+    assert d["e2e"]["steps"] == 10 and d["e2e"]["short_run"]["steps"] == 5 and d["e2e"]["short_run"]["value"] > 0
     p = d["paths"]
     assert "error" not in p, p
     for k in ("sparse_disag_mem", "sparse_naive", "multires_obstacle_fused", "multires_obstacle_staged"):

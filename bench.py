@@ -366,7 +366,7 @@ def main():
             "metric": "MLUPS (D3Q19 fp32) at 1/2/4/8 B200 and % of HBM roofline vs CPU ref",
             "value": round(value, 1), "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak" if (args.weak or world == 1) else "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (rest-equilibrium lid-driven cavity, device-initialised)",
             "config": {"workload": f"D3Q19 BGK lid-driven cavity dense {domain[0]}x{domain[1]}x{domain[2]} fp32, "
                                    f"DisagSoA, {world} z-slab partition(s), {args.halo} halo",

@@ -517,9 +517,8 @@ def e2e_run_dist(args, eng, dist, voxels_total, share, np):
     t0 = time.perf_counter()
     eng.set_canonical_planes(host_in, k0, k1)
     eng.refresh_halos()
-    last = None
-    for _ in range(steps):
-        last = eng.step_probe()
+    rows = eng.step_probe_n(steps)  # this rank's run() loop: step + fused probe, rows per 256-step batch
+    last = rows[-1]
     eng.get_canonical_planes(k0, k1, out=host_out)
     dt = time.perf_counter() - t0
     t = torch.tensor([dt, last.max_speed], dtype=torch.float64, device="cpu" if share else "cuda")
@@ -533,8 +532,9 @@ def e2e_run_dist(args, eng, dist, voxels_total, share, np):
             "h2d_bytes_per_step": int(bytes_in / steps), "d2h_bytes_per_step": int(bytes_out / steps),
             "domain": list(dom), "seconds": round(dt, 3), "final_mass": float(m.item()),
             "final_max_speed": float(t[1].item()),
-            "path": "per rank: DistributedDense.set_canonical_planes(host fp64 slab) + refresh_halos + "
-                    "steps x step_probe (rank diag row D2H) + get_canonical_planes; wall time max over ranks"}
+            "path": "per rank: DistributedDense.set_canonical_planes(host fp64 slab -> fp32 wire) + refresh_halos + "
+                    "step_probe_n(steps) (rank rows D2H per 256-step batch) + get_canonical_planes; wall time max "
+                    "over ranks"}
 
 
 if __name__ == "__main__":

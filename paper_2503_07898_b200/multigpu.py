@@ -235,6 +235,15 @@ class DistributedDense:
             self._nccl_exchange()
         return d
 
+    def step_probe_n(self, n):
+        """n steps with this rank's probe_field fused, rows read back once per
+        256 steps (zero-copy halo: the engine's own batched loop); the copy
+        mode exchanges halos from the host between steps, so it probes step
+        by step. Rows cover the rank's slab (`combine_rows` across ranks)."""
+        if self.halo_mode == "zero_copy":
+            return self.eng.step_probe_n(n)
+        return [self.step_probe() for _ in range(n)]
+
     def timed_steps(self, n):
         if self.halo_mode == "zero_copy":
             return self.eng.timed_steps(n)

@@ -210,6 +210,8 @@ struct SolverConfig {
     std::vector<int> devices;
     int halo_mode = VOXL_HALO_ZERO_COPY;
     int graph_steps = 8;
+    // Dense runs: also record the executed step schedule (voxl_dense_trace_json)
+    bool observed_trace = false;
 
     int dim() const { return lattice == VOXL_D2Q9 ? 2 : 3; }
     int partition_axis() const { return dim() == 2 ? 1 : 2; }
@@ -279,6 +281,7 @@ struct RunResult {
         int partition;
     };
     std::vector<TraceEvent> trace;             // dense runs: the OCC schedule's logical order
+    std::string observed_trace_json;           // dense runs with config.observed_trace: the executed schedule
     std::string dispatch_json;                 // sparse runs
     std::string graph_dot;                     // multires runs
     std::string distribution;                  // multires runs
@@ -360,7 +363,14 @@ inline RunResult run_dense(const SolverConfig& c) {
     // the first failing step aborts with run()'s text (voxl_dense_step_probe_n)
     std::vector<voxl_diag> rows(std::size_t(std::max(c.steps, 0)));
     int done = 0;
+    if (c.observed_trace) check(voxl_dense_trace_enable(e.handle(), 1));
     const int status = voxl_dense_step_probe_n(e.handle(), c.steps, rows.data(), &done);
+    if (c.observed_trace) {
+        r.observed_trace_json = text_of([](void* h, char* o, std::int64_t cap, std::int64_t* n) {
+            return voxl_dense_trace_json(static_cast<voxl_dense*>(h), o, cap, n);
+        }, e.handle());
+        check(voxl_dense_trace_enable(e.handle(), 0));
+    }
     for (int step = 0; step < done; ++step) {
         r.diagnostics.push_back({step, rows[std::size_t(step)].mass, rows[std::size_t(step)].max_speed});
         const auto recs = e.ledger(step);

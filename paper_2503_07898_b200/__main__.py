@@ -11,12 +11,12 @@ import sys
 import numpy as np
 
 
-def cmd_run(config_path: str, out_dir: str) -> int:
+def cmd_run(config_path: str, out_dir: str, observed_trace: bool = False) -> int:
     from .solver import config_from_json, run, write_outputs
 
     with open(config_path, "rb") as f:
         cfg = config_from_json(f.read().decode())
-    res = run(cfg)
+    res = run(cfg, observed_trace)
     write_outputs(res, out_dir)
     step, mass, umax = res.diagnostics[-1] if res.diagnostics else (0, 0.0, 0.0)
     print(f"run complete: {cfg.steps} steps, final mass {mass:.6g}, max |u| {umax:.6g}")
@@ -160,6 +160,8 @@ def main(argv=None) -> int:
     r = sub.add_parser("run")
     r.add_argument("--config", required=True)
     r.add_argument("--out", default="out")
+    r.add_argument("--observed-trace", action="store_true",
+                   help="also write trace_observed.json: the executed step schedule (dense runs)")
     sub.add_parser("verify")
     lg = sub.add_parser("ledger")
     lg.add_argument("--config", required=True)
@@ -169,7 +171,7 @@ def main(argv=None) -> int:
     a = ap.parse_args(argv)
     try:
         if a.cmd == "run":
-            return cmd_run(a.config, a.out)
+            return cmd_run(a.config, a.out, a.observed_trace)
         if a.cmd == "verify":
             return cmd_verify()
         if a.cmd == "ledger":

@@ -1,7 +1,7 @@
 // voxl_b200 -- the C++ driver of the B200 engines (proj/tools/main.cpp's `run`
 // and `verify` subcommands), built on the header-only binding voxl_b200.hpp.
 //
-//   voxl_b200 run --config FILE [--out DIR] [--precision fp64|fp32] [--devices 0,1,..]
+//   voxl_b200 run --config FILE [--out DIR] [--precision fp64|fp32] [--devices 0,1,..] [--observed-trace]
 //   voxl_b200 verify
 //
 // `run` parses the configuration with the reference's rules (config_from_json,
@@ -150,10 +150,12 @@ void write_file(const fs::path& path, const std::string& text) {
     out << text;
 }
 
-int cmd_run(const std::string& config_path, const std::string& out_dir, int precision, const std::vector<int>& devs) {
+int cmd_run(const std::string& config_path, const std::string& out_dir, int precision, const std::vector<int>& devs,
+            bool observed_trace) {
     SolverConfig config = config_from_json(read_file(config_path));
     config.precision = precision;
     config.devices = devs;
+    config.observed_trace = observed_trace;
     RunResult result = voxl::b200::run(config);
 
     fs::create_directories(out_dir);
@@ -168,6 +170,7 @@ int cmd_run(const std::string& config_path, const std::string& out_dir, int prec
     write_file(base / "config.json", config_to_json(config));
     if (!result.ledger.empty()) write_file(base / "ledger.csv", result.ledger_csv());
     if (!result.trace.empty()) write_file(base / "trace.json", result.trace_json());
+    if (!result.observed_trace_json.empty()) write_file(base / "trace_observed.json", result.observed_trace_json);
     if (!result.dispatch_json.empty()) write_file(base / "dispatch.json", result.dispatch_json);
     if (!result.graph_dot.empty()) write_file(base / "graph.dot", result.graph_dot);
     if (!result.distribution.empty()) write_file(base / "distribution.txt", result.distribution);
@@ -266,7 +269,8 @@ int cmd_verify() {
 }
 
 void usage() {
-    std::cerr << "usage: voxl_b200 run --config FILE [--out DIR] [--precision fp64|fp32] [--devices 0,1,...]\n"
+    std::cerr << "usage: voxl_b200 run --config FILE [--out DIR] [--precision fp64|fp32] [--devices 0,1,...] "
+                 "[--observed-trace]\n"
                  "       voxl_b200 verify\n";
 }
 
@@ -283,8 +287,13 @@ int main(int argc, char** argv) {
             std::string config_path, out_dir = "out";
             int precision = VOXL_F64;
             std::vector<int> devices;
+            bool observed_trace = false;
             for (int i = 2; i < argc; ++i) {
                 const std::string a = argv[i];
+                if (a == "--observed-trace") {
+                    observed_trace = true;
+                    continue;
+                }
                 if (i + 1 >= argc) {
                     usage();
                     return 2;
@@ -311,7 +320,7 @@ int main(int argc, char** argv) {
                 usage();
                 return 2;
             }
-            return cmd_run(config_path, out_dir, precision, devices);
+            return cmd_run(config_path, out_dir, precision, devices, observed_trace);
         }
         if (cmd == "verify") return cmd_verify();
         usage();

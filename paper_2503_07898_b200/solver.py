@@ -178,6 +178,7 @@ class RunResult:
     dispatch_json: str = ""
     graph_dot: str = ""
     distribution: str = ""
+    observed_trace_json: str = ""  # the executed schedule (run(..., observed_trace=True), dense path)
 
     def diagnostics_csv(self) -> str:
         """solver.cpp:139-148 (%.17g)."""
@@ -223,8 +224,10 @@ def _probed_rows(eng, steps):
         return e.rows, e
 
 
-def run_dense(c: SolverConfig) -> RunResult:
-    """run_dense (solver.cpp:225-266) on DenseEngine."""
+def run_dense(c: SolverConfig, observed_trace: bool = False) -> RunResult:
+    """run_dense (solver.cpp:225-266) on DenseEngine. observed_trace: also
+    record the executed step schedule (voxl_dense_trace_json: every launched
+    phase with its stream, device and CUDA-event times)."""
     from .dense import DenseEngine, plan_ledger
     from .initial import initial_canonical_state
 
@@ -232,9 +235,14 @@ def run_dense(c: SolverConfig) -> RunResult:
     eng = DenseEngine(lattice=c.lattice, domain=c.domain, tau=c.tau, scenario=c.scenario, velocity=c.velocity,
                       layout=c.layout, partitions=c.partitions, precision=c.precision)
     eng.set_canonical(initial_canonical_state(c))
+    if observed_trace:
+        eng.trace(True)
     # step_occ + probe_field per step, fused on the device; rows read back per
     # batch, the first failing step raises run()'s text
     rows, err = _probed_rows(eng, c.steps)
+    if observed_trace:
+        r.observed_trace_json = eng.trace_json()
+        eng.trace(False)
     for step, d in enumerate(rows):
         r.diagnostics.append((step, d.mass, d.max_speed))
         r.ledger += plan_ledger(step, lattice=c.lattice, domain=c.domain, layout=c.layout, partitions=c.partitions,
@@ -308,14 +316,15 @@ def run_multires(c: SolverConfig) -> RunResult:
     return r
 
 
-def run(c: SolverConfig) -> RunResult:
-    """run (solver.cpp:369-375)."""
+def run(c: SolverConfig, observed_trace: bool = False) -> RunResult:
+    """run (solver.cpp:369-375). observed_trace: the dense route also records
+    the executed step schedule (RunResult.observed_trace_json)."""
     c.validate()
     if c.levels > 1:
         return run_multires(c)
     if c.scenario == "flow_over_obstacle":
         return run_sparse(c)
-    return run_dense(c)
+    return run_dense(c, observed_trace)
 
 
 def write_outputs(result: RunResult, out_dir: str) -> None:
@@ -336,6 +345,8 @@ def write_outputs(result: RunResult, out_dir: str) -> None:
         w("ledger.csv", result.ledger_csv())
     if result.trace:
         w("trace.json", result.trace_json())
+    if result.observed_trace_json:
+        w("trace_observed.json", result.observed_trace_json)
     if result.dispatch_json:
         w("dispatch.json", result.dispatch_json)
     if result.graph_dot:

@@ -184,3 +184,39 @@ def test_step_probe_equals_step_plus_probe(precision, parts):
         assert abs(da.mass - db.mass) <= tol_m * db.mass
         assert abs(da.max_speed - db.max_speed) <= tol_u * db.max_speed + 1e-12
     assert np.array_equal(a.get_canonical(), b.get_canonical())
+
+
+@pytest.mark.gpu
+def test_cli_run_observed_trace(tmp_path):
+    """`run --observed-trace` adds trace_observed.json: one record per launched
+    phase of every step (single-stream schedule: one "step" kernel per
+    partition), device-timed; the reference's logical trace.json is unchanged."""
+    cfg = tmp_path / "c.json"
+    cfg.write_text(json.dumps({**CASES["dense"], "precision": "fp64", "partitions": 2}))
+    out = tmp_path / "out"
+    r = subprocess.run([sys.executable, "-m", "paper_2503_07898_b200", "run", "--config", str(cfg), "--out",
+                        str(out), "--observed-trace"], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    rec = json.loads((out / "trace_observed.json").read_text())
+    steps = json.loads(cfg.read_text())["steps"]
+    assert [(x["step"], x["phase"], x["partition"]) for x in rec] == [(s, "step", p) for s in range(steps)
+                                                                        for p in range(2)]
+    assert all(0.0 <= x["begin_ms"] <= x["end_ms"] for x in rec)
+    assert (out / "trace.json").exists()
+
+
+@pytest.mark.gpu
+def test_cpp_cli_run_observed_trace(tmp_path):
+    """The C++ driver's `run --observed-trace` (voxl::b200::run with
+    SolverConfig::observed_trace) writes the same executed-schedule record."""
+    exe = os.path.join(ROOT, "paper_2503_07898_b200", "_lib", "voxl_b200")
+    cfg = tmp_path / "c.json"
+    cfg.write_text(json.dumps({**CASES["dense"], "partitions": 2}))
+    out = tmp_path / "out"
+    r = subprocess.run([exe, "run", "--config", str(cfg), "--out", str(out), "--precision", "fp64",
+                        "--observed-trace"], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    rec = json.loads((out / "trace_observed.json").read_text())
+    steps = json.loads(cfg.read_text())["steps"]
+    assert [(x["step"], x["partition"]) for x in rec] == [(s, p) for s in range(steps) for p in range(2)]
+    assert all(x["phase"] == "step" and 0.0 <= x["begin_ms"] <= x["end_ms"] for x in rec)

@@ -87,6 +87,7 @@ private:
     void* buf_[2] = {nullptr, nullptr};
     int cur_ = 0;
     int steps_done_ = 0;
+    int sm_count_ = 0;  // the DisagMem boundary kernel runs one CTA pair per SM
     bool tma_ = false;  // one block per CTA staged by a bulk copy (E = 8, fp32; VOXL_SPARSE_TMA=1)
     std::int32_t* d_nbr_ = nullptr;
     std::uint64_t* d_masks_ = nullptr;

@@ -815,12 +815,14 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
                 }
                 A.block_begin = 0;
                 if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], hs));
-                // The boundary kernel as one long-lived CTA pair per SM,
-                // each walking a contiguous span of the boundary blocks: it
-                // holds few SM slots while the light kernel streams (512^3:
-                // 3.170 vs 3.196 ms per step with a CTA pair per block;
-                // 2 / 4 pairs per SM 3.178, half a pair 3.183)
-                const int pairs = kHeavyCtas < 0 ? 0 : (kHeavyCtas > 0 ? kHeavyCtas : sm_count_);
+                // D3Q19: the boundary kernel as one long-lived CTA pair per
+                // SM, each walking a contiguous span of the boundary blocks:
+                // it holds few SM slots while the light kernel streams
+                // (512^3: 3.171 vs 3.197 ms per step with a CTA pair per
+                // block). D3Q27 keeps a pair per block: its heavier boundary
+                // update, serialised that way, outlasts the light kernel
+                // (4.665 vs 4.577 ms).
+                const int pairs = kHeavyCtas < 0 ? 0 : (kHeavyCtas > 0 ? kHeavyCtas : (q_ == 19 ? sm_count_ : 0));
                 if (pairs > 0 && n_b > 0) A.scan_span = (n_b + pairs - 1) / pairs;
                 if (n_b > 0) Ops::launch(edge, A, kHeavy, n_b, hs);
                 A.scan_span = 0;

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
 #define VOXL_AOS_TY 8
 #endif
 #ifndef VOXL_AOS_CHUNK
-#define VOXL_AOS_CHUNK 64
+#define VOXL_AOS_CHUNK 96
 #endif
 #ifndef VOXL_AOS_SLOTS19
 #define VOXL_AOS_SLOTS19 4

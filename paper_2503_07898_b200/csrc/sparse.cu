@@ -47,6 +47,8 @@ struct SparseArgs {
     int tma;                      // host: one block per CTA staged by a bulk copy (sparse_tma_kernel)
     int scan_span;                // > 0 (bitmask sweep): each CTA pair walks this many consecutive blocks
     int scan_blocks;              //   of the sweep's scan_blocks
+    const int* span_lo;           // bitmask sweep, balanced: CTA pair p walks blocks [span_lo[p], span_lo[p+1])
+    int span_pairs;               //   for p < span_pairs
     int vel_source;
     const std::int32_t* meta_index;  // per slot (DisagBitmask)
     const R* compact_meta;           // 3 per boundary voxel (DisagBitmask)
@@ -169,6 +171,42 @@ template <class L, class R, bool Exact, int E, int MODE, bool DIAG = false>
 __global__ void __launch_bounds__(E* E* E / kSplit<E>, E == 8 && sizeof(R) == 4 ? (MODE == 0 ? block_min_ctas(L::Q) : VOXL_HEAVY_MINB) : 1)
     sparse_step_kernel(const __grid_constant__ SparseArgs<L::Q, R> A) {
     constexpr int S = kSplit<E>;
+    if (A.span_lo) {
+        // DisagBitmask boundary sweep as one long-lived CTA pair per SM
+        // (sparse.cpp:369-380: every block visited, skipped unless its bit
+        // matches). Pair p walks the blocks [span_lo[p], span_lo[p+1]), cut
+        // so that every span holds the same number of boundary blocks; the
+        // CTA tests blockDim.x bitmask bytes at once, compacts the hits into
+        // shared memory (ballot + warp prefix) and updates them in order.
+        constexpr int T = E * E * E / S;
+        constexpr int WARPS = (T + 31) / 32;
+        __shared__ int s_hit[T];
+        __shared__ int s_cnt[WARPS + 1];
+        const int pair = int(blockIdx.x) / S;
+        const int lo = A.span_lo[pair], hi = A.span_lo[pair + 1];
+        const int lane = int(threadIdx.x) & 31, warp = int(threadIdx.x) >> 5;
+        for (int base = lo; base < hi; base += T) {
+            const int b = base + int(threadIdx.x);
+            const bool hit = b < hi && int(A.bitmask[b]) == A.bitmask_want;
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (lane == 0) s_cnt[warp] = __popc(m);
+            __syncthreads();
+            int off = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) {
+                off += w < warp ? s_cnt[w] : 0;
+                total += s_cnt[w];
+            }
+            if (hit) s_hit[off + __popc(m & ((1u << lane) - 1u))] = b;
+            __syncthreads();
+            for (int i = 0; i < total; ++i) {
+                sparse_block<L, R, Exact, E, MODE, DIAG>(A, s_hit[i], int(blockIdx.x) % S);
+                __syncthreads();  // shared neighbourhood tables are rewritten by the next block
+            }
+            __syncthreads();  // s_cnt / s_hit are rewritten by the next chunk
+        }
+        return;
+    }
     if (A.scan_span > 0) {
         // DisagBitmask sweep (sparse.cpp:369-380): every block is visited and
         // skipped unless its bit matches. A CTA per block would spend most of
@@ -444,6 +482,12 @@ constexpr int kSpProbeBlocks = 592;
 #define VOXL_BITMASK_SPAN 64
 #endif
 constexpr int kBitmaskSpan = VOXL_BITMASK_SPAN;  // blocks per CTA pair of the bitmask boundary sweep
+#ifndef VOXL_BITMASK_PAIRS
+#define VOXL_BITMASK_PAIRS 0
+#endif
+// bitmask boundary sweep: CTA pairs with balanced spans (0: one per SM in
+// D3Q19, fixed kBitmaskSpan spans in D3Q27; -1: always fixed spans)
+constexpr int kBitmaskPairs = VOXL_BITMASK_PAIRS;
 #ifndef VOXL_HEAVY_LOW_PRIO
 #define VOXL_HEAVY_LOW_PRIO 0
 #endif
@@ -475,7 +519,9 @@ struct SparseOps {
         constexpr int S = kSplit<E>;
         dim3 grid(nblocks * S);
         const dim3 block(E * E * E / S);
-        if (A.scan_span > 0) {  // bitmask sweep: one CTA pair per span of blocks
+        if (A.span_lo) {  // balanced bitmask sweep: span_pairs CTA pairs
+            grid = dim3(A.span_pairs * S);
+        } else if (A.scan_span > 0) {  // bitmask sweep: one CTA pair per span of blocks
             A.scan_blocks = nblocks;
             grid = dim3((nblocks + A.scan_span - 1) / A.scan_span * S);
         } else if constexpr (E == 8 && std::is_same_v<R, float>) {
@@ -507,7 +553,7 @@ struct SparseOps {
     }
 
     static void launch(int edge, SparseArgs<Q, R>& A, int mode, int nblocks, cudaStream_t st) {
-        NvtxRange r(mode == kHeavy ? (A.scan_span ? "voxl sparse boundary sweep" : "voxl sparse boundary")
+        NvtxRange r(mode == kHeavy ? (A.scan_span || A.span_lo ? "voxl sparse boundary sweep" : "voxl sparse boundary")
                                    : (A.bitmask ? "voxl sparse light sweep" : "voxl sparse light"));
         switch (edge) {
             case 4: launch_e<4>(A, mode, nblocks, st); break;
@@ -627,6 +673,26 @@ SparseEngine::SparseEngine(const SparseConfig& cfg, const std::uint8_t* active)
                              arr_.voxel_meta_index.size() * sizeof(std::int32_t), cudaMemcpyHostToDevice));
         VOXL_CUDA(cudaMalloc(&d_bitmask_, nb));
         VOXL_CUDA(cudaMemcpy(d_bitmask_, arr_.boundary_bitmask.data(), nb, cudaMemcpyHostToDevice));
+        // the boundary sweep's spans: pair p starts at the (p * n_b / pairs)-th
+        // boundary block, so every pair updates the same number of them and
+        // every block is tested by exactly one pair
+        const int pairs = kBitmaskPairs < 0 ? 0 : (kBitmaskPairs > 0 ? kBitmaskPairs : (q_ == 19 ? sm_count_ : 0));
+        std::int64_t n_b = 0;
+        for (std::size_t b = 0; b < nb; ++b) n_b += arr_.boundary_bitmask[b] ? 1 : 0;
+        if (pairs > 0 && n_b > 0) {
+            std::vector<int> lo(std::size_t(pairs) + 1, int(nb));
+            lo[0] = 0;
+            std::int64_t seen = 0;
+            int p = 1;
+            for (std::size_t b = 0; b < nb && p < pairs; ++b) {
+                if (!arr_.boundary_bitmask[b]) continue;
+                while (p < pairs && seen == (std::int64_t(p) * n_b + pairs - 1) / pairs) lo[std::size_t(p++)] = int(b);
+                ++seen;
+            }
+            bitmask_pairs_ = pairs;
+            VOXL_CUDA(cudaMalloc(&d_bitmask_spans_, lo.size() * sizeof(int)));
+            VOXL_CUDA(cudaMemcpy(d_bitmask_spans_, lo.data(), lo.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
     }
     VOXL_CUDA(cudaMalloc(&d_error_, sizeof(int)));
     const int big = INT_MAX;
@@ -644,6 +710,7 @@ SparseEngine::~SparseEngine() {
     cudaFree(d_full_);
     cudaFree(d_origins_);
     cudaFree(d_bitmask_);
+    cudaFree(d_bitmask_spans_);
     cudaFree(d_meta_index_);
     cudaFree(d_compact_meta_);
     cudaFree(d_naive_meta_);
@@ -785,11 +852,17 @@ void SparseEngine::launch(int /*which*/, cudaEvent_t* ev_b, cudaEvent_t* ev_l, c
                     VOXL_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
                 }
                 A.bitmask_want = 1;
-                A.scan_span = kBitmaskSpan;
+                if (d_bitmask_spans_) {  // one CTA pair per SM over balanced spans
+                    A.span_lo = d_bitmask_spans_;
+                    A.span_pairs = bitmask_pairs_;
+                } else {
+                    A.scan_span = kBitmaskSpan;
+                }
                 if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[0], hs));
                 Ops::launch(edge, A, kHeavy, nb, hs);
                 if (ev_b) VOXL_CUDA(cudaEventRecord(ev_b[1], hs));
                 A.scan_span = 0;
+                A.span_lo = nullptr;
                 A.bitmask_want = 0;
                 if (ev_l) VOXL_CUDA(cudaEventRecord(ev_l[0], ls));
                 Ops::launch(edge, A, kLight, nb, ls);

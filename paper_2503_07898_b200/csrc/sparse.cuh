@@ -94,6 +94,8 @@ private:
     std::uint8_t* d_full_ = nullptr;
     int* d_origins_ = nullptr;
     std::uint8_t* d_bitmask_ = nullptr;
+    int* d_bitmask_spans_ = nullptr;  // DisagBitmask boundary sweep: bitmask_pairs_ + 1 span starts
+    int bitmask_pairs_ = 0;
     std::int32_t* d_meta_index_ = nullptr;
     void* d_compact_meta_ = nullptr;
     void* d_naive_meta_ = nullptr;

@@ -51,6 +51,7 @@ def sparse(args):
                 "frac_of_8TBs": round(gbs / 8000, 4),
                 "boundary_kernel_ms": round(b_ms / args.steps, 4), "light_kernel_ms": round(l_ms / args.steps, 4),
                 "report": json.loads(e.report_json())}
+        line["lib"] = os.environ.get("VOXL_TAG", "")
         print(json.dumps(line), flush=True)
         e.close()
 
@@ -79,6 +80,7 @@ def multires(args):
                 "steps": args.steps, "ms_per_coarse_step": round(total / args.steps, 4), "MLUPS": round(mlups, 1),
                 "achieved_GBs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak(), 4),
                 "frac_of_8TBs": round(gbs / 8000, 4), "kernels_ms": detail, "distribution": e.distribution()}
+        line["lib"] = os.environ.get("VOXL_TAG", "")
         print(json.dumps(line), flush=True)
         e.close()
 
@@ -109,6 +111,7 @@ def dense(args):
                 "domain": [n] * 3, "bytes_per_lup": bpl, "steps": args.steps,
                 "ms_per_step": round(total / args.steps, 4), "MLUPS": round(mlups, 1), "achieved_GBs": round(gbs, 1),
                 "frac_of_measured_peak": round(gbs / peak(), 4), "frac_of_8TBs": round(gbs / 8000, 4)}
+        line["lib"] = os.environ.get("VOXL_TAG", "")
         print(json.dumps(line), flush=True)
         e.close()
 

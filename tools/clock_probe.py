@@ -22,7 +22,7 @@ from bench import ClockSampler  # noqa: E402
 
 
 def measure(name, step, ks=(1, 10, 50, 200), reps=3):
-    out = {"path": name}
+    out = {"path": name, "lib": os.environ.get("VOXL_TAG", "")}
     cs = ClockSampler(0)
     time.sleep(0.3)
     step(3)
@@ -46,18 +46,23 @@ def measure(name, step, ks=(1, 10, 50, 200), reps=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--only", default="", help="dense: the dense paths only")
+    ap.add_argument("--ks", default="1,10,50,200", help="batch lengths (dense and block-sparse)")
     a = ap.parse_args()
+    ks = tuple(int(x) for x in a.ks.split(","))
     n = a.n
     dom = (n, n, n)
     torch.cuda.init()
     e = V.DenseEngine(domain=dom, precision="fp32")
     e.set_equilibrium(1.0, (0.0, 0.0, 0.0))
-    measure("dense", e.step)
-    measure("dense_probe_n", e.step_probe_n)
+    measure("dense", e.step, ks=ks)
+    measure("dense_probe_n", e.step_probe_n, ks=ks)
     e.close()
+    if a.only == "dense":
+        return
     s = V.SparseEngine(dom, V.obstacle_mask(dom), block_edge=8, strategy="disag_mem", precision="fp32")
-    measure("sparse_disag_mem", s.step)
-    measure("sparse_disag_mem_probe_n", s.step_probe_n)
+    measure("sparse_disag_mem", s.step, ks=ks)
+    measure("sparse_disag_mem_probe_n", s.step_probe_n, ks=ks)
     s.close()
     m = V.MultiResEngine(dom, 3, fused=True, precision="fp32")
     measure("multires_fused", m.step, ks=(1, 5, 20, 50))

@@ -294,9 +294,12 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
             atomicMin(A.diag_bad, (canon << 5) | (unsigned long long)dg_bad);
         }
         const unsigned live_lanes = __ballot_sync(0xffffffffu, int(blockIdx.x * kBlock + threadIdx.x) < A.na);
-        const unsigned long long warp_id =
-            (((unsigned long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (kBlock / 32) +
-            (threadIdx.x >> 5);
+        // accumulator lane: any mapping gives the same (integer) sums; the
+        // SM id and the warp's slot in its CTA spread the warps resident at
+        // one time over the lanes in two instructions
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        const unsigned long long warp_id = smid * (kBlock / 32) + (threadIdx.x >> 5);
         if constexpr (std::is_same_v<P, float>) {
             diag_warp_commit_f32(A.diag_acc, warp_id, pm, pv, live_lanes);
         } else {

@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(R) != 4 ? 0
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         const unsigned long long warp_id = smid * (kBlock / 32) + (threadIdx.x >> 5);
         if constexpr (std::is_same_v<P, float>) {
-            diag_warp_commit_f32(A.diag_acc, warp_id, pm, pv, live_lanes);
+            diag_warp_commit_f32<true, false>(A.diag_acc, warp_id, pm, pv, live_lanes);
         } else {
             for (int o = 16; o > 0; o >>= 1) {
                 pm += __shfl_xor_sync(0xffffffffu, pm, o);

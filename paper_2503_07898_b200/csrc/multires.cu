@@ -13,6 +13,15 @@
 #include <cstring>
 #include <type_traits>
 
+// fused-probe commit of the block kernels (diag_ring.cuh): per-word zero
+// tests and the L2 evict_last policy kept unless measured otherwise
+#ifndef VOXL_BLOCK_DIAG_UNCOND
+#define VOXL_BLOCK_DIAG_UNCOND 0
+#endif
+#ifndef VOXL_BLOCK_DIAG_POLICY
+#define VOXL_BLOCK_DIAG_POLICY 1
+#endif
+
 namespace voxl_b200 {
 
 namespace {
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(E* E* E / kSplit<E>, (E == 8 && sizeof(R) == 4
         const unsigned live = __ballot_sync(0xffffffffu, active);
         const unsigned long long warp_id = (unsigned long long)blockIdx.x * (E * E * E / S / 32) + (tid >> 5);
         if constexpr (std::is_same_v<P, float>) {
-            diag_warp_commit_f32(A.diag_acc, warp_id, pm, pv, live);
+            diag_warp_commit_f32<VOXL_BLOCK_DIAG_UNCOND != 0, VOXL_BLOCK_DIAG_POLICY != 0>(A.diag_acc, warp_id, pm, pv, live);
         } else {
             for (int o = 16; o > 0; o >>= 1) {
                 pm += __shfl_xor_sync(0xffffffffu, pm, o);

@@ -24,6 +24,15 @@
 #include <cstring>
 #include <cstdlib>
 
+// fused-probe commit of the block kernels (diag_ring.cuh): per-word zero
+// tests and the L2 evict_last policy kept unless measured otherwise
+#ifndef VOXL_BLOCK_DIAG_UNCOND
+#define VOXL_BLOCK_DIAG_UNCOND 0
+#endif
+#ifndef VOXL_BLOCK_DIAG_POLICY
+#define VOXL_BLOCK_DIAG_POLICY 1
+#endif
+
 namespace voxl_b200 {
 
 namespace {
@@ -407,7 +416,7 @@ __device__ __forceinline__ void sparse_block(const SparseArgs<L::Q, R>& A, int b
         constexpr int kWarps = (BV / S + 31) / 32;
         const unsigned long long warp_id = ((unsigned long long)b * S + half) * kWarps + (tid >> 5);
         if constexpr (std::is_same_v<P, float>) {
-            diag_warp_commit_f32(A.diag_acc, warp_id, pm, pv, lanes);
+            diag_warp_commit_f32<VOXL_BLOCK_DIAG_UNCOND != 0, VOXL_BLOCK_DIAG_POLICY != 0>(A.diag_acc, warp_id, pm, pv, lanes);
         } else {
             for (int o = 16; o > 0; o >>= 1) {
                 pm += __shfl_xor_sync(0xffffffffu, pm, o);
